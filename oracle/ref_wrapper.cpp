@@ -1,0 +1,191 @@
+// ref_wrapper.cpp -- flat extern "C" view of the UNMODIFIED reference implementation.
+//
+// TEST INFRASTRUCTURE. oracle/Makefile compiles this file together with the reference's own
+// sources (/root/reference/proj/src/{geometry,parametric,batch,bench}.cpp, read in place, never
+// copied) into oracle/_ref/libref_voxline.so. It is used to (1) pin the C restatement in
+// oracle/voxline_oracle.c, (2) generate tests/golden fixtures, and (3) serve as the CPU
+// baseline ("kind": "reference") in bench.py. Exceptions are mapped to the codes in
+// oracle/voxline_oracle.h.
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "voxline/batch.hpp"
+#include "voxline/bench.hpp"
+#include "voxline/geometry.hpp"
+#include "voxline/parametric.hpp"
+
+namespace {
+
+voxline::Segment seg_at(const double* p) {
+    return {{p[0], p[1], p[2]}, {p[3], p[4], p[5]}};
+}
+
+std::vector<voxline::Segment> to_segments(const double* segs, int64_t n) {
+    std::vector<voxline::Segment> v;
+    v.reserve(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) v.push_back(seg_at(segs + 6 * i));
+    return v;
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 1;
+    } catch (const std::range_error&) {
+        return 2;
+    } catch (const std::out_of_range&) {
+        return 3;
+    } catch (const std::logic_error&) {
+        return 4;
+    } catch (...) {
+        return 5;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_round_point(const double p[3], int32_t out[3]) {
+    return guarded([&] {
+        const voxline::Voxel v = voxline::round_point({p[0], p[1], p[2]});
+        out[0] = v.x;
+        out[1] = v.y;
+        out[2] = v.z;
+    });
+}
+
+double ref_segment_length(const double seg[6]) { return voxline::segment_length(seg_at(seg)); }
+
+int ref_make_plan(const double seg[6], int64_t* n, double w[3]) {
+    return guarded([&] {
+        const voxline::ParametricPlan p = voxline::make_plan(seg_at(seg));
+        *n = p.step_count;
+        w[0] = p.step_vector.x;
+        w[1] = p.step_vector.y;
+        w[2] = p.step_vector.z;
+    });
+}
+
+int ref_voxelize_parametric(const double seg[6], int32_t* out, int64_t cap, int64_t* count) {
+    return guarded([&] {
+        const voxline::VoxelChain c = voxline::voxelize_parametric(seg_at(seg));
+        *count = static_cast<int64_t>(c.voxels.size());
+        if (out) {
+            if (*count > cap) throw std::logic_error("cap");
+            std::memcpy(out, c.voxels.data(), c.voxels.size() * sizeof(voxline::Voxel));
+        }
+    });
+}
+
+int ref_chain_length_bounds(const double seg[6], int64_t* lo, int64_t* hi) {
+    return guarded([&] {
+        const auto b = voxline::chain_length_bounds(seg_at(seg));
+        *lo = b.first;
+        *hi = b.second;
+    });
+}
+
+int ref_batch_preprocess(const double* segs, int64_t n, int64_t* steps, double* w3,
+                         int64_t* offsets, int64_t* max_steps, int64_t* capacity,
+                         int64_t* live, int64_t* redundant) {
+    return guarded([&] {
+        const voxline::BatchPlan plan = voxline::batch_preprocess(to_segments(segs, n));
+        for (int64_t i = 0; i < n; ++i) {
+            const voxline::SegmentPlan& sp = plan.per_segment[static_cast<std::size_t>(i)];
+            if (steps) steps[i] = sp.step_count;
+            if (w3) {
+                w3[3 * i + 0] = sp.step_vector.x;
+                w3[3 * i + 1] = sp.step_vector.y;
+                w3[3 * i + 2] = sp.step_vector.z;
+            }
+            if (offsets) offsets[i] = sp.output_offset;
+        }
+        *max_steps = plan.max_steps;
+        *capacity = plan.total_voxel_capacity;
+        const voxline::ItemCount c = voxline::effective_item_count(plan);
+        if (live) *live = c.live;
+        if (redundant) *redundant = c.redundant;
+    });
+}
+
+int ref_kernel_work_item(const double* segs, int64_t n, int64_t i, int64_t k, int32_t out[3],
+                         int* live) {
+    return guarded([&] {
+        const voxline::BatchPlan plan = voxline::batch_preprocess(to_segments(segs, n));
+        const std::optional<voxline::Voxel> v = voxline::kernel_work_item(plan, i, k);
+        *live = v.has_value() ? 1 : 0;
+        if (v) {
+            out[0] = v->x;
+            out[1] = v->y;
+            out[2] = v->z;
+        }
+    });
+}
+
+// run_batch flattened: chain i = out[chain_off[i] .. chain_off[i+1]). out may be NULL.
+// timing_ns[3] = {preprocess, kernel, assemble}.
+int ref_run_batch(const double* segs, int64_t n, int workers, int group_size, int32_t* out,
+                  int64_t out_cap, int64_t* chain_off, int64_t* total, int64_t* timing_ns) {
+    return guarded([&] {
+        const voxline::BatchResult r =
+            voxline::run_batch(to_segments(segs, n), {group_size, workers});
+        int64_t acc = 0;
+        for (std::size_t i = 0; i < r.chains.size(); ++i) {
+            if (chain_off) chain_off[i] = acc;
+            const auto& vox = r.chains[i].voxels;
+            if (out) {
+                if (acc + static_cast<int64_t>(vox.size()) > out_cap) throw std::logic_error("cap");
+                std::memcpy(out + 3 * acc, vox.data(), vox.size() * sizeof(voxline::Voxel));
+            }
+            acc += static_cast<int64_t>(vox.size());
+        }
+        if (chain_off) chain_off[r.chains.size()] = acc;
+        *total = r.total_voxels;
+        if (timing_ns) {
+            timing_ns[0] = r.timing.preprocess_ns;
+            timing_ns[1] = r.timing.kernel_ns;
+            timing_ns[2] = r.timing.assemble_ns;
+        }
+    });
+}
+
+int ref_gen_segment_of_length(int64_t target, uint64_t seed, double out[6]) {
+    return guarded([&] {
+        const voxline::Segment s = voxline::gen_segment_of_length(target, seed);
+        const double v[6] = {s.start.x, s.start.y, s.start.z, s.end.x, s.end.y, s.end.z};
+        std::memcpy(out, v, sizeof(v));
+    });
+}
+
+int ref_gen_arbitrary_batch(int64_t total, int64_t count, uint64_t seed, double* out) {
+    return guarded([&] {
+        const std::vector<voxline::Segment> segs =
+            voxline::gen_arbitrary_batch(total, count, seed);
+        for (std::size_t i = 0; i < segs.size(); ++i) {
+            const voxline::Segment& s = segs[i];
+            const double v[6] = {s.start.x, s.start.y, s.start.z, s.end.x, s.end.y, s.end.z};
+            std::memcpy(out + 6 * i, v, sizeof(v));
+        }
+    });
+}
+
+uint64_t ref_splitmix_next(uint64_t* state) {
+    voxline::SplitMix64 r(*state);
+    const uint64_t v = r.next();
+    *state = r.state;
+    return v;
+}
+
+double ref_compute_mvps(int64_t total, double ms, int* err) {
+    double v = 0.0;
+    *err = guarded([&] { v = voxline::compute_mvps(total, ms); });
+    return v;
+}
+
+}  // extern "C"

@@ -1,0 +1,532 @@
+/*
+ * voxline_oracle.c -- CPU restatement of the reference hot path.
+ *
+ * TEST INFRASTRUCTURE: the parity checker, never the product. See voxline_oracle.h for who may
+ * load it and how it is pinned (golden vectors + the reference compiled unmodified in
+ * oracle/_ref).  Compiled with -O2 -ffp-contract=off and no -march, matching the reference's
+ * canonical FMA-free Release build (proj/CMakeLists.txt:8-10).
+ *
+ * Every function cites the reference file:line it restates (paths relative to
+ * /root/reference/proj).
+ */
+#include "voxline_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <pthread.h>
+#include <unistd.h>
+
+/* ------------------------------------------------------------------ SplitMix64 */
+/* include/voxline/bench.hpp:25-30 */
+static inline uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+uint64_t vo_splitmix_next(uint64_t* state) {
+    *state += 0x9e3779b97f4a7c15ULL;
+    return mix64(*state);
+}
+
+/* The j-th output (0-based) of SplitMix64(seed): state after j+1 increments. */
+uint64_t vo_splitmix_draw(uint64_t seed, uint64_t j) {
+    return mix64(seed + (j + 1) * 0x9e3779b97f4a7c15ULL);
+}
+
+/* include/voxline/bench.hpp:33 */
+double vo_uniform01(uint64_t* state) {
+    return (double)(vo_splitmix_next(state) >> 11) * 0x1.0p-53;
+}
+
+/* include/voxline/bench.hpp:36 */
+double vo_uniform(uint64_t* state, double lo, double hi) {
+    return lo + (hi - lo) * vo_uniform01(state);
+}
+
+/* -------------------------------------------------------------------- geometry */
+/* src/geometry.cpp:8-11 (d = E - S per component, include/voxline/geometry.hpp:68-70) */
+double vo_segment_length(const double seg[6]) {
+    const double dx = seg[3] - seg[0], dy = seg[4] - seg[1], dz = seg[5] - seg[2];
+    return sqrt(dx * dx + dy * dy + dz * dz);
+}
+
+/* src/geometry.cpp:15-28: llround (ties away from zero), non-finite / outside int32 -> range */
+static inline int round_component(double c, int32_t* out) {
+    if (!isfinite(c)) return VO_RANGE_ERROR;
+    const long long r = llround(c);
+    if (r < INT32_MIN || r > INT32_MAX) return VO_RANGE_ERROR;
+    *out = (int32_t)r;
+    return VO_OK;
+}
+
+/* src/geometry.cpp:32-34 (x, then y, then z) */
+int vo_round_point(const double p[3], int32_t out[3]) {
+    for (int a = 0; a < 3; ++a) {
+        const int e = round_component(p[a], &out[a]);
+        if (e) return e;
+    }
+    return VO_OK;
+}
+
+/* ------------------------------------------------------------------ parametric */
+/* src/parametric.cpp:8-26 */
+int vo_make_plan(const double seg[6], int64_t* n_out, double w[3]) {
+    int32_t vs[3], ve[3];
+    int e = vo_round_point(seg, vs);
+    if (e) return e;
+    e = vo_round_point(seg + 3, ve);
+    if (e) return e;
+    if (vs[0] == ve[0] && vs[1] == ve[1] && vs[2] == ve[2]) {
+        *n_out = 0;
+        w[0] = w[1] = w[2] = 0.0;
+        return VO_OK;
+    }
+    const double dx = seg[3] - seg[0], dy = seg[4] - seg[1], dz = seg[5] - seg[2];
+    const double len = vo_segment_length(seg);
+    int64_t n = (int64_t)floor(len);
+    double extent = fabs(dx);
+    if (fabs(dy) > extent) extent = fabs(dy);
+    if (fabs(dz) > extent) extent = fabs(dz);
+    const int64_t ce = (int64_t)ceil(extent);
+    if (ce > n) n = ce;
+    if (n < 1) n = 1;
+    const double nd = (double)n;
+    *n_out = n;
+    w[0] = dx / nd;
+    w[1] = dy / nd;
+    w[2] = dz / nd;
+    return VO_OK;
+}
+
+/* include/voxline/parametric.hpp:41-48: k >= N -> E; else S + W*t per component (mul, add) */
+void vo_sample(const double seg[6], int64_t n, const double w[3], int64_t k, double out[3]) {
+    if (k >= n) {
+        out[0] = seg[3];
+        out[1] = seg[4];
+        out[2] = seg[5];
+        return;
+    }
+    const double t = (double)k;
+    out[0] = seg[0] + w[0] * t;
+    out[1] = seg[1] + w[1] * t;
+    out[2] = seg[2] + w[2] * t;
+}
+
+/* src/parametric.cpp:28-40: samples k = 0..N, round, drop consecutive duplicates */
+int vo_voxelize_parametric(const double seg[6], int32_t* out, int64_t cap, int64_t* count) {
+    int64_t n;
+    double w[3];
+    int e = vo_make_plan(seg, &n, w);
+    if (e) return e;
+    int64_t m = 0;
+    int32_t prev[3] = {0, 0, 0};
+    for (int64_t k = 0; k <= n; ++k) {
+        double g[3];
+        int32_t v[3];
+        vo_sample(seg, n, w, k, g);
+        e = vo_round_point(g, v);
+        if (e) return e;
+        if (m == 0 || v[0] != prev[0] || v[1] != prev[1] || v[2] != prev[2]) {
+            if (out) {
+                if (m >= cap) return VO_LOGIC_ERROR;
+                out[3 * m + 0] = v[0];
+                out[3 * m + 1] = v[1];
+                out[3 * m + 2] = v[2];
+            }
+            prev[0] = v[0];
+            prev[1] = v[1];
+            prev[2] = v[2];
+            ++m;
+        }
+    }
+    *count = m;
+    return VO_OK;
+}
+
+/* src/parametric.cpp:42-50 */
+int vo_chain_length_bounds(const double seg[6], int64_t* lo, int64_t* hi) {
+    int32_t vs[3], ve[3];
+    int e = vo_round_point(seg, vs);
+    if (e) return e;
+    e = vo_round_point(seg + 3, ve);
+    if (e) return e;
+    int64_t span = 0;
+    for (int a = 0; a < 3; ++a) {
+        int64_t s = (int64_t)ve[a] - (int64_t)vs[a];
+        if (s < 0) s = -s;
+        if (s > span) span = s;
+    }
+    int64_t n;
+    double w[3];
+    e = vo_make_plan(seg, &n, w);
+    if (e) return e;
+    *lo = span + 1;
+    *hi = n + 1;
+    return VO_OK;
+}
+
+/* ----------------------------------------------------------------------- batch */
+/* src/batch.cpp:57-73 (serial; the first failing segment's error wins) */
+int vo_batch_preprocess(const double* segs, int64_t n, int64_t* steps, double* w3,
+                        int64_t* offsets, int64_t* max_steps, int64_t* capacity) {
+    if (n <= 0) return VO_INVALID_ARGUMENT;
+    int64_t off = 0, mx = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t s;
+        double w[3];
+        const int e = vo_make_plan(segs + 6 * i, &s, w);
+        if (e) return e;
+        if (steps) steps[i] = s;
+        if (w3) {
+            w3[3 * i + 0] = w[0];
+            w3[3 * i + 1] = w[1];
+            w3[3 * i + 2] = w[2];
+        }
+        if (offsets) offsets[i] = off;
+        if (s > mx) mx = s;
+        off += s + 1;
+    }
+    if (max_steps) *max_steps = mx;
+    if (capacity) *capacity = off;
+    return VO_OK;
+}
+
+/* src/batch.cpp:75-90 */
+int vo_kernel_work_item(const double* segs, int64_t n, const int64_t* steps, const double* w3,
+                        int64_t max_steps, int64_t i, int64_t k, int32_t out[3], int* live) {
+    if (i < 0 || i >= n || k < 0 || k > max_steps) return VO_OUT_OF_RANGE;
+    if (k > steps[i]) {
+        *live = 0;
+        return VO_OK;
+    }
+    double g[3];
+    vo_sample(segs + 6 * i, steps[i], w3 + 3 * i, k, g);
+    *live = 1;
+    return vo_round_point(g, out);
+}
+
+static int resolve_threads(int nthreads) {
+    if (nthreads > 0) return nthreads;
+    const long c = sysconf(_SC_NPROCESSORS_ONLN);
+    return c > 0 ? (int)c : 1;
+}
+
+/* Minimal pthread parallel-for: fn(ctx, i) for i in [0, n), chunks pulled from a shared cursor
+ * (the shape of the reference's parallel_over_segments, src/batch.cpp:23-53). */
+typedef void (*vo_body)(void* ctx, int64_t i);
+typedef struct {
+    int64_t n, chunk, cursor;
+    vo_body fn;
+    void* ctx;
+} vo_pool;
+
+static void* vo_worker(void* arg) {
+    vo_pool* p = (vo_pool*)arg;
+    for (;;) {
+        const int64_t b = __atomic_fetch_add(&p->cursor, p->chunk, __ATOMIC_RELAXED);
+        if (b >= p->n) return NULL;
+        const int64_t e = b + p->chunk < p->n ? b + p->chunk : p->n;
+        for (int64_t i = b; i < e; ++i) p->fn(p->ctx, i);
+    }
+}
+
+static void parallel_for(int64_t n, int nthreads, int64_t chunk, vo_body fn, void* ctx) {
+    vo_pool p = {n, chunk, 0, fn, ctx};
+    int nt = resolve_threads(nthreads);
+    if (nt > 256) nt = 256;
+    if ((int64_t)nt > (n + chunk - 1) / chunk) nt = (int)((n + chunk - 1) / chunk);
+    if (nt <= 1) {
+        vo_worker(&p);
+        return;
+    }
+    pthread_t th[256];
+    int started = 0;
+    for (int t = 0; t < nt; ++t) {
+        if (pthread_create(&th[t], NULL, vo_worker, &p) != 0) break;
+        ++started;
+    }
+    vo_worker(&p);
+    for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+}
+
+static void record_error(int64_t* first_bad, int* code, int64_t i, int e) {
+    /* keep the lowest failing index (serial semantics of src/batch.cpp:61-66) */
+    int64_t cur = __atomic_load_n(first_bad, __ATOMIC_RELAXED);
+    while (cur < 0 || i < cur) {
+        if (__atomic_compare_exchange_n(first_bad, &cur, i, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+            __atomic_store_n(code, e, __ATOMIC_RELAXED);
+            return;
+        }
+    }
+}
+
+/* Per-segment deduplicated chain length (src/batch.cpp:128-146 semantics). */
+typedef struct {
+    const double* segs;
+    int64_t* lengths;
+    int64_t first_bad;
+    int code;
+} lengths_ctx;
+
+static void lengths_body(void* vctx, int64_t i) {
+    lengths_ctx* c = (lengths_ctx*)vctx;
+    int64_t m = 0;
+    const int e = vo_voxelize_parametric(c->segs + 6 * i, NULL, 0, &m);
+    if (e) {
+        record_error(&c->first_bad, &c->code, i, e);
+        c->lengths[i] = -1;
+        return;
+    }
+    c->lengths[i] = m;
+}
+
+int vo_chain_lengths(const double* segs, int64_t n, int64_t* lengths, int nthreads) {
+    if (n <= 0) return VO_INVALID_ARGUMENT;
+    /* Preprocess-phase errors (bad endpoints) win over kernel-phase ones and the lowest
+     * segment index wins among them (src/batch.cpp:61-66 is a serial loop). */
+    int64_t dummy_n;
+    double dummy_w[3];
+    for (int64_t i = 0; i < n; ++i) {
+        const int e = vo_make_plan(segs + 6 * i, &dummy_n, dummy_w);
+        if (e) return e;
+    }
+    lengths_ctx c = {segs, lengths, -1, 0};
+    parallel_for(n, nthreads, 64, lengths_body, &c);
+    return c.first_bad >= 0 ? c.code : VO_OK;
+}
+
+typedef struct {
+    const double* segs;
+    int32_t* out;
+    const int64_t* off;
+} write_ctx;
+
+static void write_body(void* vctx, int64_t i) {
+    write_ctx* c = (write_ctx*)vctx;
+    int64_t m;
+    vo_voxelize_parametric(c->segs + 6 * i, c->out + 3 * c->off[i], c->off[i + 1] - c->off[i], &m);
+}
+
+/* src/batch.cpp:154-162 (run_batch = preprocess + kernel + assemble), flattened. */
+int vo_run_batch(const double* segs, int64_t n, int32_t* out, int64_t out_cap,
+                 int64_t* chain_off, int64_t* total, int nthreads) {
+    if (n <= 0) return VO_INVALID_ARGUMENT;
+    int64_t* len = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    if (!len) return VO_LOGIC_ERROR;
+    int e = vo_chain_lengths(segs, n, len, nthreads);
+    if (e) {
+        free(len);
+        return e;
+    }
+    int64_t acc = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (chain_off) chain_off[i] = acc;
+        acc += len[i];
+    }
+    if (chain_off) chain_off[n] = acc;
+    *total = acc;
+    free(len);
+    if (out) {
+        if (acc > out_cap || !chain_off) return VO_LOGIC_ERROR;
+        write_ctx c = {segs, out, chain_off};
+        parallel_for(n, nthreads, 64, write_body, &c);
+    }
+    return VO_OK;
+}
+
+typedef struct {
+    const double* segs;
+    uint64_t* bits;
+    int64_t V, z_lo, z_hi, outside;
+    int err;
+} bitmap_ctx;
+
+static void bitmap_body(void* vctx, int64_t i) {
+    bitmap_ctx* c = (bitmap_ctx*)vctx;
+    const double* seg = c->segs + 6 * i;
+    int64_t s;
+    double w[3];
+    const int e = vo_make_plan(seg, &s, w);
+    if (e) {
+        __atomic_store_n(&c->err, e, __ATOMIC_RELAXED);
+        return;
+    }
+    const int64_t V = c->V;
+    int64_t outside = 0;
+    for (int64_t k = 0; k <= s; ++k) {
+        double g[3];
+        int32_t v[3];
+        vo_sample(seg, s, w, k, g);
+        if (vo_round_point(g, v)) {
+            __atomic_store_n(&c->err, VO_RANGE_ERROR, __ATOMIC_RELAXED);
+            break;
+        }
+        if (v[0] < 0 || v[0] >= V || v[1] < 0 || v[1] >= V || v[2] < 0 || v[2] >= V) {
+            ++outside;
+            continue;
+        }
+        if (v[2] < c->z_lo || v[2] >= c->z_hi) continue;
+        const uint64_t b = (uint64_t)v[0] +
+                           (uint64_t)V * ((uint64_t)v[1] + (uint64_t)V * (uint64_t)(v[2] - c->z_lo));
+        __atomic_fetch_or(&c->bits[b >> 6], 1ULL << (b & 63), __ATOMIC_RELAXED);
+    }
+    if (outside) __atomic_fetch_add(&c->outside, outside, __ATOMIC_RELAXED);
+}
+
+int vo_bitmap(const double* segs, int64_t n, uint64_t* bits, int64_t V, int64_t z_lo,
+              int64_t z_hi, int64_t* outside, int nthreads) {
+    if (n <= 0) return VO_INVALID_ARGUMENT;
+    if (V <= 0 || z_lo < 0 || z_hi > V || z_lo > z_hi) return VO_INVALID_ARGUMENT;
+    bitmap_ctx c = {segs, bits, V, z_lo, z_hi, 0, 0};
+    parallel_for(n, nthreads, 64, bitmap_body, &c);
+    if (outside) *outside = c.outside;
+    return c.err;
+}
+
+/* ------------------------------------------------------------------ generators */
+/* src/bench.cpp:38-47: uniform direction on the unit sphere (Marsaglia) */
+static void sphere_direction(uint64_t* st, double d[3]) {
+    for (;;) {
+        const double u = vo_uniform(st, -1.0, 1.0);
+        const double v = vo_uniform(st, -1.0, 1.0);
+        const double s = u * u + v * v;
+        if (s >= 1.0 || s == 0.0) continue;
+        const double f = 2.0 * sqrt(1.0 - s);
+        d[0] = u * f;
+        d[1] = v * f;
+        d[2] = 1.0 - 2.0 * s;
+        return;
+    }
+}
+
+/* src/bench.cpp:62-83 */
+int vo_gen_segment_of_length(int64_t target, uint64_t seed, double out[6]) {
+    if (target < 1) return VO_INVALID_ARGUMENT;
+    uint64_t st = seed;
+    const double sx = vo_uniform(&st, -50.0, 50.0);
+    const double sy = vo_uniform(&st, -50.0, 50.0);
+    const double sz = vo_uniform(&st, -50.0, 50.0);
+    const double dist = (double)target + 0.5;
+    for (int attempt = 0; attempt < 10000; ++attempt) {
+        double d[3];
+        sphere_direction(&st, d);
+        const double seg[6] = {sx, sy, sz, sx + d[0] * dist, sy + d[1] * dist, sz + d[2] * dist};
+        int64_t n;
+        double w[3];
+        if (vo_make_plan(seg, &n, w) == VO_OK && n == target) {
+            memcpy(out, seg, sizeof(seg));
+            return VO_OK;
+        }
+    }
+    return VO_LOGIC_ERROR;
+}
+
+/* Volume-fitted variant (no reference counterpart; BASELINE configs 1,3,4,5). Direction as in
+ * src/bench.cpp:38-47 and the same exact-N retry rule as src/bench.cpp:73-80, but the start is
+ * drawn after the direction, per axis uniform in [1 + max(0,-d), (V-2) - max(0,d)), so that both
+ * endpoints (and every sample) round into [1, V-2]. */
+int vo_gen_segment_in_volume(int64_t target, uint64_t seed, int64_t V, double out[6]) {
+    if (target < 1) return VO_INVALID_ARGUMENT;
+    const double dist = (double)target + 0.5;
+    const double vmax = (double)(V - 2);
+    if (!(dist < (double)V - 3.0)) return VO_INVALID_ARGUMENT;
+    uint64_t st = seed;
+    for (int attempt = 0; attempt < 10000; ++attempt) {
+        double d[3], seg[6];
+        sphere_direction(&st, d);
+        for (int a = 0; a < 3; ++a) {
+            const double dd = d[a] * dist;
+            const double lo = 1.0 + (dd < 0.0 ? -dd : 0.0);
+            const double hi = vmax - (dd > 0.0 ? dd : 0.0);
+            seg[a] = vo_uniform(&st, lo, hi);
+            seg[3 + a] = seg[a] + dd;
+        }
+        int64_t n;
+        double w[3];
+        if (vo_make_plan(seg, &n, w) == VO_OK && n == target) {
+            memcpy(out, seg, sizeof(seg));
+            return VO_OK;
+        }
+    }
+    return VO_LOGIC_ERROR;
+}
+
+typedef struct {
+    int64_t len_fixed, len_max, V;
+    uint64_t seed;
+    double* out;
+    int err;
+} gen_ctx;
+
+static void gen_body(void* vctx, int64_t i) {
+    gen_ctx* c = (gen_ctx*)vctx;
+    int64_t L;
+    uint64_t s;
+    if (c->len_max > 0) {
+        L = 1 + (int64_t)(vo_splitmix_draw(c->seed, 2 * (uint64_t)i) % (uint64_t)c->len_max);
+        s = vo_splitmix_draw(c->seed, 2 * (uint64_t)i + 1);
+    } else {
+        L = c->len_fixed;
+        s = vo_splitmix_draw(c->seed, (uint64_t)i);
+    }
+    const int e = c->V > 0 ? vo_gen_segment_in_volume(L, s, c->V, c->out + 6 * i)
+                           : vo_gen_segment_of_length(L, s, c->out + 6 * i);
+    if (e) __atomic_store_n(&c->err, e, __ATOMIC_RELAXED);
+}
+
+int vo_gen_batch(int64_t n, int64_t len_fixed, int64_t len_max, int64_t V, uint64_t seed,
+                 double* out, int nthreads) {
+    if (n < 1) return VO_INVALID_ARGUMENT;
+    if (len_max <= 0 && len_fixed < 1) return VO_INVALID_ARGUMENT;
+    gen_ctx c = {len_fixed, len_max, V, seed, out, 0};
+    parallel_for(n, nthreads, 1024, gen_body, &c);
+    return c.err;
+}
+
+/* src/bench.cpp:85-136 */
+int vo_gen_arbitrary_batch(int64_t total, int64_t count, uint64_t seed, double* out) {
+    if (count < 1) return VO_INVALID_ARGUMENT;
+    if (total < count) return VO_INVALID_ARGUMENT;
+    uint64_t st = seed;
+    const double mean = (double)total / (double)count;
+    const double log_hi = log(fmax(2.0 * mean, 2.0));
+    double* raw = (double*)malloc(sizeof(double) * (size_t)count);
+    int64_t* len = (int64_t*)malloc(sizeof(int64_t) * (size_t)count);
+    if (!raw || !len) {
+        free(raw);
+        free(len);
+        return VO_LOGIC_ERROR;
+    }
+    double raw_sum = 0.0;
+    for (int64_t i = 0; i < count; ++i) {
+        raw[i] = exp(vo_uniform(&st, 0.0, log_hi));
+        raw_sum += raw[i];
+    }
+    const double scale = (double)total / raw_sum;
+    int64_t sum = 0;
+    for (int64_t i = 0; i < count; ++i) {
+        const long long r = llround(raw[i] * scale);
+        len[i] = r > 1 ? r : 1;
+        sum += len[i];
+    }
+    for (int64_t i = 0; sum < total; i = (i + 1) % count) {
+        ++len[i];
+        ++sum;
+    }
+    for (int64_t i = 0; sum > total; i = (i + 1) % count) {
+        if (len[i] > 1) {
+            --len[i];
+            --sum;
+        }
+    }
+    int err = VO_OK;
+    for (int64_t i = 0; i < count && !err; ++i) {
+        err = vo_gen_segment_of_length(len[i], vo_splitmix_next(&st), out + 6 * i);
+    }
+    free(raw);
+    free(len);
+    return err;
+}
