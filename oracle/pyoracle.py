@@ -18,6 +18,7 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+HASH_P = (0x9E3779B97F4A7C15, 0xC2B2AE3D27D4EB4F, 0x165667B19E3779F9)  # vo_chain_hashes
 ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libref_voxline.so")
 
@@ -85,6 +86,7 @@ class Oracle:
         L.vo_chain_lengths.argtypes = [_f64p, C.c_int64, _i64p, C.c_int]
         L.vo_bitmap.argtypes = [_f64p, C.c_int64, _u64p, C.c_int64, C.c_int64, C.c_int64, _i64p,
                                 C.c_int]
+        L.vo_chain_hashes.argtypes = [_f64p, C.c_int64, _u64p, _i64p, C.c_int]
         L.vo_gen_segment_of_length.argtypes = [C.c_int64, C.c_uint64, _f64p]
         L.vo_gen_segment_in_volume.argtypes = [C.c_int64, C.c_uint64, C.c_int64, _f64p]
         L.vo_gen_batch.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, _f64p,
@@ -174,6 +176,16 @@ class Oracle:
         _check(self.lib.vo_bitmap(_p(s, _f64p), s.shape[0], _p(words, _u64p), V, z_lo, z_hi,
                                   C.byref(outside), nthreads), "bitmap")
         return words, outside.value
+
+    def chain_hashes(self, segs, nthreads: int = 0):
+        """-> (uint64 hash per chain, int64 length per chain); see vo_chain_hashes."""
+        s = as_segments(segs)
+        n = s.shape[0]
+        h = np.zeros(max(n, 1), np.uint64)
+        ln = np.zeros(max(n, 1), np.int64)
+        _check(self.lib.vo_chain_hashes(_p(s, _f64p), n, _p(h, _u64p), _p(ln, _i64p), nthreads),
+               "chain_hashes")
+        return h[:n], ln[:n]
 
     # --- generators -----------------------------------------------------------------
     def gen_segment_of_length(self, target: int, seed: int) -> np.ndarray:

@@ -530,3 +530,62 @@ int vo_gen_arbitrary_batch(int64_t total, int64_t count, uint64_t seed, double* 
     free(len);
     return err;
 }
+
+/* ------------------------------------------------------------- full-size checking */
+/* Order-sensitive per-chain hash used to check multi-GB outputs without storing them:
+ * h_i = sum_j (x_j*P1 + y_j*P2 + z_j*P3) * (j + 1)  (mod 2^64), j = position in chain i. */
+#define VO_P1 0x9E3779B97F4A7C15ULL
+#define VO_P2 0xC2B2AE3D27D4EB4FULL
+#define VO_P3 0x165667B19E3779F9ULL
+
+typedef struct {
+    const double* segs;
+    uint64_t* hashes;
+    int64_t* lengths;
+    int64_t first_bad;
+    int code;
+} hash_ctx;
+
+static void hash_body(void* vctx, int64_t i) {
+    hash_ctx* c = (hash_ctx*)vctx;
+    const double* seg = c->segs + 6 * i;
+    int64_t n;
+    double w[3];
+    int e = vo_make_plan(seg, &n, w);
+    if (e) {
+        record_error(&c->first_bad, &c->code, i, e);
+        return;
+    }
+    uint64_t h = 0;
+    int64_t m = 0;
+    int32_t prev[3] = {0, 0, 0};
+    for (int64_t k = 0; k <= n; ++k) {
+        double g[3];
+        int32_t v[3];
+        vo_sample(seg, n, w, k, g);
+        e = vo_round_point(g, v);
+        if (e) {
+            record_error(&c->first_bad, &c->code, i, e);
+            return;
+        }
+        if (m == 0 || v[0] != prev[0] || v[1] != prev[1] || v[2] != prev[2]) {
+            const uint64_t t = (uint64_t)(int64_t)v[0] * VO_P1 + (uint64_t)(int64_t)v[1] * VO_P2 +
+                               (uint64_t)(int64_t)v[2] * VO_P3;
+            h += t * (uint64_t)(m + 1);
+            prev[0] = v[0];
+            prev[1] = v[1];
+            prev[2] = v[2];
+            ++m;
+        }
+    }
+    c->hashes[i] = h;
+    c->lengths[i] = m;
+}
+
+int vo_chain_hashes(const double* segs, int64_t n, uint64_t* hashes, int64_t* lengths,
+                    int nthreads) {
+    if (n <= 0) return VO_INVALID_ARGUMENT;
+    hash_ctx c = {segs, hashes, lengths, -1, 0};
+    parallel_for(n, nthreads, 64, hash_body, &c);
+    return c.first_bad >= 0 ? c.code : VO_OK;
+}

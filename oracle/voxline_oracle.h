@@ -61,6 +61,11 @@ int vo_chain_lengths(const double* segs, int64_t n, int64_t* lengths, int nthrea
 int vo_bitmap(const double* segs, int64_t n, uint64_t* bits, int64_t V, int64_t z_lo,
               int64_t z_hi, int64_t* outside, int nthreads);
 
+/* Per-chain order-sensitive hash + length (checks multi-GB GPU outputs without storing them):
+ * h_i = sum_j (x_j*P1 + y_j*P2 + z_j*P3) * (j+1) mod 2^64, constants in voxline_oracle.c. */
+int vo_chain_hashes(const double* segs, int64_t n, uint64_t* hashes, int64_t* lengths,
+                    int nthreads);
+
 /* Generators. vo_gen_segment_of_length follows src/bench.cpp:62-83 exactly.
  * vo_gen_segment_in_volume is the volume-fitted variant used by the BASELINE configs
  * (direction first, then start drawn so that both endpoints lie in [1, V-2]^3). */

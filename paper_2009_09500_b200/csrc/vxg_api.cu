@@ -1,0 +1,897 @@
+// vxg_api.cu -- host side of libvoxgpu.so: the C ABI declared in include/voxgpu.h.
+//
+// Owns contexts (device, stream, events, caching device allocator) and batches (device-resident
+// segments + plan == a voxline::BatchPlan). Every entry point validates arguments the way the
+// reference does before touching the GPU and maps failures onto the reference's exception
+// classes. There is no CPU fallback: every voxel is produced by a kernel in
+// vxg_kernels.cu; if no CUDA device is usable, vxg_create fails with VXG_CUDA_ERROR.
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "vxg_device.cuh"
+#include "vxg_internal.h"
+
+using vxg::Control;
+using vxg::SegRec;
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+int64_t ns_since(Clock::time_point a) {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - a).count();
+}
+
+// ---------------------------------------------------------------- caching device allocator
+// cudaMalloc/cudaFree of multi-GB buffers cost milliseconds and cudaFree synchronises the
+// device, so batches draw from a per-context cache (best fit, never shrinks unless an allocation
+// fails, in which case the cache is released and the allocation retried once).
+class DeviceCache {
+   public:
+    ~DeviceCache() { release(); }
+    void* get(size_t bytes) {
+        if (bytes == 0) bytes = 256;
+        bytes = (bytes + 255) & ~size_t(255);
+        std::lock_guard<std::mutex> g(mu_);
+        auto it = free_.lower_bound(bytes);
+        if (it != free_.end() && it->first <= bytes + bytes / 4 + (64u << 20)) {
+            void* p = it->second;
+            sizes_[p] = it->first;
+            free_.erase(it);
+            return p;
+        }
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            release_locked();
+            if (cudaMalloc(&p, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+        }
+        sizes_[p] = bytes;
+        return p;
+    }
+    void put(void* p) {
+        if (!p) return;
+        std::lock_guard<std::mutex> g(mu_);
+        auto it = sizes_.find(p);
+        if (it == sizes_.end()) return;
+        free_.emplace(it->second, p);
+        sizes_.erase(it);
+    }
+    void release() {
+        std::lock_guard<std::mutex> g(mu_);
+        release_locked();
+    }
+
+   private:
+    void release_locked() {
+        if (!free_.empty()) cudaDeviceSynchronize();
+        for (auto& kv : free_) cudaFree(kv.second);
+        free_.clear();
+    }
+    std::mutex mu_;
+    std::multimap<size_t, void*> free_;
+    std::map<void*, size_t> sizes_;
+};
+
+// error key: ((2^59 - 1 - seg) << 3) | kind; atomicMax keeps the lowest segment.
+constexpr long long kSegMax = (1ll << 59) - 1;
+
+}  // namespace
+
+struct vxg_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    int64_t err_seg = -1;
+    int64_t launches = 0;
+    int list_variant = 0;
+    DeviceCache cache;
+    Control* h_ctl = nullptr;  // pinned readback slot
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+
+    vxg_status fail(vxg_status s, int64_t seg, const char* fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        err_seg = seg;
+        return s;
+    }
+    vxg_status cuda_fail(cudaError_t e, const char* where) {
+        if (e == cudaErrorMemoryAllocation)
+            return fail(VXG_OUT_OF_MEMORY, -1, "%s: %s", where, cudaGetErrorString(e));
+        return fail(VXG_CUDA_ERROR, -1, "%s: %s", where, cudaGetErrorString(e));
+    }
+    void ok() {
+        err.clear();
+        err_seg = -1;
+    }
+};
+
+// A device buffer drawn from the context cache.
+struct DBuf {
+    vxg_context* ctx = nullptr;
+    void* p = nullptr;
+    size_t bytes = 0;
+    bool ensure(vxg_context* c, size_t b) {
+        if (p && bytes >= b) return true;
+        release();
+        ctx = c;
+        p = c->cache.get(b);
+        bytes = p ? b : 0;
+        return p != nullptr;
+    }
+    void release() {
+        if (p && ctx) ctx->cache.put(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    ~DBuf() { release(); }
+};
+
+struct vxg_batch {
+    vxg_context* ctx = nullptr;
+    int64_t n = 0;
+    const double* d_segs = nullptr;  // owned (segs) or borrowed device pointer
+    DBuf segs, rec, steps, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl, scratch;
+    int64_t max_steps = 0, capacity = 0;
+    float plan_ms = 0.f, emit_ms = 0.f, aux_ms = 0.f;  // plan kernel / emit kernel / tile index + clip
+    vxg_timing timing{0, 0, 0};
+};
+
+namespace {
+
+constexpr int kMaxCtlSlots = 4;
+
+vxg_status check_launch(vxg_context* ctx, const char* where) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return ctx->cuda_fail(e, where);
+    return VXG_OK;
+}
+
+// Read back a Control block (synchronises the stream) and convert a recorded error.
+vxg_status read_ctl(vxg_context* ctx, Control* d_ctl, Control& out, const char* phase) {
+    cudaError_t e = cudaMemcpyAsync(ctx->h_ctl, d_ctl, sizeof(Control), cudaMemcpyDeviceToHost,
+                                    ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, phase);
+    out = *ctx->h_ctl;
+    if (out.err_seg != 0) {
+        const long long key = out.err_seg;
+        const int kind = (int)(key & 7);
+        const long long seg = kSegMax - (key >> 3);
+        switch (kind) {
+            case VXG_RANGE_ERROR:
+                return ctx->fail(VXG_RANGE_ERROR, seg,
+                                 "round_point: coordinate outside the 32-bit lattice or "
+                                 "non-finite (segment %lld, %s)",
+                                 seg, phase);
+            case VXG_INVALID_ARGUMENT:
+                return ctx->fail(VXG_INVALID_ARGUMENT, seg, "%s: invalid argument (item %lld)",
+                                 phase, seg);
+            default:
+                return ctx->fail((vxg_status)kind, seg, "%s: logic error at segment %lld", phase,
+                                 seg);
+        }
+    }
+    return VXG_OK;
+}
+
+bool is_aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Pointer attributes: is `p` device-accessible memory?
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+vxg_status upload_segments(vxg_batch* b, const vxg_segment* segs, int64_t n, vxg_mem where) {
+    vxg_context* ctx = b->ctx;
+    const size_t bytes = sizeof(vxg_segment) * (size_t)n;
+    if (where == VXG_MEM_DEVICE && is_aligned16(segs)) {
+        b->d_segs = reinterpret_cast<const double*>(segs);
+        return VXG_OK;
+    }
+    if (!b->segs.ensure(ctx, bytes)) return ctx->fail(VXG_OUT_OF_MEMORY, -1, "segments: out of device memory");
+    const cudaError_t e =
+        cudaMemcpyAsync(b->segs.p, segs, bytes,
+                        where == VXG_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                        ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "segments upload");
+    b->d_segs = b->segs.as<double>();
+    return VXG_OK;
+}
+
+Control* ctl_slot(vxg_batch* b, int i) { return b->ctl.as<Control>() + i; }
+
+// Plan kernel + look-back scan (batch_preprocess).
+vxg_status run_plan(vxg_batch* b) {
+    vxg_context* ctx = b->ctx;
+    const int64_t n = b->n;
+    const int tiles = vxg::plan_tile_count(n);
+    if (!b->rec.ensure(ctx, sizeof(SegRec) * (size_t)n) ||
+        !b->steps.ensure(ctx, sizeof(long long) * (size_t)n) ||
+        !b->off.ensure(ctx, sizeof(long long) * (size_t)(n + 1)) ||
+        !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)tiles))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_preprocess: out of device memory");
+    cudaMemsetAsync(ctl_slot(b, 0), 0, sizeof(Control), ctx->stream);
+    cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)tiles, ctx->stream);
+    vxg::PlanArgs a{b->d_segs, n, b->rec.as<SegRec>(), b->steps.as<long long>(),
+                    b->off.as<long long>(), b->status.as<unsigned long long>(), ctl_slot(b, 0)};
+    cudaEventRecord(ctx->ev[0], ctx->stream);
+    vxg::launch_plan(a, ctx->stream);
+    ctx->launches++;
+    cudaEventRecord(ctx->ev[1], ctx->stream);
+    vxg_status s = check_launch(ctx, "plan_kernel");
+    if (s) return s;
+    Control c;
+    s = read_ctl(ctx, ctl_slot(b, 0), c, "batch_preprocess");
+    cudaEventElapsedTime(&b->plan_ms, ctx->ev[0], ctx->ev[1]);
+    if (s) return s;
+    b->max_steps = (int64_t)c.max_steps;
+    b->capacity = c.total;
+    return VXG_OK;
+}
+
+vxg_status new_batch(vxg_context* ctx, vxg_batch** out) {
+    vxg_batch* b = new (std::nothrow) vxg_batch();
+    if (!b) return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch: out of host memory");
+    b->ctx = ctx;
+    if (!b->ctl.ensure(ctx, sizeof(Control) * kMaxCtlSlots)) {
+        delete b;
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch: out of device memory");
+    }
+    *out = b;
+    return VXG_OK;
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Emit the voxel list into device buffers (out: >= out_cap voxels, chain: n+1).
+vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long long* d_chain,
+                            int64_t* total) {
+    vxg_context* ctx = b->ctx;
+    const int ts_log2 = vxg::list_tile_log2(ctx->list_variant);
+    const int64_t ntiles = ceil_div(b->capacity, 1ll << ts_log2);
+    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)ntiles) ||
+        !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)std::max<int64_t>(ntiles, vxg::plan_tile_count(b->n))))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
+    if ((reinterpret_cast<uintptr_t>(d_out) & 3u) != 0)
+        return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_voxelize: output must be 4-byte aligned");
+    cudaMemsetAsync(ctl_slot(b, 1), 0, sizeof(Control), ctx->stream);
+    cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)ntiles, ctx->stream);
+    cudaEventRecord(ctx->ev[2], ctx->stream);
+    vxg::launch_tile_index(b->off.as<long long>(), b->n, ts_log2, b->tile_seg.as<long long>(),
+                           ctx->stream);
+    cudaEventRecord(ctx->ev[3], ctx->stream);
+    vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->tile_seg.as<long long>(),
+                    b->n, b->capacity, ntiles, d_out, out_cap, d_chain,
+                    b->status.as<unsigned long long>(), ctl_slot(b, 1)};
+    cudaError_t e = vxg::launch_emit_list(a, ctx->list_variant, ctx->stream);
+    ctx->launches += 2;
+    cudaEventRecord(ctx->ev[4], ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "emit_list_kernel");
+    Control c;
+    vxg_status s = read_ctl(ctx, ctl_slot(b, 1), c, "batch_voxelize");
+    cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);
+    if (s) return s;
+    *total = c.total;
+    return VXG_OK;
+}
+
+// Clip every segment to [z_lo, z_hi): entries + offsets; returns entries/samples.
+vxg_status run_clip(vxg_batch* b, int64_t z_lo, int64_t z_hi, int64_t* n_entries,
+                    int64_t* samples) {
+    vxg_context* ctx = b->ctx;
+    const int64_t n = b->n;
+    const int tiles = vxg::clip_tile_count(n);
+    if (!b->entries.ensure(ctx, sizeof(vxg::ClipEntry) * (size_t)n) ||
+        !b->ent_off.ensure(ctx, sizeof(long long) * (size_t)(n + 1)) ||
+        !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)std::max<int64_t>(tiles, vxg::plan_tile_count(n))) ||
+        !b->status2.ensure(ctx, sizeof(unsigned long long) * (size_t)tiles))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "clip: out of device memory");
+    cudaMemsetAsync(ctl_slot(b, 2), 0, sizeof(Control), ctx->stream);
+    cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)tiles, ctx->stream);
+    cudaMemsetAsync(b->status2.p, 0, sizeof(unsigned long long) * (size_t)tiles, ctx->stream);
+    vxg::ClipArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), n, z_lo, z_hi,
+                    b->entries.as<vxg::ClipEntry>(), b->ent_off.as<long long>(),
+                    b->status.as<unsigned long long>(), b->status2.as<unsigned long long>(),
+                    ctl_slot(b, 2)};
+    vxg::launch_clip(a, ctx->stream);
+    ctx->launches++;
+    vxg_status s = check_launch(ctx, "clip_kernel");
+    if (s) return s;
+    Control c;
+    s = read_ctl(ctx, ctl_slot(b, 2), c, "clip");
+    if (s) return s;
+    *n_entries = c.n_entries;
+    *samples = c.total;
+    return VXG_OK;
+}
+
+vxg_status emit_bitmap_device(vxg_batch* b, unsigned long long* d_words, int64_t V, int64_t z_lo,
+                              int64_t z_hi, int clip, int64_t* outside) {
+    vxg_context* ctx = b->ctx;
+    const int ts_log2 = vxg::bitmap_tile_log2();
+    int64_t n_entries = b->n, samples = b->capacity;
+    const long long* off = b->off.as<long long>();
+    cudaEventRecord(ctx->ev[2], ctx->stream);
+    if (clip) {
+        vxg_status s = run_clip(b, z_lo, z_hi, &n_entries, &samples);
+        if (s) return s;
+        off = b->ent_off.as<long long>();
+    }
+    if (samples == 0) {
+        if (outside) *outside = 0;
+        b->emit_ms = b->aux_ms = 0.f;
+        return VXG_OK;
+    }
+    const int64_t ntiles = ceil_div(samples, 1ll << ts_log2);
+    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)ntiles))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
+    cudaMemsetAsync(ctl_slot(b, 3), 0, sizeof(Control), ctx->stream);
+    vxg::launch_tile_index(off, n_entries, ts_log2, b->tile_seg.as<long long>(), ctx->stream);
+    cudaEventRecord(ctx->ev[3], ctx->stream);
+    vxg::BitmapArgs a{b->rec.as<SegRec>(), clip ? b->entries.as<vxg::ClipEntry>() : nullptr, off,
+                      b->tile_seg.as<long long>(), n_entries, samples, ntiles, d_words, V, z_lo,
+                      z_hi, ctl_slot(b, 3)};
+    cudaError_t e = vxg::launch_emit_bitmap(a, clip != 0, ctx->stream);
+    ctx->launches += 2;
+    cudaEventRecord(ctx->ev[4], ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "emit_bitmap_kernel");
+    Control c;
+    vxg_status s = read_ctl(ctx, ctl_slot(b, 3), c, "bitmap");
+    cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);
+    if (s) return s;
+    if (outside) *outside = (int64_t)c.outside;
+    return VXG_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+VXG_API int vxg_abi_version(void) { return VXG_ABI_VERSION; }
+
+VXG_API vxg_status vxg_create(int device, vxg_context** out) {
+    if (!out) return VXG_INVALID_ARGUMENT;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return VXG_CUDA_ERROR;
+    }
+    if (device < 0 || device >= count) return VXG_INVALID_ARGUMENT;
+    if (cudaSetDevice(device) != cudaSuccess) return VXG_CUDA_ERROR;
+    vxg_context* ctx = new (std::nothrow) vxg_context();
+    if (!ctx) return VXG_OUT_OF_MEMORY;
+    ctx->device = device;
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ctl), sizeof(Control), cudaHostAllocDefault) !=
+            cudaSuccess ||
+        cudaEventCreate(&ctx->ev[0]) != cudaSuccess || cudaEventCreate(&ctx->ev[1]) != cudaSuccess ||
+        cudaEventCreate(&ctx->ev[2]) != cudaSuccess || cudaEventCreate(&ctx->ev[3]) != cudaSuccess ||
+        cudaEventCreate(&ctx->ev[4]) != cudaSuccess) {
+        delete ctx;
+        return VXG_CUDA_ERROR;
+    }
+    ctx->own_stream = true;
+    if (const char* v = std::getenv("VXG_LIST_VARIANT")) ctx->list_variant = std::atoi(v);
+    *out = ctx;
+    return VXG_OK;
+}
+
+VXG_API void vxg_destroy(vxg_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->cache.release();
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+    for (cudaEvent_t e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    delete ctx;
+}
+
+VXG_API vxg_status vxg_set_stream(vxg_context* ctx, void* stream) {
+    if (!ctx) return VXG_INVALID_ARGUMENT;
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (stream) {
+        ctx->stream = static_cast<cudaStream_t>(stream);
+        ctx->own_stream = false;
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return VXG_CUDA_ERROR;
+        ctx->own_stream = true;
+    }
+    return VXG_OK;
+}
+
+VXG_API void* vxg_get_stream(vxg_context* ctx) { return ctx ? ctx->stream : nullptr; }
+VXG_API const char* vxg_last_error(const vxg_context* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+VXG_API int64_t vxg_last_error_segment(const vxg_context* ctx) { return ctx ? ctx->err_seg : -1; }
+VXG_API int64_t vxg_launch_count(const vxg_context* ctx) { return ctx ? ctx->launches : 0; }
+
+VXG_API vxg_status vxg_synchronize(vxg_context* ctx) {
+    if (!ctx) return VXG_INVALID_ARGUMENT;
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? VXG_OK : ctx->cuda_fail(e, "synchronize");
+}
+
+VXG_API void* vxg_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+VXG_API void vxg_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+// ------------------------------------------------------------------------------- geometry
+VXG_API vxg_status vxg_round_points(vxg_context* ctx, const double* pts, int64_t n, int32_t* out) {
+    if (!ctx || n < 0 || (n && (!pts || !out))) return VXG_INVALID_ARGUMENT;
+    ctx->ok();
+    if (n == 0) return VXG_OK;
+    cudaSetDevice(ctx->device);
+    DBuf dp, dout, dctl;
+    if (!dp.ensure(ctx, 24 * (size_t)n) || !dout.ensure(ctx, 12 * (size_t)n) ||
+        !dctl.ensure(ctx, sizeof(Control)))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "round_point: out of device memory");
+    cudaMemcpyAsync(dp.p, pts, 24 * (size_t)n, cudaMemcpyHostToDevice, ctx->stream);
+    cudaMemsetAsync(dctl.p, 0, sizeof(Control), ctx->stream);
+    vxg::launch_round_points(dp.as<double>(), n, dout.as<int32_t>(), dctl.as<Control>(), ctx->stream);
+    ctx->launches++;
+    cudaMemcpyAsync(out, dout.p, 12 * (size_t)n, cudaMemcpyDeviceToHost, ctx->stream);
+    Control c;
+    return read_ctl(ctx, dctl.as<Control>(), c, "round_point");
+}
+
+VXG_API vxg_status vxg_segment_lengths(vxg_context* ctx, const vxg_segment* segs, int64_t n,
+                                       double* out) {
+    if (!ctx || n < 0 || (n && (!segs || !out))) return VXG_INVALID_ARGUMENT;
+    ctx->ok();
+    if (n == 0) return VXG_OK;
+    cudaSetDevice(ctx->device);
+    DBuf ds, dout;
+    if (!ds.ensure(ctx, 48 * (size_t)n) || !dout.ensure(ctx, 8 * (size_t)n))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "segment_length: out of device memory");
+    cudaMemcpyAsync(ds.p, segs, 48 * (size_t)n, cudaMemcpyHostToDevice, ctx->stream);
+    vxg::launch_segment_lengths(ds.as<double>(), n, dout.as<double>(), ctx->stream);
+    ctx->launches++;
+    cudaMemcpyAsync(out, dout.p, 8 * (size_t)n, cudaMemcpyDeviceToHost, ctx->stream);
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? VXG_OK : ctx->cuda_fail(e, "segment_length");
+}
+
+VXG_API vxg_status vxg_make_plans(vxg_context* ctx, const vxg_segment* segs, int64_t n,
+                                  int64_t* steps, double* w3) {
+    if (!ctx || n <= 0 || !segs) return ctx ? ctx->fail(VXG_INVALID_ARGUMENT, -1, "make_plan: no segments") : VXG_INVALID_ARGUMENT;
+    vxg_batch* b = nullptr;
+    vxg_status s = vxg_batch_create(ctx, segs, n, VXG_MEM_HOST, &b);
+    if (s) return s;
+    std::vector<vxg_segment_plan> plans((size_t)n);
+    s = vxg_batch_plans(b, plans.data());
+    vxg_batch_destroy(b);
+    if (s) return s;
+    for (int64_t i = 0; i < n; ++i) {
+        if (steps) steps[i] = plans[(size_t)i].step_count;
+        if (w3) {
+            w3[3 * i + 0] = plans[(size_t)i].wx;
+            w3[3 * i + 1] = plans[(size_t)i].wy;
+            w3[3 * i + 2] = plans[(size_t)i].wz;
+        }
+    }
+    return VXG_OK;
+}
+
+VXG_API vxg_status vxg_voxelize_parametric(vxg_context* ctx, const vxg_segment* seg,
+                                           vxg_voxel* out, int64_t cap, int64_t* count) {
+    if (!ctx || !seg || !count || cap < 0 || (cap > 0 && !out)) return VXG_INVALID_ARGUMENT;
+    vxg_batch* b = nullptr;
+    vxg_status s = vxg_batch_create(ctx, seg, 1, VXG_MEM_HOST, &b);
+    if (s) return s;
+    if (!b->out.ensure(ctx, 12 * (size_t)b->capacity) || !b->chain.ensure(ctx, 16)) {
+        vxg_batch_destroy(b);
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "voxelize_parametric: out of device memory");
+    }
+    int64_t total = 0;
+    s = emit_list_device(b, b->out.as<int32_t>(), b->capacity, b->chain.as<long long>(), &total);
+    if (!s) {
+        *count = total;
+        const int64_t ncopy = std::min(total, cap);
+        if (ncopy > 0) {
+            const cudaError_t e = cudaMemcpyAsync(out, b->out.p, 12 * (size_t)ncopy,
+                                                  cudaMemcpyDeviceToHost, ctx->stream);
+            if (e == cudaSuccess) cudaStreamSynchronize(ctx->stream);
+            else s = ctx->cuda_fail(e, "voxelize_parametric readback");
+        }
+        if (!s && total > cap)
+            s = ctx->fail(VXG_LOGIC_ERROR, 0, "voxelize_parametric: chain of %lld voxels exceeds cap %lld",
+                          (long long)total, (long long)cap);
+    }
+    vxg_batch_destroy(b);
+    return s;
+}
+
+VXG_API vxg_status vxg_chain_length_bounds(vxg_context* ctx, const vxg_segment* seg, int64_t* lo,
+                                           int64_t* hi) {
+    if (!ctx || !seg || !lo || !hi) return VXG_INVALID_ARGUMENT;
+    // rounded endpoints and the plan both come from the GPU (src/parametric.cpp:42-50)
+    const double pts[6] = {seg->sx, seg->sy, seg->sz, seg->ex, seg->ey, seg->ez};
+    int32_t v[6];
+    vxg_status s = vxg_round_points(ctx, pts, 2, v);
+    if (s) return s;
+    int64_t n = 0;
+    s = vxg_make_plans(ctx, seg, 1, &n, nullptr);
+    if (s) return s;
+    int64_t span = 0;
+    for (int a = 0; a < 3; ++a) span = std::max<int64_t>(span, std::llabs((int64_t)v[3 + a] - v[a]));
+    *lo = span + 1;
+    *hi = n + 1;
+    return VXG_OK;
+}
+
+// ------------------------------------------------------------------------------- batch
+VXG_API vxg_status vxg_batch_create(vxg_context* ctx, const vxg_segment* segs, int64_t n,
+                                    vxg_mem where, vxg_batch** out) {
+    if (!ctx || !out) return VXG_INVALID_ARGUMENT;
+    ctx->ok();
+    *out = nullptr;
+    if (n <= 0) return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_preprocess: empty segment list");
+    if (!segs) return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_preprocess: null segments");
+    cudaSetDevice(ctx->device);
+    vxg_batch* b = nullptr;
+    vxg_status s = new_batch(ctx, &b);
+    if (s) return s;
+    b->n = n;
+    const auto t0 = Clock::now();
+    s = upload_segments(b, segs, n, where);
+    if (!s) s = run_plan(b);
+    b->timing.preprocess_ns = ns_since(t0);
+    if (s) {
+        delete b;
+        return s;
+    }
+    *out = b;
+    return VXG_OK;
+}
+
+VXG_API vxg_status vxg_batch_from_plan(vxg_context* ctx, const vxg_segment* segs,
+                                       const vxg_segment_plan* plans, int64_t n,
+                                       int64_t max_steps, int64_t capacity, vxg_batch** out) {
+    if (!ctx || !out) return VXG_INVALID_ARGUMENT;
+    ctx->ok();
+    *out = nullptr;
+    // src/batch.cpp:98-105
+    if (n <= 0 || !segs || !plans) return ctx->fail(VXG_LOGIC_ERROR, -1, "batch_voxelize: malformed plan");
+    const vxg_segment_plan& last = plans[n - 1];
+    if (last.output_offset + last.step_count + 1 != capacity)
+        return ctx->fail(VXG_LOGIC_ERROR, -1, "batch_voxelize: plan capacity mismatch");
+    int64_t mx = 0;
+    for (int64_t i = 0; i < n; ++i) mx = std::max(mx, plans[i].step_count);
+    if (mx != max_steps)
+        return ctx->fail(VXG_LOGIC_ERROR, -1, "batch_voxelize: plan max_steps mismatch");
+    cudaSetDevice(ctx->device);
+    vxg_batch* b = nullptr;
+    vxg_status s = new_batch(ctx, &b);
+    if (s) return s;
+    b->n = n;
+    DBuf dplans;
+    s = upload_segments(b, segs, n, VXG_MEM_HOST);
+    if (!s && (!b->rec.ensure(ctx, sizeof(SegRec) * (size_t)n) ||
+               !b->steps.ensure(ctx, 8 * (size_t)n) || !b->off.ensure(ctx, 8 * (size_t)(n + 1)) ||
+               !dplans.ensure(ctx, sizeof(vxg_segment_plan) * (size_t)n)))
+        s = ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
+    if (!s) {
+        cudaMemcpyAsync(dplans.p, plans, sizeof(vxg_segment_plan) * (size_t)n, cudaMemcpyHostToDevice,
+                        ctx->stream);
+        cudaMemcpyAsync(b->off.as<long long>() + n, &capacity, 8, cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemsetAsync(ctl_slot(b, 0), 0, sizeof(Control), ctx->stream);
+        vxg::launch_pack_plan(b->d_segs, dplans.as<vxg_segment_plan>(), n, b->rec.as<SegRec>(),
+                              b->steps.as<long long>(), b->off.as<long long>(), ctl_slot(b, 0),
+                              ctx->stream);
+        ctx->launches++;
+        Control c;
+        s = read_ctl(ctx, ctl_slot(b, 0), c, "batch_voxelize");
+        if (s == VXG_LOGIC_ERROR) ctx->err = "batch_voxelize: malformed plan (offsets are not the prefix sum of N_i + 1)";
+    }
+    if (s) {
+        delete b;
+        return s;
+    }
+    b->max_steps = max_steps;
+    b->capacity = capacity;
+    *out = b;
+    return VXG_OK;
+}
+
+VXG_API void vxg_batch_destroy(vxg_batch* b) {
+    if (!b) return;
+    cudaStreamSynchronize(b->ctx->stream);
+    delete b;
+}
+
+VXG_API vxg_status vxg_batch_info(const vxg_batch* b, int64_t* n, int64_t* max_steps,
+                                  int64_t* capacity) {
+    if (!b) return VXG_INVALID_ARGUMENT;
+    if (n) *n = b->n;
+    if (max_steps) *max_steps = b->max_steps;
+    if (capacity) *capacity = b->capacity;
+    return VXG_OK;
+}
+
+VXG_API vxg_status vxg_batch_plans(vxg_batch* b, vxg_segment_plan* out) {
+    if (!b || !out) return VXG_INVALID_ARGUMENT;
+    vxg_context* ctx = b->ctx;
+    cudaSetDevice(ctx->device);
+    DBuf d;
+    if (!d.ensure(ctx, sizeof(vxg_segment_plan) * (size_t)b->n))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "plans: out of device memory");
+    vxg::launch_export_plans(b->rec.as<SegRec>(), b->off.as<long long>(), b->n,
+                             d.as<vxg_segment_plan>(), ctx->stream);
+    ctx->launches++;
+    cudaError_t e = cudaMemcpyAsync(out, d.p, sizeof(vxg_segment_plan) * (size_t)b->n,
+                                    cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    return e == cudaSuccess ? VXG_OK : ctx->cuda_fail(e, "plans readback");
+}
+
+VXG_API vxg_status vxg_batch_item_count(const vxg_batch* b, int64_t* live, int64_t* redundant) {
+    if (!b) return VXG_INVALID_ARGUMENT;
+    if (live) *live = b->capacity;
+    if (redundant) *redundant = b->n * (b->max_steps + 1) - b->capacity;
+    return VXG_OK;
+}
+
+VXG_API vxg_status vxg_batch_work_item(vxg_batch* b, int64_t i, int64_t k, int32_t out[3],
+                                       int* live) {
+    if (!b || !out || !live) return VXG_INVALID_ARGUMENT;
+    vxg_context* ctx = b->ctx;
+    ctx->ok();
+    if (i < 0 || i >= b->n || k < 0 || k > b->max_steps)
+        return ctx->fail(VXG_OUT_OF_RANGE, -1,
+                         "kernel_work_item: item index outside the %lld x %lld grid",
+                         (long long)b->n, (long long)(b->max_steps + 1));
+    cudaSetDevice(ctx->device);
+    long long off2[2];
+    cudaError_t e = cudaMemcpyAsync(off2, b->off.as<long long>() + i, 16, cudaMemcpyDeviceToHost,
+                                    ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "kernel_work_item");
+    if (k > off2[1] - off2[0] - 1) {
+        *live = 0;
+        return VXG_OK;
+    }
+    DBuf d;
+    if (!d.ensure(ctx, 16)) return ctx->fail(VXG_OUT_OF_MEMORY, -1, "kernel_work_item: oom");
+    cudaMemsetAsync(ctl_slot(b, 3), 0, sizeof(Control), ctx->stream);
+    vxg::launch_work_item(b->rec.as<SegRec>(), b->off.as<long long>(), i, k, d.as<int32_t>(),
+                          ctl_slot(b, 3), ctx->stream);
+    ctx->launches++;
+    cudaMemcpyAsync(out, d.p, 12, cudaMemcpyDeviceToHost, ctx->stream);
+    Control c;
+    const vxg_status s = read_ctl(ctx, ctl_slot(b, 3), c, "kernel_work_item");
+    if (s) return s;
+    *live = 1;
+    return VXG_OK;
+}
+
+VXG_API vxg_status vxg_batch_emit_list(vxg_batch* b, vxg_voxel* out, int64_t out_cap,
+                                       int64_t* chain_off, int64_t* total, vxg_mem where) {
+    if (!b || !total || (!out && out_cap > 0) || !chain_off) return VXG_INVALID_ARGUMENT;
+    vxg_context* ctx = b->ctx;
+    ctx->ok();
+    cudaSetDevice(ctx->device);
+    const auto t0 = Clock::now();
+    vxg_status s;
+    if (where == VXG_MEM_DEVICE) {
+        s = emit_list_device(b, reinterpret_cast<int32_t*>(out), out_cap,
+                             reinterpret_cast<long long*>(chain_off), total);
+        b->timing.kernel_ns = ns_since(t0);
+        b->timing.assemble_ns = 0;
+        return s;
+    }
+    if (!b->out.ensure(ctx, 12 * (size_t)std::max<int64_t>(b->capacity, 1)) ||
+        !b->chain.ensure(ctx, 8 * (size_t)(b->n + 1)))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
+    s = emit_list_device(b, b->out.as<int32_t>(), b->capacity, b->chain.as<long long>(), total);
+    b->timing.kernel_ns = ns_since(t0);
+    if (s) return s;
+    if (*total > out_cap)
+        return ctx->fail(VXG_LOGIC_ERROR, -1, "batch_voxelize: %lld voxels exceed the output capacity %lld",
+                         (long long)*total, (long long)out_cap);
+    const auto t1 = Clock::now();
+    cudaError_t e = cudaMemcpyAsync(out, b->out.p, 12 * (size_t)*total, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(chain_off, b->chain.p, 8 * (size_t)(b->n + 1), cudaMemcpyDeviceToHost,
+                            ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    b->timing.assemble_ns = ns_since(t1);
+    return e == cudaSuccess ? VXG_OK : ctx->cuda_fail(e, "batch_voxelize readback");
+}
+
+VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t V, int64_t z_lo,
+                                         int64_t z_hi, int clip, int64_t* outside, vxg_mem where) {
+    if (!b || !words) return VXG_INVALID_ARGUMENT;
+    vxg_context* ctx = b->ctx;
+    ctx->ok();
+    if (V <= 0 || V > (1ll << 21) || z_lo < 0 || z_hi > V || z_lo > z_hi)
+        return ctx->fail(VXG_INVALID_ARGUMENT, -1, "bitmap: invalid volume / slab");
+    cudaSetDevice(ctx->device);
+    const size_t nwords = (size_t)((V * V * (z_hi - z_lo) + 63) / 64);
+    const auto t0 = Clock::now();
+    if (where == VXG_MEM_DEVICE) {
+        const vxg_status s = emit_bitmap_device(b, reinterpret_cast<unsigned long long*>(words), V,
+                                                z_lo, z_hi, clip, outside);
+        b->timing.kernel_ns = ns_since(t0);
+        return s;
+    }
+    DBuf d;
+    if (!d.ensure(ctx, 8 * std::max<size_t>(nwords, 1)))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
+    cudaMemcpyAsync(d.p, words, 8 * nwords, cudaMemcpyHostToDevice, ctx->stream);
+    vxg_status s = emit_bitmap_device(b, d.as<unsigned long long>(), V, z_lo, z_hi, clip, outside);
+    b->timing.kernel_ns = ns_since(t0);
+    if (s) return s;
+    const auto t1 = Clock::now();
+    cudaError_t e = cudaMemcpyAsync(words, d.p, 8 * nwords, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    b->timing.assemble_ns = ns_since(t1);
+    return e == cudaSuccess ? VXG_OK : ctx->cuda_fail(e, "bitmap readback");
+}
+
+VXG_API vxg_status vxg_batch_slab_samples(vxg_batch* b, int64_t z_lo, int64_t z_hi,
+                                          int64_t* samples) {
+    if (!b || !samples) return VXG_INVALID_ARGUMENT;
+    b->ctx->ok();
+    cudaSetDevice(b->ctx->device);
+    int64_t ne = 0;
+    return run_clip(b, z_lo, z_hi, &ne, samples);
+}
+
+VXG_API vxg_status vxg_batch_timing(const vxg_batch* b, vxg_timing* t) {
+    if (!b || !t) return VXG_INVALID_ARGUMENT;
+    t->preprocess_ns = (int64_t)((double)b->plan_ms * 1e6);
+    t->kernel_ns = (int64_t)((double)b->emit_ms * 1e6);
+    t->assemble_ns = (int64_t)((double)b->aux_ms * 1e6);
+    return VXG_OK;
+}
+
+VXG_API vxg_status vxg_run_batch(vxg_context* ctx, const vxg_segment* segs, int64_t n,
+                                 vxg_voxel* out, int64_t out_cap, int64_t* chain_off,
+                                 int64_t* total, vxg_timing* timing) {
+    if (!ctx) return VXG_INVALID_ARGUMENT;
+    vxg_batch* b = nullptr;
+    vxg_status s = vxg_batch_create(ctx, segs, n, VXG_MEM_HOST, &b);
+    if (s) return s;
+    s = vxg_batch_emit_list(b, out, out_cap, chain_off, total, VXG_MEM_HOST);
+    if (timing) *timing = b->timing;
+    vxg_batch_destroy(b);
+    return s;
+}
+
+// ------------------------------------------------------------------------------- generators
+VXG_API vxg_status vxg_gen_segments(vxg_context* ctx, int64_t n, const int64_t* lens,
+                                    const uint64_t* seeds, int64_t len_fixed, int64_t len_max,
+                                    int64_t V, uint64_t seed, vxg_segment* out, vxg_mem where) {
+    if (!ctx || !out) return VXG_INVALID_ARGUMENT;
+    ctx->ok();
+    if (n < 1) return ctx->fail(VXG_INVALID_ARGUMENT, -1, "gen: need >= 1 segment");
+    if (!lens && len_max <= 0 && len_fixed < 1)
+        return ctx->fail(VXG_INVALID_ARGUMENT, -1, "gen_segment_of_length: target must be >= 1");
+    cudaSetDevice(ctx->device);
+    DBuf dout, dl, ds, dctl;
+    double* d_out = reinterpret_cast<double*>(out);
+    if (where == VXG_MEM_HOST) {
+        if (!dout.ensure(ctx, 48 * (size_t)n)) return ctx->fail(VXG_OUT_OF_MEMORY, -1, "gen: oom");
+        d_out = dout.as<double>();
+    }
+    const long long* d_lens = reinterpret_cast<const long long*>(lens);
+    const unsigned long long* d_seeds = reinterpret_cast<const unsigned long long*>(seeds);
+    if (lens && where == VXG_MEM_HOST) {
+        if (!dl.ensure(ctx, 8 * (size_t)n) || !ds.ensure(ctx, 8 * (size_t)n))
+            return ctx->fail(VXG_OUT_OF_MEMORY, -1, "gen: oom");
+        cudaMemcpyAsync(dl.p, lens, 8 * (size_t)n, cudaMemcpyHostToDevice, ctx->stream);
+        cudaMemcpyAsync(ds.p, seeds, 8 * (size_t)n, cudaMemcpyHostToDevice, ctx->stream);
+        d_lens = dl.as<long long>();
+        d_seeds = ds.as<unsigned long long>();
+    }
+    if (!dctl.ensure(ctx, sizeof(Control))) return ctx->fail(VXG_OUT_OF_MEMORY, -1, "gen: oom");
+    cudaMemsetAsync(dctl.p, 0, sizeof(Control), ctx->stream);
+    vxg::GenArgs a{n, d_lens, d_seeds, len_fixed, len_max, V, seed, d_out, dctl.as<Control>()};
+    vxg::launch_gen(a, ctx->stream);
+    ctx->launches++;
+    if (where == VXG_MEM_HOST)
+        cudaMemcpyAsync(out, d_out, 48 * (size_t)n, cudaMemcpyDeviceToHost, ctx->stream);
+    Control c;
+    vxg_status s = read_ctl(ctx, dctl.as<Control>(), c, "gen_segments");
+    if (s == VXG_LOGIC_ERROR) ctx->err = "gen_segment_of_length: direction sampling failed";
+    if (s == VXG_INVALID_ARGUMENT) ctx->err = "gen_segment_of_length: target must be >= 1 (and fit the volume)";
+    return s;
+}
+
+VXG_API vxg_status vxg_gen_arbitrary_batch(vxg_context* ctx, int64_t total, int64_t count,
+                                           uint64_t seed, vxg_segment* out) {
+    if (!ctx || !out) return VXG_INVALID_ARGUMENT;
+    ctx->ok();
+    // src/bench.cpp:85-136: length planning on the host (glibc exp/log, as the reference), the
+    // segments themselves on the GPU.
+    if (count < 1) return ctx->fail(VXG_INVALID_ARGUMENT, -1, "gen_arbitrary_batch: need >= 1 segment");
+    if (total < count)
+        return ctx->fail(VXG_INVALID_ARGUMENT, -1,
+                         "gen_arbitrary_batch: target %lld is infeasible for %lld segments of length >= 1",
+                         (long long)total, (long long)count);
+    uint64_t st = seed;
+    auto next = [&]() {
+        st += vxg::kGamma;
+        return vxg::mix64(st);
+    };
+    auto uniform = [&](double lo, double hi) {
+        volatile double u = (double)(next() >> 11) * 0x1.0p-53;
+        volatile double span = hi - lo;
+        volatile double prod = span * u;
+        return lo + prod;
+    };
+    const double mean = (double)total / (double)count;
+    const double log_hi = std::log(std::max(2.0 * mean, 2.0));
+    std::vector<double> raw((size_t)count);
+    double raw_sum = 0.0;
+    for (double& r : raw) {
+        r = std::exp(uniform(0.0, log_hi));
+        raw_sum += r;
+    }
+    const double scale = (double)total / raw_sum;
+    std::vector<int64_t> lens((size_t)count);
+    std::vector<uint64_t> seeds((size_t)count);
+    int64_t sum = 0;
+    for (size_t i = 0; i < raw.size(); ++i) {
+        volatile double x = raw[i] * scale;
+        lens[i] = std::max<int64_t>(1, std::llround(x));
+        sum += lens[i];
+    }
+    for (size_t i = 0; sum < total; i = (i + 1) % lens.size()) {
+        ++lens[i];
+        ++sum;
+    }
+    for (size_t i = 0; sum > total; i = (i + 1) % lens.size()) {
+        if (lens[i] > 1) {
+            --lens[i];
+            --sum;
+        }
+    }
+    for (auto& s : seeds) s = next();
+    return vxg_gen_segments(ctx, count, lens.data(), seeds.data(), 0, 0, 0, 0, out, VXG_MEM_HOST);
+}
+
+}  // extern "C"

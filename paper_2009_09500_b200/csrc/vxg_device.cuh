@@ -1,0 +1,214 @@
+// vxg_device.cuh -- device arithmetic shared by every kernel.
+//
+// Bit-exact parity with the reference CPU path hinges on evaluating exactly the reference's
+// IEEE-754 operation sequence with round-to-nearest and NO fused multiply-add (nvcc contracts
+// `s + w*t` to DFMA by default). Every FP64 operation below is therefore an
+// explicit _rn intrinsic (DMUL / DADD / DSQRT / DDIV), and the library is also built with
+// --fmad=false as a second line of defence.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vxg {
+
+// Packed per-segment record consumed by the emit kernels (64 B: one half cache line).
+struct alignas(16) SegRec {
+    double sx, sy, sz;   // S
+    double wx, wy, wz;   // W = (E - S) / N
+    int32_t ex, ey, ez;  // round_point(E): the k == N sample (include/voxline/parametric.hpp:43)
+    uint32_t flags;      // REC_CHECK: samples can approach the int32 edge -> checked rounding
+};
+static_assert(sizeof(SegRec) == 64, "SegRec must be 64 B");
+
+enum : uint32_t { REC_CHECK = 1u };
+
+// Endpoints whose magnitude exceeds this get per-sample range checks in the emit kernels;
+// below it every sample S + W*k (k < N) provably rounds inside the int32 lattice because it lies
+// between S and E up to a relative error of a few ulp.
+constexpr double kCheckThreshold = 2147483000.0;
+
+// Run-control block shared by the kernels of one batch (one cudaMemsetAsync resets it).
+struct Control {
+    unsigned long long max_steps;   // N_max (atomicMax)
+    long long err_seg;              // error key (see record_error), 0 = none
+    long long pad0;
+    long long total;                // emit: total voxels (or capacity for the plan)
+    unsigned long long tile_counter;// dynamic tile ids (look-back forward progress)
+    unsigned long long outside;     // bitmap: samples outside the volume
+    long long n_entries;            // clip: non-empty entries
+    long long pad1[2];
+};
+
+// ----------------------------------------------------------------------------- rounding
+// llround (src/geometry.cpp:21): half away from zero == trunc(RZ(c + copysign(0.5, c))).
+// Proof sketch: for c >= 0, floor(RZ(c + 0.5)) == floor(c + 0.5) because the integer
+// floor(c + 0.5) is representable and <= c + 0.5, so RZ cannot round below it; c < 0 mirrors.
+__device__ __forceinline__ double round_bias(double c) {
+    return __dadd_rz(c, copysign(0.5, c));
+}
+
+__device__ __forceinline__ int32_t round_fast(double c) {
+    return __double2int_rz(round_bias(c));
+}
+
+// Checked variant: false if c is non-finite or llround(c) falls outside int32
+// (src/geometry.cpp:16-26). NaN fails both comparisons.
+__device__ __forceinline__ bool round_checked(double c, int32_t& out) {
+    const double h = round_bias(c);
+    if (!(h > -2147483649.0 && h < 2147483648.0)) {
+        out = 0;
+        return false;
+    }
+    out = __double2int_rz(h);
+    return true;
+}
+
+// S + W*t with separate multiply and add (include/voxline/parametric.hpp:44-47).
+__device__ __forceinline__ double sample_axis(double s, double w, double t) {
+    return __dadd_rn(s, __dmul_rn(w, t));
+}
+
+// ----------------------------------------------------------------------------- plan
+// make_plan (src/parametric.cpp:8-26). Returns false on a range error of either endpoint.
+struct Plan {
+    long long n;
+    double wx, wy, wz;
+    int32_t ex, ey, ez;
+};
+
+__device__ __forceinline__ bool make_plan(double sx, double sy, double sz, double ex, double ey,
+                                          double ez, Plan& p) {
+    int32_t vsx, vsy, vsz;
+    bool ok = round_checked(sx, vsx) & round_checked(sy, vsy) & round_checked(sz, vsz);
+    ok &= round_checked(ex, p.ex) & round_checked(ey, p.ey) & round_checked(ez, p.ez);
+    if (!ok) {
+        p.n = 0;
+        p.wx = p.wy = p.wz = 0.0;
+        return false;
+    }
+    if (vsx == p.ex && vsy == p.ey && vsz == p.ez) {
+        p.n = 0;
+        p.wx = p.wy = p.wz = 0.0;
+        return true;
+    }
+    const double dx = __dsub_rn(ex, sx), dy = __dsub_rn(ey, sy), dz = __dsub_rn(ez, sz);
+    // sqrt((dx*dx + dy*dy) + dz*dz), left to right (src/geometry.cpp:10)
+    const double len =
+        __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    long long n = static_cast<long long>(floor(len));
+    const double ext = fmax(fabs(dx), fmax(fabs(dy), fabs(dz)));
+    const long long ce = static_cast<long long>(ceil(ext));
+    n = n > ce ? n : ce;
+    n = n > 1 ? n : 1;
+    const double nd = __ll2double_rn(n);
+    p.n = n;
+    p.wx = __ddiv_rn(dx, nd);
+    p.wy = __ddiv_rn(dy, nd);
+    p.wz = __ddiv_rn(dz, nd);
+    return true;
+}
+
+__device__ __forceinline__ uint32_t rec_flags(double sx, double sy, double sz, double ex,
+                                              double ey, double ez) {
+    const double m = fmax(fmax(fmax(fabs(sx), fabs(sy)), fmax(fabs(sz), fabs(ex))),
+                          fmax(fabs(ey), fabs(ez)));
+    return m > kCheckThreshold ? REC_CHECK : 0u;
+}
+
+// ----------------------------------------------------------------------------- SplitMix64
+// include/voxline/bench.hpp:20-37
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
+__host__ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64_t j) {
+    return mix64(seed + (j + 1) * kGamma);
+}
+
+struct SplitMix {
+    uint64_t state;
+    __device__ __forceinline__ uint64_t next() {
+        state += kGamma;
+        return mix64(state);
+    }
+    __device__ __forceinline__ double uniform01() {
+        return __dmul_rn(__ull2double_rn(next() >> 11), 0x1.0p-53);
+    }
+    __device__ __forceinline__ double uniform(double lo, double hi) {
+        return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), uniform01()));
+    }
+};
+
+// ----------------------------------------------------------------------------- memory order
+__device__ __forceinline__ void st_release(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_stream_v4(void* p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// ----------------------------------------------------------------------------- look-back
+// Decoupled look-back (single-pass prefix scan): tile t publishes its aggregate (flag A) as soon
+// as it is known, then accumulates predecessors' values until it meets an inclusive prefix
+// (flag P), and publishes its own inclusive prefix. Values are 62-bit and packed with the flag
+// into one 64-bit word, so a relaxed single-copy-atomic access carries both.
+constexpr unsigned long long kFlagA = 1ull << 62;
+constexpr unsigned long long kFlagP = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+// Called by all 32 lanes of one warp; returns the exclusive prefix of `tile` (in every lane).
+__device__ __forceinline__ long long lookback_warp(unsigned long long* status, long long tile,
+                                                   long long aggregate) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_relaxed_u64(&status[0], kFlagP | (unsigned long long)aggregate);
+        return 0;
+    }
+    if (lane == 0) st_relaxed_u64(&status[tile], kFlagA | (unsigned long long)aggregate);
+    long long excl = 0;
+    long long end = tile;  // examine tiles [end-32, end)
+    while (true) {
+        const long long j = end - 1 - lane;
+        unsigned long long s;
+        if (j >= 0) {
+            do {
+                s = ld_relaxed_u64(&status[j]);
+            } while ((s >> 62) == 0);
+        } else {
+            s = kFlagP;  // virtual prefix 0 before tile 0
+        }
+        const unsigned int pmask = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+        long long v = (long long)(s & kValMask);
+        if (pmask) {
+            const int stop = __ffs(pmask) - 1;  // nearest inclusive prefix
+            if (lane > stop) v = 0;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (pmask) break;
+        end -= 32;
+    }
+    if (lane == 0) st_relaxed_u64(&status[tile], kFlagP | (unsigned long long)(excl + aggregate));
+    return excl;
+}
+
+}  // namespace vxg

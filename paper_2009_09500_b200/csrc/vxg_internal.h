@@ -1,0 +1,94 @@
+// vxg_internal.h -- kernel argument blocks and launchers shared by vxg_kernels.cu and vxg_api.cu.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/voxgpu.h"
+
+namespace vxg {
+
+struct SegRec;
+struct Control;
+
+struct ClipEntry {  // one segment's in-slab k-range: items k in [ka, kb) then (optionally) k = n
+    long long seg, ka, kb, n;
+};
+
+struct PlanArgs {
+    const double* segs;  // AoS, 6 doubles per segment, 16-B aligned
+    long long n;
+    SegRec* rec;
+    long long* steps;
+    long long* offsets;  // n + 1
+    unsigned long long* status;
+    Control* ctl;
+};
+
+struct ListArgs {
+    const SegRec* rec;
+    const long long* off;       // nseg + 1 sample offsets
+    const long long* tile_seg;  // ntiles
+    long long nseg, total_samples, ntiles;
+    int32_t* out;               // 3 int32 per voxel, 4-B aligned
+    long long out_cap;
+    long long* chain_off;       // nseg + 1
+    unsigned long long* status;
+    Control* ctl;
+};
+
+struct BitmapArgs {
+    const SegRec* rec;
+    const ClipEntry* entries;   // CLIP mode only
+    const long long* off;       // n_entries + 1
+    const long long* tile_seg;
+    long long n_entries, total_samples, ntiles;
+    unsigned long long* words;
+    long long V, z_lo, z_hi;
+    Control* ctl;
+};
+
+struct ClipArgs {
+    const SegRec* rec;
+    const long long* off;  // n + 1 (full plan)
+    long long n;
+    long long z_lo, z_hi;
+    ClipEntry* entries;    // up to n
+    long long* ent_off;    // up to n + 1
+    unsigned long long* status;
+    unsigned long long* status2;
+    Control* ctl;
+};
+
+struct GenArgs {
+    long long n;
+    const long long* lens;
+    const unsigned long long* seeds;
+    long long len_fixed, len_max, V;
+    unsigned long long seed;
+    double* out;
+    Control* ctl;
+};
+
+int plan_tile_count(long long n);
+int clip_tile_count(long long n);
+int list_tile_log2(int variant);
+int bitmap_tile_log2();
+
+void launch_plan(const PlanArgs& a, cudaStream_t s);
+void launch_tile_index(const long long* off, long long n_entries, int ts_log2, long long* tile_seg,
+                       cudaStream_t s);
+cudaError_t launch_emit_list(const ListArgs& a, int variant, cudaStream_t s);
+cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
+void launch_clip(const ClipArgs& a, cudaStream_t s);
+void launch_round_points(const double* p, long long n, int32_t* out, Control* ctl, cudaStream_t s);
+void launch_segment_lengths(const double* segs, long long n, double* out, cudaStream_t s);
+void launch_export_plans(const SegRec* rec, const long long* off, long long n,
+                         vxg_segment_plan* out, cudaStream_t s);
+void launch_pack_plan(const double* segs, const vxg_segment_plan* plans, long long n, SegRec* rec,
+                      long long* steps, long long* off, Control* ctl, cudaStream_t s);
+void launch_work_item(const SegRec* rec, const long long* off, long long i, long long k,
+                      int32_t* out, Control* ctl, cudaStream_t s);
+void launch_gen(const GenArgs& a, cudaStream_t s);
+
+}  // namespace vxg

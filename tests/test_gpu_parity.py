@@ -1,0 +1,341 @@
+"""Parity of the B200 path (through the C ABI) with the oracle and the reference's golden vectors.
+
+Bar: bit-exact voxel lists, chain offsets, plans (W compared as raw doubles), bitmaps and error
+classes. Small/medium corpora are compared element for element; full BASELINE sizes through
+size-independent properties and per-chain hashes (tests/gpu_checks.py).
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from tests.golden.make_golden import decimal_grid_corpus, digest, mixed_batch, seg_digest
+from tests.test_oracle_golden import _corpus
+
+pytestmark = pytest.mark.gpu
+
+
+# ------------------------------------------------------------------ golden vectors
+def test_golden_plans_chains_bounds(vx, golden):
+    for name, case in golden["plans"].items():
+        s = case["segment"]
+        n, w = vx.make_plan(s[:3], s[3:])
+        assert n == case["n"], name
+        assert w == [float.fromhex(h) for h in case["w_hex"]], name
+        assert [list(v) for v in vx.voxelize_parametric(s[:3], s[3:])] == case["chain"], name
+        assert list(vx.chain_length_bounds(s[:3], s[3:])) == case["bounds"], name
+
+
+def test_golden_rounding(vx, golden):
+    for case in golden["round_ok"]:
+        assert list(vx.round_point(case["p"])) == case["v"]
+    for case in golden["round_bad"]:
+        with pytest.raises(ValueError):
+            vx.round_point([float(x) for x in case["p"]])
+        with pytest.raises(vx.RangeError):
+            vx.round_point([float(x) for x in case["p"]])
+
+
+def test_fma_sensitive_vector(vx):
+    # under FMA the k=12 sample rounds to (12,5,0) and the chain has 13 voxels
+    chain = vx.voxelize_parametric((0.1, 0.3, 0.7), (12.45, 4.9, 0.2))
+    assert len(chain) == 14 and chain[12] == (11, 5, 0)
+
+
+def test_golden_batch(vx, golden):
+    plan = vx.batch_preprocess([((0, 0, 0), (5, 0, 0)), ((0, 0, 0), (3, 3, 3))])
+    g = golden["batch_two"]
+    assert plan.step_counts == g["steps"] and plan.output_offsets == g["offsets"]
+    assert plan.max_steps == g["max_steps"] and plan.total_voxel_capacity == g["capacity"] == 12
+    segs = [((0, 0, 0), (5, 0, 0)), ((0, 0, 0), (2, 1, 0))]
+    plan = vx.batch_preprocess(segs)
+    g = golden["batch_short"]
+    assert vx.kernel_work_item(plan, 1, 2) == tuple(g["item_1_2"]) == (2, 1, 0)
+    assert vx.kernel_work_item(plan, 0, 0) == tuple(g["item_0_0"])
+    assert vx.kernel_work_item(plan, 1, 5) is None
+    assert vx.effective_item_count(plan) == (g["live"], g["redundant"]) == (9, 3)
+    for i, k in [(2, 0), (-1, 0), (0, 6), (0, -1)]:
+        with pytest.raises(IndexError):
+            vx.kernel_work_item(plan, i, k)
+    res = vx.batch_voxelize(plan, workers=1, group_size=64)
+    assert [[list(v) for v in c] for c in res["chains"]] == g["chains"]
+    assert res["total_voxels"] == g["total"]
+    assert res["timing"]["preprocess_ns"] == 0
+
+
+def test_golden_generators(vx, golden):
+    for key, hexes in golden["gen_segment_of_length"].items():
+        target, seed = map(int, key.split("_"))
+        s, e = vx.gen_segment_of_length(target, seed)
+        assert list(s) + list(e) == [float.fromhex(h) for h in hexes], key
+    arb = np.asarray([list(s) + list(e) for s, e in vx.gen_arbitrary_batch(10000000, 1024, 7)])
+    assert seg_digest(arb) == golden["gen_arbitrary_10M_1024_7"]["digest"]
+
+
+def test_acceptance_c4_c5(vx, golden):
+    c = golden["acceptance_c4c5"]
+    segs = vx.gen_arbitrary_batch(500000, 1024, c["seed"])
+    arr = np.asarray([list(s) + list(e) for s, e in segs])
+    assert seg_digest(arr) == c["digest_segments"]
+    plan = vx.batch_preprocess(segs)
+    live, red = vx.effective_item_count(plan)
+    assert (live, red) == (c["live"], c["redundant"])
+    assert live + red == c["grid"]
+    vox, off, total = vx.run_batch_flat(arr)
+    assert total == c["total_voxels"] and digest(vox, off) == c["digest_chains"]
+    # criterion 4: output independent of the (host) partitioning knobs
+    seq = [vx.voxelize_parametric(s, e) for s, e in segs[:64]]
+    for workers, group in [(1, 1), (8, 256)]:
+        res = vx.batch_voxelize(plan, workers, group)
+        assert res["chains"][:64] == seq
+
+
+def test_golden_corpora(vx, oracle, golden):
+    for name, spec in golden["corpora"].items():
+        segs = _corpus(name, spec, oracle)
+        vox, off, total = vx.run_batch_flat(segs)
+        assert total == spec["total_voxels"], name
+        assert digest(vox, off) == spec["digest"], name
+
+
+def test_gpu_generator_matches_oracle(vx, oracle):
+    for kw in [dict(n=5000, len_fixed=128, V=512, seed=3), dict(n=5000, len_fixed=64, V=1024, seed=4),
+               dict(n=5000, len_max=2048, V=4096, seed=5), dict(n=3000, len_fixed=77, V=0, seed=6),
+               dict(n=3000, len_max=300, V=0, seed=7)]:
+        g = vx.gen_segments(kw["n"], kw.get("len_fixed", 0), kw.get("len_max", 0), kw["V"],
+                            kw["seed"])
+        o = oracle.gen_batch(kw["n"], kw.get("len_fixed", 0), kw.get("len_max", 0), kw["V"],
+                             kw["seed"])
+        assert np.array_equal(g.view(np.uint64), o.view(np.uint64)), kw
+
+
+# ------------------------------------------------------------------ seeded corpora vs oracle
+def _compare(vx, oracle, segs):
+    vox, off, total = vx.run_batch_flat(segs)
+    ovox, ooff, ototal = oracle.run_batch(segs)
+    assert total == ototal
+    assert np.array_equal(off, ooff)
+    assert np.array_equal(vox, ovox)
+    return total
+
+
+@pytest.mark.parametrize("scale", [1.0, 37.5, 1e3, 1e6, 1e9])
+def test_random_uniform(vx, oracle, scale):
+    rng = np.random.default_rng(int(scale) % 1000 + 11)
+    n = 20000 if scale < 1e3 else 200
+    segs = rng.uniform(-scale, scale, size=(n, 6))
+    if scale >= 1e3:  # keep the capacity modest: short segments far from the origin
+        segs[:, 3:] = segs[:, :3] + rng.uniform(-300, 300, size=(n, 3))
+    _compare(vx, oracle, segs)
+
+
+def test_ties_and_grids(vx, oracle):
+    rng = np.random.default_rng(3)
+    for q in (2, 4, 10, 20):
+        segs = np.round(rng.uniform(-60, 60, size=(20000, 6)) * q) / q
+        _compare(vx, oracle, segs)
+    segs = np.asarray(decimal_grid_corpus(30000, 1234))
+    _compare(vx, oracle, segs)
+
+
+def test_reference_corpora(vx, oracle):
+    for count, seed, every, mx in [(300, 402, 3, 500.0), (1500, 203, 5, 1e4), (64, 404, 3, 500.0)]:
+        _compare(vx, oracle, np.asarray(mixed_batch(count, seed, every, mx)))
+
+
+def test_zero_and_one_sample_segments(vx, oracle):
+    rng = np.random.default_rng(9)
+    base = rng.uniform(10, 20, size=(50000, 3))
+    segs = np.concatenate([base, base + rng.uniform(-0.3, 0.3, size=(50000, 3))], axis=1)
+    # thousands of N = 0 segments per 4096-sample tile (m close to the tile size)
+    _compare(vx, oracle, segs)
+    segs[::7, 3:] += 1.0
+    _compare(vx, oracle, segs)
+
+
+def test_tile_boundaries(vx, oracle):
+    # segment starts landing exactly on and around 2048/4096-sample tile boundaries
+    for L in (4095, 4096, 4097, 2047, 2048, 1, 2, 31, 32, 33):
+        segs = oracle.gen_batch(64, L, 0, 0 if L > 1000 else 0, 100 + L)
+        _compare(vx, oracle, segs)
+
+
+def test_single_long_segments(vx, oracle):
+    # config 2: one segment swept 1 .. 10^6 voxels
+    for L in (1, 10, 100, 1000, 10_000, 100_000, 1_000_000):
+        s = oracle.gen_segment_of_length(L, 2024 + L)
+        got = np.asarray(vx.voxelize_parametric(s[:3], s[3:]), dtype=np.int32)
+        assert np.array_equal(got, oracle.voxelize_parametric(s)), L
+
+
+def test_config_scaled_lists(vx, oracle):
+    for kw in [dict(n=65536, len_fixed=128, V=512, seed=0x5EED0101),
+               dict(n=20000, len_max=2048, V=4096, seed=0x5EED0104)]:
+        segs = vx.gen_segments(kw["n"], kw.get("len_fixed", 0), kw.get("len_max", 0), kw["V"],
+                               kw["seed"])
+        _compare(vx, oracle, segs)
+
+
+# ------------------------------------------------------------------ errors
+def test_error_semantics(vx):
+    with pytest.raises(ValueError):
+        vx.batch_preprocess([])
+    with pytest.raises(vx.InvalidArgument):
+        vx.run_batch([])
+    # tests/test_batch.cpp:175-181: overflow surfaces as range_error (from preprocess)
+    with pytest.raises(vx.RangeError):
+        vx.run_batch([((0, 0, 0), (5, 0, 0)), ((0, 0, 0), (3e9, 0, 0))], workers=2, group_size=1)
+    segs = [((0, 0, 0), (5, 0, 0)), ((0, float("nan"), 0), (1, 1, 1)), ((1, 1, 1), (2, 2, 2)),
+            ((0, 0, 0), (float("inf"), 0, 0))]
+    with pytest.raises(vx.RangeError) as e:
+        vx.run_batch(segs)
+    assert e.value.segment == 1  # lowest failing segment, as the reference's serial loop
+    plan = vx.batch_preprocess([((0, 0, 0), (5, 0, 0))])
+    with pytest.raises(ValueError):
+        vx.batch_voxelize(plan, workers=0)
+    with pytest.raises(ValueError):
+        vx.batch_voxelize(plan, group_size=0)
+    with pytest.raises(ValueError):
+        vx.compute_mvps(10, 0.0)
+    with pytest.raises(ValueError):
+        vx.gen_arbitrary_batch(5, 10, 1)
+
+
+def test_int32_edges(vx, oracle):
+    segs = np.array([[2147483640.0, 0, 0, 2147483647.4, 0, 0],
+                     [-2147483640.0, 5, 5, -2147483648.4, 9, -3],
+                     [2147483000.5, -2147483000.5, 1, 2147483100.25, -2147483100.75, 7]])
+    _compare(vx, oracle, segs)
+    with pytest.raises(vx.RangeError):
+        vx.run_batch_flat(np.array([[2147483640.0, 0, 0, 2147483647.5, 0, 0]]))
+
+
+def test_concurrent_contexts(vx, oracle):
+    segs = [oracle.gen_batch(3000, 0, 400, 1024, 50 + t) for t in range(4)]
+    expect = [oracle.run_batch(s) for s in segs]
+    errors = []
+
+    def work(t):
+        try:
+            for _ in range(3):
+                vox, off, total = vx.run_batch_flat(segs[t])  # per-thread default context
+                assert total == expect[t][2] and np.array_equal(vox, expect[t][0])
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    [t.start() for t in ths]
+    [t.join() for t in ths]
+    assert not errors, errors
+
+
+# ------------------------------------------------------------------ bitmaps
+def test_bitmap_vs_oracle(vx, oracle):
+    segs = vx.gen_segments(20000, 64, 0, 256, 77)
+    words, outside = vx.voxelize_bitmap(segs, 256, clip=False)
+    ow, oo = oracle.bitmap(segs, 256)
+    assert outside == oo == 0
+    assert np.array_equal(words, ow)
+    # z-slab partition (1, 2, 4, 8 slabs) with device clipping == the full bitmap
+    for G in (1, 2, 4, 8):
+        h = 256 // G
+        parts = [vx.voxelize_bitmap(segs, 256, g * h, (g + 1) * h, clip=True)[0] for g in range(G)]
+        assert np.array_equal(np.concatenate(parts), ow), G
+
+
+def test_bitmap_outside_and_negative(vx, oracle):
+    rng = np.random.default_rng(12)
+    segs = rng.uniform(-40, 160, size=(5000, 6))
+    for z0, z1, clip in [(0, 128, False), (17, 93, True), (0, 128, True)]:
+        words, outside = vx.voxelize_bitmap(segs, 128, z0, z1, clip=clip)
+        ow, oo = oracle.bitmap(segs, 128, z0, z1)
+        assert np.array_equal(words, ow), (z0, z1, clip)
+        if not clip:
+            assert outside == oo
+
+
+def test_bitmap_clip_adversarial(vx, oracle):
+    # nearly-flat z, exact ties on slab boundaries, descending z
+    rng = np.random.default_rng(4)
+    segs = np.round(rng.uniform(0, 63, size=(20000, 6)) * 2) / 2
+    segs[::3, 5] = segs[::3, 2] + 1e-13
+    for z0, z1 in [(0, 32), (32, 64), (10, 11), (31, 33)]:
+        words, _ = vx.voxelize_bitmap(segs, 64, z0, z1, clip=True)
+        ow, _ = oracle.bitmap(segs, 64, z0, z1)
+        assert np.array_equal(words, ow), (z0, z1)
+
+
+# ------------------------------------------------------------------ device-resident (torch)
+def test_torch_device_buffers(vx, oracle):
+    import torch
+    segs = oracle.gen_batch(10000, 0, 512, 1024, 31)
+    d = torch.from_numpy(segs).cuda()
+    b = vx.Batch(None, device_ptr=d.data_ptr(), n=segs.shape[0])
+    out = torch.empty((b.capacity, 3), dtype=torch.int32, device="cuda")
+    chain = torch.empty(b.n + 1, dtype=torch.int64, device="cuda")
+    total = b.emit_list_device(out.data_ptr(), b.capacity, chain.data_ptr())
+    vox, off, ototal = oracle.run_batch(segs)
+    assert total == ototal
+    assert np.array_equal(out[:total].cpu().numpy(), vox)
+    assert np.array_equal(chain.cpu().numpy(), off)
+    words = torch.zeros((1024 ** 3) // 64, dtype=torch.int64, device="cuda")
+    b.emit_bitmap_device(words.data_ptr(), 1024, 0, 1024, False)
+    ow, _ = oracle.bitmap(segs, 1024)
+    assert np.array_equal(words.cpu().numpy().view(np.uint64), ow)
+
+
+# ------------------------------------------------------------------ full BASELINE sizes
+@pytest.mark.slow
+def test_full_config4_list_hashes(vx, oracle):
+    """Config 4 at full size: 4M segments, N ~ U{1..2048}: every chain's length and
+    order-sensitive hash equal the oracle's (4.3 G samples); first/last voxels pinned."""
+    import torch
+    from tests.gpu_checks import device_chain_hashes
+    n = 4 * 1024 * 1024
+    d = torch.empty((n, 6), dtype=torch.float64, device="cuda")
+    ctx = vx.default_context()
+    ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, 0, 2048, 4096, 0x5EED0004, d.data_ptr(), 1))
+    b = vx.Batch(None, device_ptr=d.data_ptr(), n=n)
+    out = torch.empty((b.capacity, 3), dtype=torch.int32, device="cuda")
+    chain = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    total = b.emit_list_device(out.data_ptr(), b.capacity, chain.data_ptr())
+    segs = d.cpu().numpy()
+    h, ln = device_chain_hashes(out[:total], chain)
+    oh, oln = oracle.chain_hashes(segs)
+    assert int(oln.sum()) == total
+    assert np.array_equal(ln, oln)
+    assert np.array_equal(h, oh)
+    # first voxel of every chain is round(S), last is round(E)
+    first = out[chain[:-1]].cpu().numpy()
+    last = out[chain[1:] - 1].cpu().numpy()
+    assert np.array_equal(first, np.floor(segs[:, :3] + 0.5).astype(np.int32))
+    assert np.array_equal(last, np.floor(segs[:, 3:] + 0.5).astype(np.int32))
+
+
+@pytest.mark.slow
+def test_full_config5_slabs_consistent(vx, oracle):
+    """Config 5 geometry (4096^3 bitmap, N ~ U{1..2048}) on 8M segments: the 8 device-clipped
+    z-slabs reassemble the unclipped full bitmap bit for bit, and a 1/512 subsample of the
+    segments matches the oracle's bitmap exactly."""
+    import torch
+    V, n = 4096, 8 * 1024 * 1024
+    d = torch.empty((n, 6), dtype=torch.float64, device="cuda")
+    ctx = vx.default_context()
+    ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, 0, 2048, V, 0x5EED0005, d.data_ptr(), 1))
+    b = vx.Batch(None, device_ptr=d.data_ptr(), n=n)
+    nwords = V * V * V // 64
+    full = torch.zeros(nwords, dtype=torch.int64, device="cuda")
+    b.emit_bitmap_device(full.data_ptr(), V, 0, V, False)
+    slabs = torch.zeros(nwords, dtype=torch.int64, device="cuda")
+    h = V // 8
+    per = nwords // 8
+    for g in range(8):
+        b.emit_bitmap_device(slabs.data_ptr() + 8 * g * per, V, g * h, (g + 1) * h, True)
+    assert torch.equal(full, slabs)
+    del slabs, full
+    sub = d[::512].contiguous()
+    bs = vx.Batch(None, device_ptr=sub.data_ptr(), n=sub.shape[0])
+    w = torch.zeros(nwords, dtype=torch.int64, device="cuda")
+    bs.emit_bitmap_device(w.data_ptr(), V, 0, V, True)
+    ow, _ = oracle.bitmap(sub.cpu().numpy(), V)
+    assert np.array_equal(w.cpu().numpy().view(np.uint64), ow)
