@@ -99,6 +99,7 @@ struct vxg_context {
     int64_t err_seg = -1;
     int64_t launches = 0;
     int list_variant = 0;
+    int debug = 0;  // VXG_DEBUG (diagnostics only)
     DeviceCache cache;
     Control* h_ctl = nullptr;  // pinned readback slot
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -176,6 +177,8 @@ vxg_status read_ctl(vxg_context* ctx, Control* d_ctl, Control& out, const char* 
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, phase);
     out = *ctx->h_ctl;
+    if (out.abort)
+        return ctx->fail(VXG_LOGIC_ERROR, -1, "%s: look-back watchdog fired (internal error)", phase);
     if (out.err_seg != 0) {
         const long long key = out.err_seg;
         const int kind = (int)(key & 7);
@@ -275,22 +278,23 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long long* d_chain,
                             int64_t* total) {
     vxg_context* ctx = b->ctx;
-    const int ts_log2 = vxg::list_tile_log2(ctx->list_variant);
-    const int64_t ntiles = ceil_div(b->capacity, 1ll << ts_log2);
-    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)ntiles) ||
-        !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)std::max<int64_t>(ntiles, vxg::plan_tile_count(b->n))))
+    const int ts_log2 = vxg::list_chunk_log2(ctx->list_variant);
+    const int64_t nchunks = ceil_div(b->capacity, 1ll << ts_log2);
+    const int64_t nstatus = nchunks;  // one look-back status word per warp chunk
+    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)nchunks) ||
+        !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)std::max<int64_t>(nstatus, vxg::plan_tile_count(b->n))))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
     if ((reinterpret_cast<uintptr_t>(d_out) & 3u) != 0)
         return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_voxelize: output must be 4-byte aligned");
     cudaMemsetAsync(ctl_slot(b, 1), 0, sizeof(Control), ctx->stream);
-    cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)ntiles, ctx->stream);
+    cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)nstatus, ctx->stream);
     cudaEventRecord(ctx->ev[2], ctx->stream);
     vxg::launch_tile_index(b->off.as<long long>(), b->n, ts_log2, b->tile_seg.as<long long>(),
                            ctx->stream);
     cudaEventRecord(ctx->ev[3], ctx->stream);
     vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->tile_seg.as<long long>(),
-                    b->n, b->capacity, ntiles, d_out, out_cap, d_chain,
-                    b->status.as<unsigned long long>(), ctl_slot(b, 1)};
+                    b->n, b->capacity, nchunks, d_out, out_cap, d_chain,
+                    b->status.as<unsigned long long>(), ctl_slot(b, 1), ctx->debug};
     cudaError_t e = vxg::launch_emit_list(a, ctx->list_variant, ctx->stream);
     ctx->launches += 2;
     cudaEventRecord(ctx->ev[4], ctx->stream);
@@ -404,6 +408,7 @@ VXG_API vxg_status vxg_create(int device, vxg_context** out) {
     }
     ctx->own_stream = true;
     if (const char* v = std::getenv("VXG_LIST_VARIANT")) ctx->list_variant = std::atoi(v);
+    if (const char* v = std::getenv("VXG_DEBUG")) ctx->debug = std::atoi(v);
     *out = ctx;
     return VXG_OK;
 }
@@ -748,6 +753,8 @@ VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t 
     ctx->ok();
     if (V <= 0 || V > (1ll << 21) || z_lo < 0 || z_hi > V || z_lo > z_hi)
         return ctx->fail(VXG_INVALID_ARGUMENT, -1, "bitmap: invalid volume / slab");
+    if ((V * V * (z_hi - z_lo) + 63) / 64 >= 0xffffffffll)  // word indices are 32-bit keys in-kernel
+        return ctx->fail(VXG_INVALID_ARGUMENT, -1, "bitmap: slab larger than 2^32 words; split it");
     cudaSetDevice(ctx->device);
     const size_t nwords = (size_t)((V * V * (z_hi - z_lo) + 63) / 64);
     const auto t0 = Clock::now();

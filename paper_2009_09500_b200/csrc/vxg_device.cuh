@@ -37,7 +37,8 @@ struct Control {
     unsigned long long tile_counter;// dynamic tile ids (look-back forward progress)
     unsigned long long outside;     // bitmap: samples outside the volume
     long long n_entries;            // clip: non-empty entries
-    long long pad1[2];
+    int abort;                      // look-back watchdog fired (see lookback_resolve)
+    int pad1[3];
 };
 
 // ----------------------------------------------------------------------------- rounding
@@ -174,23 +175,40 @@ constexpr unsigned long long kFlagA = 1ull << 62;
 constexpr unsigned long long kFlagP = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
-// Called by all 32 lanes of one warp; returns the exclusive prefix of `tile` (in every lane).
-__device__ __forceinline__ long long lookback_warp(unsigned long long* status, long long tile,
-                                                   long long aggregate) {
+// Publish a tile's aggregate (tile 0 publishes its inclusive prefix directly). One lane.
+__device__ __forceinline__ void lookback_publish(unsigned long long* status, long long tile,
+                                                 long long aggregate) {
+    st_relaxed_u64(&status[tile], (tile == 0 ? kFlagP : kFlagA) | (unsigned long long)aggregate);
+}
+
+// Resolve a tile whose aggregate was already published: accumulate predecessors back to the
+// nearest inclusive prefix, publish this tile's inclusive prefix, return the exclusive one.
+// Called by all 32 lanes of one warp.
+// Watchdog: a spin that outlives kSpinLimit polls (~seconds) raises Control::abort, which makes
+// every other spinning warp give up too; the kernel then terminates with a logic error instead
+// of hanging the GPU.
+constexpr unsigned kSpinLimit = 1u << 23;
+
+__device__ __forceinline__ long long lookback_resolve(unsigned long long* status, long long tile,
+                                                      long long aggregate, Control* ctl) {
     const int lane = threadIdx.x & 31;
-    if (tile == 0) {
-        if (lane == 0) st_relaxed_u64(&status[0], kFlagP | (unsigned long long)aggregate);
-        return 0;
-    }
-    if (lane == 0) st_relaxed_u64(&status[tile], kFlagA | (unsigned long long)aggregate);
+    if (tile == 0) return 0;
     long long excl = 0;
     long long end = tile;  // examine tiles [end-32, end)
     while (true) {
         const long long j = end - 1 - lane;
         unsigned long long s;
         if (j >= 0) {
+            unsigned spins = 0;
             do {
                 s = ld_relaxed_u64(&status[j]);
+                if ((++spins & 1023u) == 0) {
+                    if (spins >= kSpinLimit) atomicExch(&ctl->abort, 1);
+                    if (*reinterpret_cast<volatile int*>(&ctl->abort)) {
+                        s = kFlagP;  // give up (the call fails with a logic error)
+                        break;
+                    }
+                }
             } while ((s >> 62) == 0);
         } else {
             s = kFlagP;  // virtual prefix 0 before tile 0
@@ -209,6 +227,57 @@ __device__ __forceinline__ long long lookback_warp(unsigned long long* status, l
     }
     if (lane == 0) st_relaxed_u64(&status[tile], kFlagP | (unsigned long long)(excl + aggregate));
     return excl;
+}
+
+// ----------------------------------------------------------------------------- errors / samples
+// Error key ((2^59 - 1 - seg) << 3) | kind: atomicMax keeps the lowest failing segment, so the
+// reported segment matches the reference's serial preprocess loop (src/batch.cpp:61-66).
+__device__ __forceinline__ void record_error(Control* ctl, long long seg, int kind) {
+    const long long key = ((((1ll << 59) - 1) - seg) << 3) | (long long)kind;
+    atomicMax(&ctl->err_seg, key);
+}
+
+// Voxel of sample k of a segment (include/voxline/parametric.hpp:41-48 + src/geometry.cpp:32).
+__device__ __forceinline__ void eval_sample(const SegRec& r, long long k, long long N, int32_t& x,
+                                            int32_t& y, int32_t& z, bool& bad) {
+    if (k >= N) {  // the final sample is E itself
+        x = r.ex;
+        y = r.ey;
+        z = r.ez;
+        return;
+    }
+    const double t = __ll2double_rn(k);
+    const double gx = sample_axis(r.sx, r.wx, t);
+    const double gy = sample_axis(r.sy, r.wy, t);
+    const double gz = sample_axis(r.sz, r.wz, t);
+    if (r.flags & REC_CHECK) {
+        bool ok = round_checked(gx, x);
+        ok &= round_checked(gy, y);
+        ok &= round_checked(gz, z);
+        bad |= !ok;
+    } else {
+        x = round_fast(gx);
+        y = round_fast(gy);
+        z = round_fast(gz);
+    }
+}
+
+__device__ __forceinline__ SegRec load_rec(const SegRec* p) {
+    const uint4* q = reinterpret_cast<const uint4*>(p);
+    SegRec r;
+    uint4* d = reinterpret_cast<uint4*>(&r);
+    d[0] = __ldg(q + 0);
+    d[1] = __ldg(q + 1);
+    d[2] = __ldg(q + 2);
+    d[3] = __ldg(q + 3);
+    return r;
+}
+
+// Publish + resolve in one go (called by all 32 lanes of one warp).
+__device__ __forceinline__ long long lookback_warp(unsigned long long* status, long long tile,
+                                                   long long aggregate, Control* ctl) {
+    if ((threadIdx.x & 31) == 0) lookback_publish(status, tile, aggregate);
+    return lookback_resolve(status, tile, aggregate, ctl);
 }
 
 }  // namespace vxg

@@ -28,13 +28,14 @@ struct PlanArgs {
 struct ListArgs {
     const SegRec* rec;
     const long long* off;       // nseg + 1 sample offsets
-    const long long* tile_seg;  // ntiles
-    long long nseg, total_samples, ntiles;
+    const long long* tile_seg;  // nchunks: entry containing each chunk's first sample
+    long long nseg, total_samples, nchunks;
     int32_t* out;               // 3 int32 per voxel, 4-B aligned
     long long out_cap;
     long long* chain_off;       // nseg + 1
     unsigned long long* status;
     Control* ctl;
+    int debug;                  // VXG_DEBUG bit 0: skip the look-back (diagnostics only)
 };
 
 struct BitmapArgs {
@@ -72,7 +73,7 @@ struct GenArgs {
 
 int plan_tile_count(long long n);
 int clip_tile_count(long long n);
-int list_tile_log2(int variant);
+int list_chunk_log2(int variant);  // samples per warp chunk (= per look-back status word)
 int bitmap_tile_log2();
 
 void launch_plan(const PlanArgs& a, cudaStream_t s);

@@ -51,13 +51,6 @@ __device__ __forceinline__ long long block_excl_scan(long long v, long long* s_w
     return s_warp[warp] + incl - v;
 }
 
-// Error key ((2^59 - 1 - seg) << 3) | kind: atomicMax keeps the lowest failing segment, so the
-// reported segment matches the reference's serial preprocess loop (src/batch.cpp:61-66).
-__device__ __forceinline__ void record_error(Control* ctl, long long seg, int kind) {
-    const long long key = ((((1ll << 59) - 1) - seg) << 3) | (long long)kind;
-    atomicMax(&ctl->err_seg, key);
-}
-
 // =============================================================================== plan kernel
 // One tile = BLOCK*IPT segments. Segments are read striped (coalesced), the (N_i + 1) counts are
 // transposed through shared memory into a blocked arrangement for the in-order scan, and the
@@ -122,7 +115,7 @@ __global__ void __launch_bounds__(BLOCK) plan_kernel(PlanArgs a) {
     long long agg;
     const long long excl = block_excl_scan<BLOCK>(sum, s_warp, agg);
     if (tid < 32) {
-        const long long pre = lookback_warp(a.status, tile, agg);
+        const long long pre = lookback_warp(a.status, tile, agg, a.ctl);
         if (tid == 0) s_prefix = pre;
     }
     __syncthreads();
@@ -157,308 +150,6 @@ __global__ void tile_index_kernel(const long long* __restrict__ off, long long n
     const long long t_first = (o + ts - 1) >> ts_log2;
     const long long t_last = (e - 1) >> ts_log2;
     for (long long t = t_first; t <= t_last; ++t) tile_seg[t] = c;
-}
-
-// =============================================================================== sample eval
-__device__ __forceinline__ void eval_sample(const SegRec& r, long long k, long long N, int32_t& x,
-                                            int32_t& y, int32_t& z, bool& bad) {
-    if (k >= N) {  // include/voxline/parametric.hpp:43: the final sample is E itself
-        x = r.ex;
-        y = r.ey;
-        z = r.ez;
-        return;
-    }
-    const double t = __ll2double_rn(k);
-    const double gx = sample_axis(r.sx, r.wx, t);
-    const double gy = sample_axis(r.sy, r.wy, t);
-    const double gz = sample_axis(r.sz, r.wz, t);
-    if (r.flags & REC_CHECK) {
-        bool ok = round_checked(gx, x);
-        ok &= round_checked(gy, y);
-        ok &= round_checked(gz, z);
-        bad |= !ok;
-    } else {
-        x = round_fast(gx);
-        y = round_fast(gy);
-        z = round_fast(gz);
-    }
-}
-
-__device__ __forceinline__ SegRec load_rec(const SegRec* p) {
-    const uint4* q = reinterpret_cast<const uint4*>(p);
-    SegRec r;
-    uint4* d = reinterpret_cast<uint4*>(&r);
-    d[0] = __ldg(q + 0);
-    d[1] = __ldg(q + 1);
-    d[2] = __ldg(q + 2);
-    d[3] = __ldg(q + 3);
-    return r;
-}
-
-// Largest c in [lo, hi] with so[c] <= f (so[lo] <= f guaranteed).
-__device__ __forceinline__ int seg_search(const long long* so, int lo, int hi, long long f) {
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (so[mid] <= f) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
-
-// =============================================================================== emit: list
-// One CTA per tile of TS = BLOCK*IPT consecutive flat samples (the paper's N_P x (N_max+1) grid
-// without redundant items). Items are striped (sample t0 + j*BLOCK + tid) so that a warp row
-// holds 32 consecutive samples: the previous sample comes from __shfl_up, keep flags from
-// __ballot, ranks from popc, and compacted 12-B records land conflict-free in shared memory.
-// The tile's output position comes from the decoupled look-back; the tile is then written with
-// 16-B streaming stores (head/tail words scalar).
-template <int BLOCK, int IPT>
-__global__ void __launch_bounds__(BLOCK) emit_list_kernel(ListArgs a) {
-    constexpr int TS = BLOCK * IPT;
-    constexpr int NW = BLOCK / 32;
-    constexpr int NE = IPT * NW;
-    static_assert(NE % 32 == 0, "IPT * warps must be a multiple of 32");
-    extern __shared__ __align__(16) unsigned char smem[];
-    long long* so = reinterpret_cast<long long*>(smem);
-    unsigned char* stage = smem;
-    __shared__ unsigned int s_mask[NE];
-    __shared__ int s_base[NE];
-    __shared__ long long s_tile, s_prefix, s_cnt;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = (long long)atomicAdd(&a.ctl->tile_counter, 1ull);
-    __syncthreads();
-    const long long tile = s_tile;
-    const long long t0 = tile * TS;
-    const long long tend = min(t0 + (long long)TS, a.total_samples);
-    const long long seg_lo = a.tile_seg[tile];
-    const long long seg_hi = (tile + 1 < a.ntiles) ? a.tile_seg[tile + 1] : a.nseg - 1;
-    const int m = (int)(seg_hi - seg_lo + 1);
-    for (int q = tid; q <= m; q += BLOCK) so[q] = a.off[seg_lo + q];
-    __syncthreads();
-
-    int32_t vx[IPT], vy[IPT], vz[IPT];
-    unsigned int keepbits = 0;
-    int c = 0, cached = -1;
-    SegRec r;
-    long long N = 0, so_c = 0;
-    bool bad = false;
-    long long bad_seg = 0;
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        const long long f = t0 + (long long)j * BLOCK + tid;
-        const bool valid = f < tend;
-        int32_t x = 0, y = 0, z = 0;
-        long long k = 0;
-        if (valid) {
-            c = seg_search(so, c, m - 1, f);
-            if (c != cached) {
-                cached = c;
-                r = load_rec(a.rec + seg_lo + c);
-                so_c = so[c];
-                N = so[c + 1] - so_c - 1;
-            }
-            k = f - so_c;
-            bool b = false;
-            eval_sample(r, k, N, x, y, z, b);
-            if (b) {
-                bad = true;
-                bad_seg = seg_lo + c;
-            }
-        }
-        int32_t px = __shfl_up_sync(0xffffffffu, x, 1);
-        int32_t py = __shfl_up_sync(0xffffffffu, y, 1);
-        int32_t pz = __shfl_up_sync(0xffffffffu, z, 1);
-        if (lane == 0 && valid && k > 0) {
-            bool b = false;
-            eval_sample(r, k - 1, N, px, py, pz, b);
-        }
-        const bool keep = valid && (k == 0 || x != px || y != py || z != pz);
-        const unsigned int mask = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) s_mask[j * NW + warp] = mask;
-        vx[j] = x;
-        vy[j] = y;
-        vz[j] = z;
-        keepbits |= (keep ? 1u : 0u) << j;
-    }
-    if (bad) record_error(a.ctl, bad_seg, 2);
-    __syncthreads();
-
-    if (warp == 0) {
-        constexpr int PER = NE / 32;
-        int cnt[PER];
-        int sum = 0;
-#pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            cnt[q] = __popc(s_mask[lane * PER + q]);
-            sum += cnt[q];
-        }
-        int incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        int run = incl - sum;
-#pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            s_base[lane * PER + q] = run;
-            run += cnt[q];
-        }
-        const long long agg = __shfl_sync(0xffffffffu, incl, 31);
-        const long long pre = lookback_warp(a.status, tile, agg);
-        if (lane == 0) {
-            s_prefix = pre;
-            s_cnt = agg;
-        }
-    }
-    __syncthreads();
-    const long long prefix = s_prefix, cnt = s_cnt;
-
-    // chain offsets: each segment whose k = 0 sample lies in this tile (k = 0 is always kept)
-    for (int q = tid; q < m; q += BLOCK) {
-        const long long st = so[q];
-        if (st >= t0 && st < tend) {
-            const int loc = (int)(st - t0);
-            const int j = loc / BLOCK, t = loc % BLOCK;
-            const int e = j * NW + (t >> 5);
-            const int rank = s_base[e] + __popc(s_mask[e] & ((1u << (t & 31)) - 1u));
-            a.chain_off[seg_lo + q] = prefix + rank;
-        }
-    }
-    if (tile == a.ntiles - 1 && tid == 0) {
-        a.chain_off[a.nseg] = prefix + cnt;
-        a.ctl->total = prefix + cnt;
-    }
-    const bool fits = prefix + cnt <= a.out_cap;
-    if (!fits && tid == 0) record_error(a.ctl, seg_lo, 4);
-    __syncthreads();  // so[] is dead from here on; the staging buffer aliases it
-
-    const uintptr_t gbyte0 = reinterpret_cast<uintptr_t>(a.out) + 12ull * (unsigned long long)prefix;
-    const int head = (int)(gbyte0 & 15u);
-    const unsigned int lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        if ((keepbits >> j) & 1u) {
-            const int e = j * NW + warp;
-            const int rank = s_base[e] + __popc(s_mask[e] & lt);
-            int32_t* d = reinterpret_cast<int32_t*>(stage + head + 12 * rank);
-            d[0] = vx[j];
-            d[1] = vy[j];
-            d[2] = vz[j];
-        }
-    }
-    __syncthreads();
-    if (!fits) return;
-    const int nbytes = head + 12 * (int)cnt;
-    const int nchunks = (nbytes + 15) >> 4;
-    unsigned char* gbase = reinterpret_cast<unsigned char*>(gbyte0 - (uintptr_t)head);
-    for (int ch = tid; ch < nchunks; ch += BLOCK) {
-        const int lo = ch << 4;
-        if (lo >= head && lo + 16 <= nbytes) {
-            st_stream_v4(gbase + lo, *reinterpret_cast<const uint4*>(stage + lo));
-        } else {
-#pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                const int b = lo + 4 * w;
-                if (b >= head && b < nbytes)
-                    *reinterpret_cast<uint32_t*>(gbase + b) =
-                        *reinterpret_cast<const uint32_t*>(stage + b);
-            }
-        }
-    }
-}
-
-// =============================================================================== emit: bitmap
-// Same tiling; every sample voxel inside [0,V)^2 x [z_lo,z_hi) sets its bit. Lanes of a warp row
-// hold consecutive samples, so voxels sharing a 64-bit word are merged with __match_any_sync +
-// an OR-reduction and written by one RED.OR per word group.
-template <int BLOCK, int IPT, bool CLIP>
-__global__ void __launch_bounds__(BLOCK) emit_bitmap_kernel(BitmapArgs a) {
-    constexpr int TS = BLOCK * IPT;
-    extern __shared__ __align__(16) unsigned char smem[];
-    long long* so = reinterpret_cast<long long*>(smem);
-    __shared__ long long s_tile;
-    const int tid = threadIdx.x, lane = tid & 31;
-    if (tid == 0) s_tile = (long long)atomicAdd(&a.ctl->tile_counter, 1ull);
-    __syncthreads();
-    const long long tile = s_tile;
-    const long long t0 = tile * TS;
-    const long long tend = min(t0 + (long long)TS, a.total_samples);
-    const long long e_lo = a.tile_seg[tile];
-    const long long e_hi = (tile + 1 < a.ntiles) ? a.tile_seg[tile + 1] : a.n_entries - 1;
-    const int m = (int)(e_hi - e_lo + 1);
-    for (int q = tid; q <= m; q += BLOCK) so[q] = a.off[e_lo + q];
-    __syncthreads();
-
-    const long long V = a.V;
-    int c = 0, cached = -1;
-    SegRec r;
-    long long N = 0, so_c = 0, ka = 0, kspan = 0, seg = 0;
-    bool bad = false;
-    long long bad_seg = 0;
-    unsigned long long outside = 0;
-#pragma unroll 4
-    for (int j = 0; j < IPT; ++j) {
-        const long long f = t0 + (long long)j * BLOCK + tid;
-        const bool valid = f < tend;
-        long long word = -1;
-        unsigned long long bit = 0;
-        if (valid) {
-            c = seg_search(so, c, m - 1, f);
-            if (c != cached) {
-                cached = c;
-                so_c = so[c];
-                if (CLIP) {
-                    const ClipEntry* ce = a.entries + e_lo + c;
-                    seg = ce->seg;
-                    ka = ce->ka;
-                    kspan = ce->kb - ce->ka;
-                    N = ce->n;
-                    r = load_rec(a.rec + seg);
-                } else {
-                    seg = e_lo + c;
-                    r = load_rec(a.rec + seg);
-                    N = so[c + 1] - so_c - 1;
-                    ka = 0;
-                    kspan = N;
-                }
-            }
-            const long long loc = f - so_c;
-            const long long k = loc < kspan ? ka + loc : N;
-            int32_t x, y, z;
-            bool b = false;
-            eval_sample(r, k, N, x, y, z, b);
-            if (b) {
-                bad = true;
-                bad_seg = seg;
-            }
-            if ((unsigned long long)x < (unsigned long long)V &&
-                (unsigned long long)y < (unsigned long long)V &&
-                (unsigned long long)z < (unsigned long long)V) {
-                if (z >= a.z_lo && z < a.z_hi) {
-                    const unsigned long long bi =
-                        (unsigned long long)x +
-                        (unsigned long long)V * ((unsigned long long)y +
-                                                 (unsigned long long)V * (unsigned long long)(z - a.z_lo));
-                    word = (long long)(bi >> 6);
-                    bit = 1ull << (bi & 63);
-                }
-            } else {
-                ++outside;
-            }
-        }
-        const unsigned int peers = __match_any_sync(0xffffffffu, word);
-        const unsigned int lo = __reduce_or_sync(peers, (unsigned int)bit);
-        const unsigned int hi = __reduce_or_sync(peers, (unsigned int)(bit >> 32));
-        if (word >= 0 && lane == __ffs(peers) - 1)
-            atomicOr(reinterpret_cast<unsigned long long*>(a.words) + word,
-                     ((unsigned long long)hi << 32) | lo);
-    }
-    if (bad) record_error(a.ctl, bad_seg, 2);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) outside += __shfl_xor_sync(0xffffffffu, outside, o);
-    if (lane == 0 && outside) atomicAdd(&a.ctl->outside, outside);
 }
 
 // =============================================================================== clip
@@ -564,8 +255,8 @@ __global__ void __launch_bounds__(BLOCK) clip_kernel(ClipArgs a) {
     __syncthreads();
     const long long ex_e = block_excl_scan<BLOCK>(sn, s_warp, agg_e);
     if (tid < 32) {
-        const long long ps = lookback_warp(a.status, tile, agg_s);
-        const long long pe = lookback_warp(a.status2, tile, agg_e);
+        const long long ps = lookback_warp(a.status, tile, agg_s, a.ctl);
+        const long long pe = lookback_warp(a.status2, tile, agg_e, a.ctl);
         if (tid == 0) {
             s_pre_s = ps;
             s_pre_e = pe;
@@ -786,59 +477,6 @@ void launch_tile_index(const long long* off, long long n_entries, int ts_log2, l
     const int b = 256;
     tile_index_kernel<<<(unsigned)((n_entries + b - 1) / b), b, 0, s>>>(off, n_entries, ts_log2,
                                                                          tile_seg);
-}
-
-template <int BLOCK, int IPT>
-static cudaError_t launch_list_t(const ListArgs& a, cudaStream_t s) {
-    constexpr int TS = BLOCK * IPT;
-    const size_t smem_so = sizeof(long long) * (TS + 2);
-    const size_t smem_st = 16 + 12 * (size_t)TS;
-    const size_t smem = smem_so > smem_st ? smem_so : smem_st;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(emit_list_kernel<BLOCK, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attr = true;
-    }
-    emit_list_kernel<BLOCK, IPT><<<(unsigned)a.ntiles, BLOCK, smem, s>>>(a);
-    return cudaGetLastError();
-}
-
-int list_tile_log2(int variant) {
-    switch (variant) {
-        case 1: return 12;  // 256 x 16
-        case 2: return 11;  // 256 x 8
-        case 3: return 12;  // 512 x 8
-        default: return 12; // 256 x 16
-    }
-}
-
-cudaError_t launch_emit_list(const ListArgs& a, int variant, cudaStream_t s) {
-    switch (variant) {
-        case 2: return launch_list_t<256, 8>(a, s);
-        case 3: return launch_list_t<512, 8>(a, s);
-        default: return launch_list_t<256, 16>(a, s);
-    }
-}
-
-int bitmap_tile_log2() { return 12; }
-
-template <int BLOCK, int IPT, bool CLIP>
-static cudaError_t launch_bitmap_t(const BitmapArgs& a, cudaStream_t s) {
-    constexpr int TS = BLOCK * IPT;
-    const size_t smem = sizeof(long long) * (TS + 2);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(emit_bitmap_kernel<BLOCK, IPT, CLIP>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    emit_bitmap_kernel<BLOCK, IPT, CLIP><<<(unsigned)a.ntiles, BLOCK, smem, s>>>(a);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s) {
-    return clip ? launch_bitmap_t<256, 16, true>(a, s) : launch_bitmap_t<256, 16, false>(a, s);
 }
 
 void launch_clip(const ClipArgs& a, cudaStream_t s) {
