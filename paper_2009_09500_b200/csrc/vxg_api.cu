@@ -99,7 +99,6 @@ struct vxg_context {
     int64_t err_seg = -1;
     int64_t launches = 0;
     int list_variant = 0;
-    int debug = 0;  // VXG_DEBUG (diagnostics only)
     DeviceCache cache;
     Control* h_ctl = nullptr;  // pinned readback slot
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -154,7 +153,8 @@ struct vxg_batch {
     vxg_context* ctx = nullptr;
     int64_t n = 0;
     const double* d_segs = nullptr;  // owned (segs) or borrowed device pointer
-    DBuf segs, rec, steps, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl, scratch;
+    DBuf segs, rec, steps, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl, counts,
+        prefix;
     int64_t max_steps = 0, capacity = 0;
     float plan_ms = 0.f, emit_ms = 0.f, aux_ms = 0.f;  // plan kernel / emit kernel / tile index + clip
     vxg_timing timing{0, 0, 0};
@@ -280,25 +280,34 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
     vxg_context* ctx = b->ctx;
     const int ts_log2 = vxg::list_chunk_log2(ctx->list_variant);
     const int64_t nchunks = ceil_div(b->capacity, 1ll << ts_log2);
-    const int64_t nstatus = nchunks;  // one look-back status word per warp chunk
+    const int64_t nscan = vxg::scan_tile_count(nchunks);
     if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)nchunks) ||
-        !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)std::max<int64_t>(nstatus, vxg::plan_tile_count(b->n))))
+        !b->counts.ensure(ctx, sizeof(int) * (size_t)nchunks) ||
+        !b->prefix.ensure(ctx, sizeof(long long) * (size_t)(nchunks + 1)) ||
+        !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)std::max<int64_t>(nscan, vxg::plan_tile_count(b->n))))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
     if ((reinterpret_cast<uintptr_t>(d_out) & 3u) != 0)
         return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_voxelize: output must be 4-byte aligned");
     cudaMemsetAsync(ctl_slot(b, 1), 0, sizeof(Control), ctx->stream);
-    cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)nstatus, ctx->stream);
+    cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)nscan, ctx->stream);
     cudaEventRecord(ctx->ev[2], ctx->stream);
     vxg::launch_tile_index(b->off.as<long long>(), b->n, ts_log2, b->tile_seg.as<long long>(),
                            ctx->stream);
-    cudaEventRecord(ctx->ev[3], ctx->stream);
     vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->tile_seg.as<long long>(),
                     b->n, b->capacity, nchunks, d_out, out_cap, d_chain,
-                    b->status.as<unsigned long long>(), ctl_slot(b, 1), ctx->debug};
-    cudaError_t e = vxg::launch_emit_list(a, ctx->list_variant, ctx->stream);
-    ctx->launches += 2;
+                    b->counts.as<int>(), b->prefix.as<long long>(), ctl_slot(b, 1)};
+    cudaError_t e = vxg::launch_list_phase(a, ctx->list_variant, 0, ctx->stream);  // count
+    vxg::ScanArgs sa{b->counts.as<int>(), nchunks, b->prefix.as<long long>(),
+                     b->status.as<unsigned long long>(), ctl_slot(b, 1)};
+    if (e == cudaSuccess) {
+        vxg::launch_scan_counts(sa, ctx->stream);
+        cudaMemsetAsync(&ctl_slot(b, 1)->tile_counter, 0, sizeof(unsigned long long), ctx->stream);
+        cudaEventRecord(ctx->ev[3], ctx->stream);
+        e = vxg::launch_list_phase(a, ctx->list_variant, 1, ctx->stream);  // emit
+    }
+    ctx->launches += 4;
     cudaEventRecord(ctx->ev[4], ctx->stream);
-    if (e != cudaSuccess) return ctx->cuda_fail(e, "emit_list_kernel");
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "list emit");
     Control c;
     vxg_status s = read_ctl(ctx, ctl_slot(b, 1), c, "batch_voxelize");
     cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);
@@ -408,7 +417,6 @@ VXG_API vxg_status vxg_create(int device, vxg_context** out) {
     }
     ctx->own_stream = true;
     if (const char* v = std::getenv("VXG_LIST_VARIANT")) ctx->list_variant = std::atoi(v);
-    if (const char* v = std::getenv("VXG_DEBUG")) ctx->debug = std::atoi(v);
     *out = ctx;
     return VXG_OK;
 }

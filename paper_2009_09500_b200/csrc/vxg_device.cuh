@@ -17,11 +17,31 @@ struct alignas(16) SegRec {
     double sx, sy, sz;   // S
     double wx, wy, wz;   // W = (E - S) / N
     int32_t ex, ey, ez;  // round_point(E): the k == N sample (include/voxline/parametric.hpp:43)
-    uint32_t flags;      // REC_CHECK: samples can approach the int32 edge -> checked rounding
+    uint32_t flags;      // REC_* below
 };
 static_assert(sizeof(SegRec) == 64, "SegRec must be 64 B");
 
-enum : uint32_t { REC_CHECK = 1u };
+enum : uint32_t {
+    REC_CHECK = 1u,  // samples can approach the int32 edge -> checked rounding, generic path
+    REC_WIDE = 2u,   // some |W| > 1 (only from caller-supplied plans) -> exact dedup, generic path
+    REC_POS = 4u,    // every coordinate of S and E >= 1: samples are positive, round = trunc(x+.5)
+};
+
+// Voxel key for consecutive-duplicate tests: x + 8y + 64z (mod 2^32). Consecutive samples of one
+// segment differ by |W| <= 1 per axis plus a few ulp, so their voxels differ by at most 2 per
+// axis, and dx + 8dy + 64dz with |d| <= 3 vanishes only for d == 0: within a segment the key
+// equality is exactly voxel equality. (Records with |W| > 1 carry REC_WIDE and compare exactly.)
+__device__ __forceinline__ int32_t voxel_key(int32_t x, int32_t y, int32_t z) {
+    return x + 8 * y + 64 * z;
+}
+
+// llround for samples known to lie in (-0.5, 2^31): a = RZ(c + 0.5) is >= 0 and floor(a) ==
+// llround(c); RZ(a + 2^52) = 2^52 + floor(a) exactly (the binade [2^52, 2^53) has ulp 1), so
+// the integer is the low word of the mantissa. Two DADDs on the FP64 pipe, no F2I conversion
+// (F2I.F64 issues at 16/clk/SM, a quarter of the DADD rate).
+__device__ __forceinline__ int32_t round_pos(double c) {
+    return __double2loint(__dadd_rz(__dadd_rz(c, 0.5), 0x1p52));
+}
 
 // Endpoints whose magnitude exceeds this get per-sample range checks in the emit kernels;
 // below it every sample S + W*k (k < N) provably rounds inside the int32 lattice because it lies
@@ -114,7 +134,9 @@ __device__ __forceinline__ uint32_t rec_flags(double sx, double sy, double sz, d
                                               double ey, double ez) {
     const double m = fmax(fmax(fmax(fabs(sx), fabs(sy)), fmax(fabs(sz), fabs(ex))),
                           fmax(fabs(ey), fabs(ez)));
-    return m > kCheckThreshold ? REC_CHECK : 0u;
+    const double lo = fmin(fmin(fmin(sx, sy), fmin(sz, ex)), fmin(ey, ez));
+    // samples lie between S and E up to a few ulp: all >= 1 - tiny > -0.5 when lo >= 1
+    return (m > kCheckThreshold ? REC_CHECK : 0u) | (lo >= 1.0 ? REC_POS : 0u);
 }
 
 // ----------------------------------------------------------------------------- SplitMix64
@@ -194,31 +216,33 @@ __device__ __forceinline__ long long lookback_resolve(unsigned long long* status
     const int lane = threadIdx.x & 31;
     if (tile == 0) return 0;
     long long excl = 0;
-    long long end = tile;  // examine tiles [end-32, end)
+    long long end = tile;  // examine tiles [end-32, end), lane i <-> tile end-1-i
     while (true) {
         const long long j = end - 1 - lane;
-        unsigned long long s;
-        if (j >= 0) {
-            unsigned spins = 0;
-            do {
-                s = ld_relaxed_u64(&status[j]);
-                if ((++spins & 1023u) == 0) {
-                    if (spins >= kSpinLimit) atomicExch(&ctl->abort, 1);
-                    if (*reinterpret_cast<volatile int*>(&ctl->abort)) {
-                        s = kFlagP;  // give up (the call fails with a logic error)
-                        break;
-                    }
+        unsigned long long s = j >= 0 ? ld_relaxed_u64(&status[j]) : kFlagP;  // virtual P before 0
+        unsigned pmask, need;
+        unsigned spins = 0;
+        // Wait only for the tiles nearer than the nearest inclusive prefix (lanes 0..stop); tiles
+        // beyond it are irrelevant even if they have not published yet.
+        while (true) {
+            pmask = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+            const unsigned xmask = __ballot_sync(0xffffffffu, (s >> 62) == 0);
+            need = pmask ? (0xffffffffu >> (31 - (__ffs(pmask) - 1))) : 0xffffffffu;
+            if (!(xmask & need)) break;
+            if (((xmask & need) >> lane) & 1u) s = ld_relaxed_u64(&status[j]);
+            if ((++spins & 255u) == 0) {  // (spins is warp-uniform)
+                if (spins >= (kSpinLimit >> 2) && lane == 0) atomicExch(&ctl->abort, 1);
+                const int ab = *reinterpret_cast<volatile int*>(&ctl->abort);
+                if (__any_sync(0xffffffffu, ab != 0)) {  // give up: the call fails (logic error)
+                    s = kFlagP;
+                    pmask = 1u;
+                    need = 1u;
+                    break;
                 }
-            } while ((s >> 62) == 0);
-        } else {
-            s = kFlagP;  // virtual prefix 0 before tile 0
+            }
         }
-        const unsigned int pmask = __ballot_sync(0xffffffffu, (s >> 62) == 2);
         long long v = (long long)(s & kValMask);
-        if (pmask) {
-            const int stop = __ffs(pmask) - 1;  // nearest inclusive prefix
-            if (lane > stop) v = 0;
-        }
+        if (!((need >> lane) & 1u)) v = 0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         excl += v;

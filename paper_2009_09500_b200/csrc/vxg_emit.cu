@@ -84,226 +84,270 @@ __device__ __forceinline__ void walker_row(RowWalker& w, const long long* __rest
 }
 
 // =============================================================================== emit: list
-// Persistent, software-pipelined warps. Each warp claims groups of K consecutive chunks of
-// CH = 32*IPT samples. For every chunk it walks the rows, keeps a sample iff its voxel differs
-// from the previous sample's (k == 0 always kept), compacts the kept voxels into one of its two
-// shared-memory buffers and publishes the chunk's count (decoupled look-back, flag A). Only
-// after computing the NEXT chunk does it resolve the previous chunk's output position, write the
-// chain offsets of the segments starting in it and stream it out with 16-B stores: by then its
-// predecessors have long published, so the look-back rarely spins.
+// Two passes over fixed chunks of CH = 32*IPT consecutive flat samples (the paper's
+// N_P x (N_max + 1) grid without redundant items), batch_voxelize's kernel and assemble phases
+// (src/batch.cpp:107-150) fused:
+//   list_count_kernel : kept (deduplicated) voxels per chunk -- pure compute, no shared memory
+//   scan_counts       : exclusive prefix of the counts (decoupled look-back, vxg_kernels.cu)
+//   list_emit_kernel  : recompute the chunk knowing its output position, stage the kept voxels in
+//                       shared memory at their final 16-B alignment and stream them out with one
+//                       TMA bulk store (cp.async.bulk) plus 4-B head/tail words
+// Recomputing the samples costs ~13 FP64 ops per sample and buys a pass without any inter-warp
+// waiting (a single-pass look-back stalls on predecessors and needs double-buffered staging).
 //
-// Rows without an entry boundary (most rows: config-4 segments are ~1000 samples long) take a
-// fast path: one warp-uniform record, t = (row_start - so_c) + lane, S + W*t, llround, compare
-// with the neighbour lane. The k == N (E) sample always lies in a boundary row. Boundary rows,
-// partially valid rows and records that need checked rounding take the generic path.
-struct ChunkState {
-    long long chunk, wbase, wend, c_first, c_last;
-    int count;
-    unsigned mask;  // lane j: keep mask of row j
-    int rowbase;    // lane j: kept voxels before row j
+// A warp walks its chunk in rows of 32 consecutive samples. Rows without an entry boundary (most
+// rows: config-4 segments are ~1000 samples long) take the fast path: one warp-uniform record,
+// t = (row_start - so_c) + lane, S + W*t, llround, and a keep flag from comparing the voxel key
+// with the neighbour lane's (lane 0: the previous row's lane 31). The k == N (E) sample always
+// lies in a boundary row. Boundary rows, partial rows and records that need checked rounding or
+// exact comparison take the generic path through the row walker.
+
+// Walker state carried from one chunk to the next consecutive one (same warp): the entry of the
+// next sample, its record and the key of the last sample.
+struct WalkCtx {
+    RowWalker w;
+    SegRec R;       // record of entry w.c (warp-uniform)
+    int32_t carry;  // voxel key of the sample before the next row (if in entry w.c)
+    bool valid;
 };
 
 template <int IPT>
-__device__ __forceinline__ void list_compute(const ListArgs& a, long long chunk,
-                                             unsigned char* region, ChunkState& cs) {
+__device__ __forceinline__ void walk_init(const ListArgs& a, long long chunk, WalkCtx& wc) {
+    constexpr int CH = 32 * IPT;
+    const long long wbase = chunk * CH;
+    RowWalker& w = wc.w;
+    w.c = __ldg(a.tile_seg + chunk);  // entry containing the chunk's first sample
+    w.so_c = __ldg(a.off + w.c);
+    w.so_next = __ldg(a.off + w.c + 1);
+    wc.R = load_rec(a.rec + w.c);
+    wc.carry = 0;
+    if (wbase > w.so_c) {
+        int32_t px, py, pz;
+        bool b = false;
+        eval_sample(wc.R, wbase - 1 - w.so_c, w.so_next - w.so_c - 1, px, py, pz, b);
+        wc.carry = voxel_key(px, py, pz);
+    }
+    wc.valid = true;
+}
+
+// Walk one chunk. EMIT: stage kept voxels at stage + 12*rank and keep per-row masks / bases
+// (lane j holds row j's) for the chain offsets. Returns the chunk's kept count (warp-uniform).
+template <int IPT, bool EMIT>
+__device__ __forceinline__ int walk_chunk(const ListArgs& a, long long chunk, WalkCtx& wc,
+                                          unsigned char* stage, unsigned& my_mask,
+                                          int& my_rowbase) {
     constexpr int CH = 32 * IPT;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    int32_t* reg32 = reinterpret_cast<int32_t*>(region);
     const long long wbase = chunk * CH;
     const long long wend = min(wbase + (long long)CH, a.total_samples);
-    const long long e_lo = __ldg(a.tile_seg + chunk);
-    const long long e_hi = chunk + 1 < a.nchunks ? __ldg(a.tile_seg + chunk + 1) : a.nseg - 1;
-    RowWalker w;
-    walker_init(w, a.off, e_lo, e_hi, wbase);
-    cs.chunk = chunk;
-    cs.wbase = wbase;
-    cs.wend = wend;
-    cs.c_first = w.c;
-    SegRec R = load_rec(a.rec + w.c);  // record of entry w.c (warp-uniform)
-
-    // voxel of sample wbase - 1 when it belongs to the same entry (lane 0's previous sample)
-    int32_t cx = 0, cy = 0, cz = 0;
+    if (!wc.valid) walk_init<IPT>(a, chunk, wc);
+    RowWalker& w = wc.w;
+    SegRec& R = wc.R;
+    int32_t& carry = wc.carry;
     bool bad = false;
     long long bad_seg = 0;
-    if (wbase > w.so_c) {
-        bool b = false;
-        eval_sample(R, wbase - 1 - w.so_c, w.so_next - w.so_c - 1, cx, cy, cz, b);
-    }
     const double lane_d = (double)lane;
     int running = 0;
-    unsigned my_mask = 0;
-    int my_rowbase = 0;
-#pragma unroll 1
-    for (int j = 0; j < IPT; ++j) {
-        const long long row_start = wbase + (long long)j * 32;
-        if (row_start >= wend) break;
-        int32_t x, y, z;
-        bool keep;
-        if (w.so_next > row_start + 32 && row_start + 32 <= wend && !(R.flags & REC_CHECK)) {
-            // ---- fast path: 32 consecutive samples of one entry, none of them the last
-            const double t = __dadd_rn(__ll2double_rn(row_start - w.so_c), lane_d);
-            x = round_fast(sample_axis(R.sx, R.wx, t));
-            y = round_fast(sample_axis(R.sy, R.wy, t));
-            z = round_fast(sample_axis(R.sz, R.wz, t));
-            int32_t px = __shfl_up_sync(0xffffffffu, x, 1);
-            int32_t py = __shfl_up_sync(0xffffffffu, y, 1);
-            int32_t pz = __shfl_up_sync(0xffffffffu, z, 1);
-            if (lane == 0) {
-                px = cx;
-                py = cy;
-                pz = cz;
-            }
-            keep = (lane == 0 && row_start == w.so_c) || x != px || y != py || z != pz;
-        } else {
-            // ---- generic path
-            const long long c_before = w.c;
-            long long e, st, nx;
-            walker_row(w, a.off, a.nseg, row_start, e, st, nx);
-            const long long f = row_start + lane;
-            const bool valid = f < wend;
-            long long k = 0;
-            x = y = z = 0;
-            if (valid) {
-                const SegRec rr = e == c_before ? R : load_rec(a.rec + e);
-                k = f - st;
-                bool b = false;
-                eval_sample(rr, k, nx - st - 1, x, y, z, b);
-                if (b) {
-                    bad = true;
-                    bad_seg = e;
-                }
-            }
-            int32_t px = __shfl_up_sync(0xffffffffu, x, 1);
-            int32_t py = __shfl_up_sync(0xffffffffu, y, 1);
-            int32_t pz = __shfl_up_sync(0xffffffffu, z, 1);
-            if (lane == 0) {
-                px = cx;
-                py = cy;
-                pz = cz;
-            }
-            keep = valid && (k == 0 || x != px || y != py || z != pz);
-            // (the walker may step one past the last entry at the end of the sample space)
-            if (w.c != c_before && w.c < a.nseg) R = load_rec(a.rec + w.c);
-        }
-        cx = __shfl_sync(0xffffffffu, x, 31);
-        cy = __shfl_sync(0xffffffffu, y, 31);
-        cz = __shfl_sync(0xffffffffu, z, 31);
+
+    auto commit = [&](int j, bool keep, int32_t x, int32_t y, int32_t z) {
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
-        if (keep) {
-            int32_t* d = reg32 + 3 * (running + __popc(mask & lt));
-            d[0] = x;
-            d[1] = y;
-            d[2] = z;
-        }
-        if (lane == j) {
-            my_mask = mask;
-            my_rowbase = running;
+        if (EMIT) {
+            if (keep) {
+                uint32_t* d = reinterpret_cast<uint32_t*>(stage + 12 * (running + __popc(mask & lt)));
+                d[0] = (uint32_t)x;
+                d[1] = (uint32_t)y;
+                d[2] = (uint32_t)z;
+            }
+            if (lane == j) {
+                my_mask = mask;
+                my_rowbase = running;
+            }
         }
         running += __popc(mask);
+    };
+
+    int j = 0;
+    while (j < IPT) {
+        const long long row_start = wbase + (long long)j * 32;
+        if (row_start >= wend) break;
+        // ---- fast rows: row r is fast iff row_start_r + 32 <= min(so_next - 1, wend)
+        const long long lim = min(w.so_next - 1, wend);
+        int nfast = 0;
+        if (!(R.flags & (REC_CHECK | REC_WIDE)) && lim >= row_start + 32)
+            nfast = (int)min((lim - row_start) >> 5, (long long)(IPT - j));
+        if (nfast > 0) {
+            double t = __dadd_rn(__ll2double_rn(row_start - w.so_c), lane_d);
+            const bool first0 = lane == 0 && row_start == w.so_c;  // k == 0 at lane 0, row 0
+            if (R.flags & REC_POS) {
+#pragma unroll 2
+                for (int f = 0; f < nfast; ++f) {
+                    const int32_t x = round_pos(sample_axis(R.sx, R.wx, t));
+                    const int32_t y = round_pos(sample_axis(R.sy, R.wy, t));
+                    const int32_t z = round_pos(sample_axis(R.sz, R.wz, t));
+                    const int32_t key = voxel_key(x, y, z);
+                    int32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
+                    if (lane == 0) pk = carry;
+                    carry = __shfl_sync(0xffffffffu, key, 31);
+                    commit(j + f, key != pk || (f == 0 && first0), x, y, z);
+                    t = __dadd_rn(t, 32.0);
+                }
+            } else {
+#pragma unroll 2
+                for (int f = 0; f < nfast; ++f) {
+                    const int32_t x = round_fast(sample_axis(R.sx, R.wx, t));
+                    const int32_t y = round_fast(sample_axis(R.sy, R.wy, t));
+                    const int32_t z = round_fast(sample_axis(R.sz, R.wz, t));
+                    const int32_t key = voxel_key(x, y, z);
+                    int32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
+                    if (lane == 0) pk = carry;
+                    carry = __shfl_sync(0xffffffffu, key, 31);
+                    commit(j + f, key != pk || (f == 0 && first0), x, y, z);
+                    t = __dadd_rn(t, 32.0);
+                }
+            }
+            j += nfast;
+            continue;
+        }
+        // ---- generic row: entry boundaries, the k == N sample, partial rows, checked records
+        const long long c_before = w.c;
+        long long e, st, nx;
+        walker_row(w, a.off, a.nseg, row_start, e, st, nx);
+        const long long f = row_start + lane;
+        const bool valid = f < wend;
+        long long k = 0;
+        int32_t x = 0, y = 0, z = 0, px = 0, py = 0, pz = 0;
+        SegRec rr = R;
+        if (valid) {
+            if (e != c_before) rr = load_rec(a.rec + e);
+            k = f - st;
+            bool b = false;
+            eval_sample(rr, k, nx - st - 1, x, y, z, b);
+            if (b) {
+                bad = true;
+                bad_seg = e;
+            }
+        }
+        px = __shfl_up_sync(0xffffffffu, x, 1);
+        py = __shfl_up_sync(0xffffffffu, y, 1);
+        pz = __shfl_up_sync(0xffffffffu, z, 1);
+        bool same;
+        if (lane == 0) {
+            // lane 0's previous sample (same entry iff k > 0): the carried key, or recomputed
+            // exactly for records whose |W| > 1 (key equality is exact only for small steps)
+            if (rr.flags & REC_WIDE) {
+                bool b = false;
+                if (valid && k > 0) eval_sample(rr, k - 1, nx - st - 1, px, py, pz, b);
+                same = x == px && y == py && z == pz;
+            } else {
+                same = voxel_key(x, y, z) == carry;
+            }
+        } else {
+            same = x == px && y == py && z == pz;
+        }
+        carry = __shfl_sync(0xffffffffu, voxel_key(x, y, z), 31);
+        commit(j, valid && (k == 0 || !same), x, y, z);
+        // (the walker may step one past the last entry at the end of the sample space)
+        if (w.c != c_before && w.c < a.nseg) R = load_rec(a.rec + w.c);
+        ++j;
     }
     if (bad) record_error(a.ctl, bad_seg, 2);
-    cs.c_last = w.c;
-    cs.count = running;
-    cs.mask = my_mask;
-    cs.rowbase = my_rowbase;
+    // the walker now stands at sample wend: valid for chunk + 1 unless this was the last chunk
+    wc.valid = wend == wbase + CH && w.c < a.nseg;
+    return running;
 }
 
-template <int IPT>
-__device__ __forceinline__ void list_finish(const ListArgs& a, const ChunkState& cs,
-                                            const unsigned char* region) {
-    const int lane = threadIdx.x & 31;
-    const long long prefix = (a.debug & 1)
-                                 ? cs.wbase
-                                 : lookback_resolve(a.status, cs.chunk, (long long)cs.count, a.ctl);
-    // chain offsets of the entries whose k = 0 sample lies in the chunk (always kept)
-    for (long long q0 = cs.c_first; q0 <= cs.c_last; q0 += 32) {
-        const long long q = q0 + lane;
-        const long long st = q <= cs.c_last ? __ldg(a.off + q) : -1;
-        const bool in = st >= cs.wbase && st < cs.wend;
-        const int loc = in ? (int)(st - cs.wbase) : 0;
-        const unsigned mk = __shfl_sync(0xffffffffu, cs.mask, loc >> 5);
-        const int rb = __shfl_sync(0xffffffffu, cs.rowbase, loc >> 5);
-        if (in) a.chain_off[q] = prefix + rb + __popc(mk & ((1u << (loc & 31)) - 1u));
+// Pass 1: one warp per G consecutive chunks (walker carried across them).
+template <int NW, int IPT, int G>
+__global__ void __launch_bounds__(NW * 32) list_count_kernel(ListArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long first = ((long long)blockIdx.x * NW + warp) * G;
+    if (first >= a.nchunks) return;
+    WalkCtx wc;
+    wc.valid = false;
+    unsigned m;
+    int rb;
+    for (int q = 0; q < G; ++q) {
+        const long long chunk = first + q;
+        if (chunk >= a.nchunks) break;
+        const int cnt = walk_chunk<IPT, false>(a, chunk, wc, nullptr, m, rb);
+        if (lane == 0) a.counts[chunk] = cnt;
     }
-    if (cs.wend == a.total_samples && lane == 0) {
-        a.chain_off[a.nseg] = prefix + cs.count;
-        a.ctl->total = prefix + cs.count;
-    }
-    if (prefix + cs.count > a.out_cap) {
-        if (lane == 0) record_error(a.ctl, cs.c_first, 4);
-        __syncwarp();
-        return;
-    }
-    // region bytes [0, 12*count) -> out + 12*prefix, 16-B stores, unaligned head/tail words
+}
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// Pass 2: one warp per chunk; the chunk's output position is known before it starts.
+template <int NW, int IPT>
+__global__ void __launch_bounds__(NW * 32) list_emit_kernel(ListArgs a) {
+    constexpr int CH = 32 * IPT;
+    constexpr int REGION = CH * 12 + 16;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long chunk = (long long)blockIdx.x * NW + warp;
+    if (chunk >= a.nchunks) return;
+    unsigned char* region = smem + warp * REGION;
+    const long long prefix = __ldg(a.chunk_prefix + chunk);
     const uintptr_t g0 = reinterpret_cast<uintptr_t>(a.out) + 12ull * (unsigned long long)prefix;
     const int head = (int)(g0 & 15u);
-    const int nbytes = 12 * cs.count;
-    const int nchunks = (head + nbytes + 15) >> 4;
-    unsigned char* gbase = reinterpret_cast<unsigned char*>(g0 - (uintptr_t)head);
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(region);
-    for (int ch = lane; ch < nchunks; ch += 32) {
-        const int lo = (ch << 4) - head;  // region byte of the 16-B chunk's first word
-        if (lo >= 0 && lo + 16 <= nbytes) {
-            uint4 v;
-            v.x = src[(lo >> 2) + 0];
-            v.y = src[(lo >> 2) + 1];
-            v.z = src[(lo >> 2) + 2];
-            v.w = src[(lo >> 2) + 3];
-            st_stream_v4(gbase + (ch << 4), v);
-        } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int b = lo + 4 * q;
-                if (b >= 0 && b < nbytes)
-                    *reinterpret_cast<uint32_t*>(gbase + (ch << 4) + 4 * q) = src[b >> 2];
-            }
-        }
+    unsigned char* stage = region + head;  // stage byte b <-> global byte g0 + b, same mod 16
+    WalkCtx wc;
+    wc.valid = false;
+    unsigned my_mask = 0;
+    int my_rowbase = 0;
+    const long long wbase = chunk * CH;
+    const long long wend = min(wbase + (long long)CH, a.total_samples);
+    walk_init<IPT>(a, chunk, wc);
+    const long long c_first = wc.w.c;
+    const int count = walk_chunk<IPT, true>(a, chunk, wc, stage, my_mask, my_rowbase);
+    const long long c_last = wc.w.c;
+    const long long last = prefix + count;
+    if (last > a.out_cap) {  // caller's buffer too small: report, write nothing
+        if (lane == 0) record_error(a.ctl, c_first, 4);
+        return;
     }
-    __syncwarp();  // the region may be overwritten by the warp's next chunk
-}
-
-// Persistent warps claim groups of K consecutive chunks. A warp computes and publishes ALL K
-// chunks of its group (into K shared-memory buffers) before it resolves any of them, so the
-// aggregate of every claimed chunk is published without waiting on anything: a resolution waits
-// at most for chunks claimed earlier by other warps, never on a chain of resolutions (an
-// interleaved compute/resolve order inside a group serialises the warps). Only the group's first
-// resolution can wait; the others find their predecessor (the warp's own chunk) resolved.
-template <int NWB, int IPT, int K, int MINB>
-__global__ void __launch_bounds__(NWB * 32, MINB) emit_list_kernel(ListArgs a) {
-    static_assert(IPT <= 32, "row bookkeeping is kept one row per lane");
-    constexpr int CH = 32 * IPT;
-    extern __shared__ __align__(16) unsigned char smem[];  // per warp: K buffers of CH*12 bytes
-    __shared__ ChunkState s_state[NWB][K];                 // lane 0's scalars of each chunk
-    __shared__ unsigned s_mask[NWB][K][IPT];
-    __shared__ int s_rowbase[NWB][K][IPT];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned char* buf0 = smem + (size_t)warp * K * CH * 12;
-    while (true) {
-        long long g = 0;
-        if (lane == 0) g = (long long)atomicAdd(&a.ctl->tile_counter, (unsigned long long)K);
-        g = __shfl_sync(0xffffffffu, g, 0);
-        if (g >= a.nchunks) break;
-        const int nq = (int)min((long long)K, a.nchunks - g);
-        for (int q = 0; q < nq; ++q) {
-            ChunkState cs;
-            list_compute<IPT>(a, g + q, buf0 + q * CH * 12, cs);
-            if (lane == 0) {
-                if (!(a.debug & 1)) lookback_publish(a.status, g + q, cs.count);
-                s_state[warp][q] = cs;
-            }
-            if (lane < IPT) {
-                s_mask[warp][q][lane] = cs.mask;
-                s_rowbase[warp][q][lane] = cs.rowbase;
-            }
+    // chain offsets of the entries whose k = 0 sample lies in the chunk (always kept)
+    for (long long q0 = c_first; q0 <= c_last; q0 += 32) {
+        const long long q = q0 + lane;
+        const long long st = q <= c_last && q < a.nseg ? __ldg(a.off + q) : -1;
+        const bool in = st >= wbase && st < wend;
+        const int loc = in ? (int)(st - wbase) : 0;
+        const unsigned mk = __shfl_sync(0xffffffffu, my_mask, loc >> 5);
+        const int rb = __shfl_sync(0xffffffffu, my_rowbase, loc >> 5);
+        if (in) a.chain_off[q] = prefix + rb + __popc(mk & ((1u << (loc & 31)) - 1u));
+    }
+    if (wend == a.total_samples && lane == 0) {
+        a.chain_off[a.nseg] = last;
+        a.ctl->total = last;
+    }
+    // stream out: global bytes [g0, g1); the 16-B aligned middle by one bulk copy
+    const uintptr_t g1 = g0 + 12ull * (unsigned)count;
+    const uintptr_t a0 = (g0 + 15) & ~(uintptr_t)15;
+    const uintptr_t a1 = g1 & ~(uintptr_t)15;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // STS -> async proxy
+    __syncwarp();
+    if (a1 > a0) {
+        if (lane == 0) {
+            bulk_store(reinterpret_cast<void*>(a0), stage + (a0 - g0), (unsigned)(a1 - a0));
         }
-        __syncwarp();
-        for (int q = 0; q < nq; ++q) {
-            ChunkState cs = s_state[warp][q];
-            cs.mask = lane < IPT ? s_mask[warp][q][lane] : 0u;
-            cs.rowbase = lane < IPT ? s_rowbase[warp][q][lane] : 0;
-            list_finish<IPT>(a, cs, buf0 + q * CH * 12);
-        }
+        // head words [g0, a0) and tail words [a1, g1)
+        const int hw = (int)((a0 - g0) >> 2), tw = (int)((g1 - a1) >> 2);
+        if (lane < hw)
+            reinterpret_cast<uint32_t*>(g0)[lane] = reinterpret_cast<const uint32_t*>(stage)[lane];
+        else if (lane >= 4 && lane - 4 < tw)
+            reinterpret_cast<uint32_t*>(a1)[lane - 4] =
+                reinterpret_cast<const uint32_t*>(stage + (a1 - g0))[lane - 4];
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    } else {
+        const int nw = (int)((g1 - g0) >> 2);  // fewer than 8 words
+        if (lane < nw)
+            reinterpret_cast<uint32_t*>(g0)[lane] = reinterpret_cast<const uint32_t*>(stage)[lane];
     }
 }
 
@@ -408,47 +452,40 @@ __global__ void __launch_bounds__(NW * 32) emit_bitmap_kernel(BitmapArgs a) {
 }
 
 // =============================================================================== launchers
-template <int NWB, int IPT, int K, int MINB>
-static cudaError_t launch_list_t(const ListArgs& a, cudaStream_t s) {
-    const size_t smem = (size_t)NWB * K * 32 * IPT * 12;
-    static int grid_cap = 0;
-    if (!grid_cap) {
-        cudaFuncSetAttribute(emit_list_kernel<NWB, IPT, K, MINB>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, emit_list_kernel<NWB, IPT, K, MINB>,
-                                                      NWB * 32, smem);
-        grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+// list launch shape: NW warps per block, IPT rows per chunk (CH = 32*IPT samples), G chunks per
+// counting warp. variant 0 = 8 x 16 x 4 (512-sample chunks, 6 KB staging per warp),
+// 1 = 8 x 32 x 2 (1024-sample chunks, 12 KB), 2 = 8 x 8 x 8 (256, 3 KB).
+template <int NW, int IPT, int G>
+static cudaError_t launch_list_t(const ListArgs& a, int phase, cudaStream_t s) {
+    if (phase == 0) {
+        const long long warps = (a.nchunks + G - 1) / G;
+        list_count_kernel<NW, IPT, G><<<(unsigned)((warps + NW - 1) / NW), NW * 32, 0, s>>>(a);
+    } else {
+        const size_t smem = (size_t)NW * (32 * IPT * 12 + 16);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(list_emit_kernel<NW, IPT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        list_emit_kernel<NW, IPT><<<(unsigned)((a.nchunks + NW - 1) / NW), NW * 32, smem, s>>>(a);
     }
-    const long long groups = (a.nchunks + (long long)NWB * K - 1) / ((long long)NWB * K);
-    const int grid = (int)(groups < grid_cap ? groups : grid_cap);
-    emit_list_kernel<NWB, IPT, K, MINB><<<grid > 0 ? grid : 1, NWB * 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 
-// variant -> (warps per block, rows per chunk, chunks per claim, min blocks per SM):
-//   0 = 4 x 16 x 2 x 4 (512-sample chunks, 12 KB smem per warp, 16 warps/SM)
-//   1 = 4 x 8 x 4 x 4  (256-sample chunks, 12 KB per warp, 16 warps/SM)
-//   2 = 4 x 8 x 2 x 8  (256, 6 KB per warp, 32 warps/SM, 64 registers)
-//   3 = 8 x 16 x 2 x 2 (512, 12 KB per warp, 16 warps/SM)
-//   4 = 4 x 16 x 1 x 8 (512, 6 KB per warp, one claim per chunk, 32 warps/SM)
 int list_chunk_log2(int variant) {
     switch (variant) {
-        case 1: return 8;
+        case 1: return 10;
         case 2: return 8;
         default: return 9;
     }
 }
 
-cudaError_t launch_emit_list(const ListArgs& a, int variant, cudaStream_t s) {
+cudaError_t launch_list_phase(const ListArgs& a, int variant, int phase, cudaStream_t s) {
     switch (variant) {
-        case 1: return launch_list_t<4, 8, 4, 4>(a, s);
-        case 2: return launch_list_t<4, 8, 2, 8>(a, s);
-        case 3: return launch_list_t<8, 16, 2, 2>(a, s);
-        case 4: return launch_list_t<4, 16, 1, 8>(a, s);
-        default: return launch_list_t<4, 16, 2, 4>(a, s);
+        case 1: return launch_list_t<8, 32, 2>(a, phase, s);
+        case 2: return launch_list_t<8, 8, 8>(a, phase, s);
+        default: return launch_list_t<8, 16, 4>(a, phase, s);
     }
 }
 

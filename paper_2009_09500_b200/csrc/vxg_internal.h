@@ -33,9 +33,17 @@ struct ListArgs {
     int32_t* out;               // 3 int32 per voxel, 4-B aligned
     long long out_cap;
     long long* chain_off;       // nseg + 1
+    int* counts;                // nchunks: kept voxels per chunk (count pass)
+    const long long* chunk_prefix;  // nchunks + 1: exclusive prefix of counts (emit pass)
+    Control* ctl;
+};
+
+struct ScanArgs {  // exclusive scan of n int counts -> n + 1 long long prefixes
+    const int* in;
+    long long n;
+    long long* out;
     unsigned long long* status;
     Control* ctl;
-    int debug;                  // VXG_DEBUG bit 0: skip the look-back (diagnostics only)
 };
 
 struct BitmapArgs {
@@ -79,7 +87,10 @@ int bitmap_tile_log2();
 void launch_plan(const PlanArgs& a, cudaStream_t s);
 void launch_tile_index(const long long* off, long long n_entries, int ts_log2, long long* tile_seg,
                        cudaStream_t s);
-cudaError_t launch_emit_list(const ListArgs& a, int variant, cudaStream_t s);
+// phase 0 = count pass, 1 = emit pass
+cudaError_t launch_list_phase(const ListArgs& a, int variant, int phase, cudaStream_t s);
+int scan_tile_count(long long n);
+void launch_scan_counts(const ScanArgs& a, cudaStream_t s);
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
 void launch_clip(const ClipArgs& a, cudaStream_t s);
 void launch_round_points(const double* p, long long n, int32_t* out, Control* ctl, cudaStream_t s);

@@ -129,6 +129,17 @@ __global__ void k_i2f32(double* out, int a) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// same-address atomicAdd claims (lane 0 of every warp), as a persistent-kernel work queue does
+__global__ void k_claim(unsigned long long* ctr, unsigned long long* out, int iters) {
+    unsigned long long acc = 0;
+    for (int i = 0; i < iters; ++i) {
+        unsigned long long g = 0;
+        if ((threadIdx.x & 31) == 0) g = atomicAdd(ctr, 1ull);
+        acc += __shfl_sync(0xffffffffu, g, 0);
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
 int main() {
     int dev = 0, sms = 0, clk_khz = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -159,6 +170,23 @@ int main() {
     run("round_magic", [&] { k_round_magic<<<blocks, threads>>>((int*)d, 1.0, 0.3); }, 1);
     run("i2f_s64", [&] { k_i2f<<<blocks, threads>>>(d, 1); }, 1);
     run("i2f_s32", [&] { k_i2f32<<<blocks, threads>>>(d, 1); }, 1);
+    {
+        unsigned long long *ctr, *o;
+        cudaMalloc(&ctr, 8);
+        cudaMalloc(&o, sizeof(unsigned long long) * sms * 4 * 128);
+        const int iters = 256;
+        k_claim<<<sms * 4, 128>>>(ctr, o, iters);
+        cudaDeviceSynchronize();
+        cudaEventRecord(e0);
+        k_claim<<<sms * 4, 128>>>(ctr, o, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double claims = (double)sms * 4 * 4 * iters;
+        printf("%-14s %8.3f ms  %10.1f Mclaims/s (one global counter, %d warps)\n", "claim_atomic",
+               ms, claims / (ms / 1e3) / 1e6, sms * 16);
+    }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
