@@ -239,7 +239,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2009_09500_b200 as vx
     ctx = vx.Context(local)
-    stream = torch.cuda.current_stream()
+    # one dedicated stream for everything: the library's kernels, torch's allocations and the
+    # timing events are all ordered on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
     # ---- inputs: generated on the device by the product generator (bit-identical to oracle)

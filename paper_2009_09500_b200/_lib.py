@@ -177,7 +177,16 @@ class Context:
         raise _EXC.get(status, VoxGpuError)(msg or f"libvoxgpu status {status}", seg)
 
     def set_stream(self, stream_handle: int | None):
+        """Enqueue on a caller's cudaStream_t. None = the context's own stream; 0 (torch's
+        handle for the legacy default stream) maps to cudaStreamLegacy."""
+        if stream_handle == 0:
+            stream_handle = 1  # cudaStreamLegacy
         self.check(self.lib.vxg_set_stream(self.h, stream_handle))
+
+    def use_torch_stream(self):
+        """Order device-pointer calls after work torch queued on its current stream."""
+        import torch
+        self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
 
     @property
     def launches(self) -> int:

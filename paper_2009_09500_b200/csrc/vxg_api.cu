@@ -98,7 +98,7 @@ struct vxg_context {
     std::string err;
     int64_t err_seg = -1;
     int64_t launches = 0;
-    int list_variant = 0;
+    int num_sms = 148;
     DeviceCache cache;
     Control* h_ctl = nullptr;  // pinned readback slot
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -153,8 +153,7 @@ struct vxg_batch {
     vxg_context* ctx = nullptr;
     int64_t n = 0;
     const double* d_segs = nullptr;  // owned (segs) or borrowed device pointer
-    DBuf segs, rec, steps, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl, counts,
-        prefix;
+    DBuf segs, rec, steps, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl;
     int64_t max_steps = 0, capacity = 0;
     float plan_ms = 0.f, emit_ms = 0.f, aux_ms = 0.f;  // plan kernel / emit kernel / tile index + clip
     vxg_timing timing{0, 0, 0};
@@ -274,38 +273,30 @@ vxg_status new_batch(vxg_context* ctx, vxg_batch** out) {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Emit the voxel list into device buffers (out: >= out_cap voxels, chain: n+1).
+// Emit the voxel list into device buffers (out: >= out_cap voxels, chain: n+1): tile index +
+// the single-pass list kernel.
 vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long long* d_chain,
                             int64_t* total) {
     vxg_context* ctx = b->ctx;
-    const int ts_log2 = vxg::list_chunk_log2(ctx->list_variant);
-    const int64_t nchunks = ceil_div(b->capacity, 1ll << ts_log2);
-    const int64_t nscan = vxg::scan_tile_count(nchunks);
-    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)nchunks) ||
-        !b->counts.ensure(ctx, sizeof(int) * (size_t)nchunks) ||
-        !b->prefix.ensure(ctx, sizeof(long long) * (size_t)(nchunks + 1)) ||
-        !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)std::max<int64_t>(nscan, vxg::plan_tile_count(b->n))))
+    const int sub_log2 = vxg::list_sub_log2();
+    const int64_t nsub = ceil_div(b->capacity, 1ll << sub_log2);
+    const int64_t nchunks = ceil_div(nsub, vxg::list_nw());
+    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)nsub) ||
+        !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)std::max<int64_t>(nchunks, vxg::plan_tile_count(b->n))))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
     if ((reinterpret_cast<uintptr_t>(d_out) & 3u) != 0)
         return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_voxelize: output must be 4-byte aligned");
     cudaMemsetAsync(ctl_slot(b, 1), 0, sizeof(Control), ctx->stream);
-    cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)nscan, ctx->stream);
+    cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)nchunks, ctx->stream);
     cudaEventRecord(ctx->ev[2], ctx->stream);
-    vxg::launch_tile_index(b->off.as<long long>(), b->n, ts_log2, b->tile_seg.as<long long>(),
+    vxg::launch_tile_index(b->off.as<long long>(), b->n, sub_log2, b->tile_seg.as<long long>(),
                            ctx->stream);
+    cudaEventRecord(ctx->ev[3], ctx->stream);
     vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->tile_seg.as<long long>(),
-                    b->n, b->capacity, nchunks, d_out, out_cap, d_chain,
-                    b->counts.as<int>(), b->prefix.as<long long>(), ctl_slot(b, 1)};
-    cudaError_t e = vxg::launch_list_phase(a, ctx->list_variant, 0, ctx->stream);  // count
-    vxg::ScanArgs sa{b->counts.as<int>(), nchunks, b->prefix.as<long long>(),
-                     b->status.as<unsigned long long>(), ctl_slot(b, 1)};
-    if (e == cudaSuccess) {
-        vxg::launch_scan_counts(sa, ctx->stream);
-        cudaMemsetAsync(&ctl_slot(b, 1)->tile_counter, 0, sizeof(unsigned long long), ctx->stream);
-        cudaEventRecord(ctx->ev[3], ctx->stream);
-        e = vxg::launch_list_phase(a, ctx->list_variant, 1, ctx->stream);  // emit
-    }
-    ctx->launches += 4;
+                    b->n, b->capacity, nsub, nchunks, d_out, out_cap, d_chain,
+                    b->status.as<unsigned long long>(), ctl_slot(b, 1)};
+    const cudaError_t e = vxg::launch_list(a, ctx->num_sms, ctx->stream);
+    ctx->launches += 2;
     cudaEventRecord(ctx->ev[4], ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "list emit");
     Control c;
@@ -416,7 +407,7 @@ VXG_API vxg_status vxg_create(int device, vxg_context** out) {
         return VXG_CUDA_ERROR;
     }
     ctx->own_stream = true;
-    if (const char* v = std::getenv("VXG_LIST_VARIANT")) ctx->list_variant = std::atoi(v);
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
     *out = ctx;
     return VXG_OK;
 }

@@ -35,12 +35,14 @@ __device__ __forceinline__ int32_t voxel_key(int32_t x, int32_t y, int32_t z) {
     return x + 8 * y + 64 * z;
 }
 
-// llround for samples known to lie in (-0.5, 2^31): a = RZ(c + 0.5) is >= 0 and floor(a) ==
-// llround(c); RZ(a + 2^52) = 2^52 + floor(a) exactly (the binade [2^52, 2^53) has ulp 1), so
-// the integer is the low word of the mantissa. Two DADDs on the FP64 pipe, no F2I conversion
-// (F2I.F64 issues at 16/clk/SM, a quarter of the DADD rate).
+// llround for samples known to lie in (-0.5, 2^31): one DADD in round-toward-minus-infinity
+// against K = 2^51 + 0.5. The sum lies in [2^51, 2^52), whose ulp is 0.5, so
+// RM(c + K) = 2^51 + floor(2c + 1) / 2 exactly and the 52-bit mantissa field is F = floor(2c + 1);
+// llround(c) = floor(c + 0.5) = F >> 1 (one funnel shift on the ALU pipe). One FP64 op instead of
+// the two of an RZ add + magic-number extraction, and no F2I (quarter-rate conversion pipe).
 __device__ __forceinline__ int32_t round_pos(double c) {
-    return __double2loint(__dadd_rz(__dadd_rz(c, 0.5), 0x1p52));
+    const double d = __dadd_rd(c, 0x1.0000000000001p51);
+    return (int32_t)__funnelshift_r((unsigned)__double2loint(d), (unsigned)__double2hiint(d), 1);
 }
 
 // Endpoints whose magnitude exceeds this get per-sample range checks in the emit kernels;
@@ -205,49 +207,75 @@ __device__ __forceinline__ void lookback_publish(unsigned long long* status, lon
 
 // Resolve a tile whose aggregate was already published: accumulate predecessors back to the
 // nearest inclusive prefix, publish this tile's inclusive prefix, return the exclusive one.
-// Called by all 32 lanes of one warp.
+// Called by all 32 lanes of one warp. Each round examines a window of 32*LB predecessors (lane i
+// holds tiles end-1-LB*i-q, q < LB), so a prefix that lies a few hundred tiles back -- the
+// number of tiles in flight -- is reached in one or two L2 round trips.
 // Watchdog: a spin that outlives kSpinLimit polls (~seconds) raises Control::abort, which makes
 // every other spinning warp give up too; the kernel then terminates with a logic error instead
 // of hanging the GPU.
-constexpr unsigned kSpinLimit = 1u << 23;
+constexpr unsigned kSpinLimit = 1u << 22;
+constexpr int kLookbackItems = 4;
 
 __device__ __forceinline__ long long lookback_resolve(unsigned long long* status, long long tile,
                                                       long long aggregate, Control* ctl) {
+    constexpr int LB = kLookbackItems;
     const int lane = threadIdx.x & 31;
     if (tile == 0) return 0;
     long long excl = 0;
-    long long end = tile;  // examine tiles [end-32, end), lane i <-> tile end-1-i
+    long long end = tile;  // window: tiles [end - 32*LB, end)
     while (true) {
-        const long long j = end - 1 - lane;
-        unsigned long long s = j >= 0 ? ld_relaxed_u64(&status[j]) : kFlagP;  // virtual P before 0
-        unsigned pmask, need;
+        unsigned long long s[LB];
+#pragma unroll
+        for (int q = 0; q < LB; ++q) {
+            const long long j = end - 1 - (long long)(LB * lane + q);
+            s[q] = j >= 0 ? ld_relaxed_u64(&status[j]) : kFlagP;  // virtual P before tile 0
+        }
         unsigned spins = 0;
-        // Wait only for the tiles nearer than the nearest inclusive prefix (lanes 0..stop); tiles
-        // beyond it are irrelevant even if they have not published yet.
+        int qp;          // this lane's first item with an inclusive prefix (LB if none)
+        unsigned pmask;  // lanes holding one
         while (true) {
-            pmask = __ballot_sync(0xffffffffu, (s >> 62) == 2);
-            const unsigned xmask = __ballot_sync(0xffffffffu, (s >> 62) == 0);
-            need = pmask ? (0xffffffffu >> (31 - (__ffs(pmask) - 1))) : 0xffffffffu;
-            if (!(xmask & need)) break;
-            if (((xmask & need) >> lane) & 1u) s = ld_relaxed_u64(&status[j]);
-            if ((++spins & 255u) == 0) {  // (spins is warp-uniform)
-                if (spins >= (kSpinLimit >> 2) && lane == 0) atomicExch(&ctl->abort, 1);
+            qp = LB;
+#pragma unroll
+            for (int q = LB - 1; q >= 0; --q)
+                if ((s[q] >> 62) == 2) qp = q;
+            pmask = __ballot_sync(0xffffffffu, qp < LB);
+            const int plane = pmask ? __ffs(pmask) - 1 : 32;
+            // items that matter: everything nearer than the nearest prefix, and that prefix
+            const int lim = lane < plane ? LB : (lane == plane ? qp + 1 : 0);
+            bool missing = false;
+#pragma unroll
+            for (int q = 0; q < LB; ++q) missing |= q < lim && (s[q] >> 62) == 0;
+            if (!__any_sync(0xffffffffu, missing)) {
+                long long v = 0;
+#pragma unroll
+                for (int q = 0; q < LB; ++q)
+                    if (q < lim) v += (long long)(s[q] & kValMask);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                excl += v;
+                break;
+            }
+            // back off: a spinning warp must not steal issue slots from the warps whose
+            // aggregates it is waiting for
+            __nanosleep(spins < 64 ? 20u : 200u);
+#pragma unroll
+            for (int q = 0; q < LB; ++q) {
+                if (q < lim && (s[q] >> 62) == 0) {
+                    const long long j = end - 1 - (long long)(LB * lane + q);
+                    s[q] = ld_relaxed_u64(&status[j]);
+                }
+            }
+            if ((++spins & 63u) == 0) {  // (spins is warp-uniform)
+                if (spins >= (kSpinLimit >> 4) && lane == 0) atomicExch(&ctl->abort, 1);
                 const int ab = *reinterpret_cast<volatile int*>(&ctl->abort);
                 if (__any_sync(0xffffffffu, ab != 0)) {  // give up: the call fails (logic error)
-                    s = kFlagP;
                     pmask = 1u;
-                    need = 1u;
                     break;
                 }
             }
         }
-        long long v = (long long)(s & kValMask);
-        if (!((need >> lane) & 1u)) v = 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        excl += v;
         if (pmask) break;
-        end -= 32;
+        end -= 32 * LB;
     }
     if (lane == 0) st_relaxed_u64(&status[tile], kFlagP | (unsigned long long)(excl + aggregate));
     return excl;

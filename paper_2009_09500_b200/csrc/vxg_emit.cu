@@ -84,85 +84,79 @@ __device__ __forceinline__ void walker_row(RowWalker& w, const long long* __rest
 }
 
 // =============================================================================== emit: list
-// Two passes over fixed chunks of CH = 32*IPT consecutive flat samples (the paper's
-// N_P x (N_max + 1) grid without redundant items), batch_voxelize's kernel and assemble phases
-// (src/batch.cpp:107-150) fused:
-//   list_count_kernel : kept (deduplicated) voxels per chunk -- pure compute, no shared memory
-//   scan_counts       : exclusive prefix of the counts (decoupled look-back, vxg_kernels.cu)
-//   list_emit_kernel  : recompute the chunk knowing its output position, stage the kept voxels in
-//                       shared memory at their final 16-B alignment and stream them out with one
-//                       TMA bulk store (cp.async.bulk) plus 4-B head/tail words
-// Recomputing the samples costs ~13 FP64 ops per sample and buys a pass without any inter-warp
-// waiting (a single-pass look-back stalls on predecessors and needs double-buffered staging).
+// ONE pass fusing batch_voxelize's kernel and assemble phases (src/batch.cpp:107-150): every
+// sample is evaluated once, duplicates are dropped in registers, and the kept voxels are
+// compacted into the flat list with a single-pass decoupled look-back over CTA chunks.
 //
-// A warp walks its chunk in rows of 32 consecutive samples. Rows without an entry boundary (most
-// rows: config-4 segments are ~1000 samples long) take the fast path: one warp-uniform record,
-// t = (row_start - so_c) + lane, S + W*t, llround, and a keep flag from comparing the voxel key
-// with the neighbour lane's (lane 0: the previous row's lane 31). The k == N (E) sample always
-// lies in a boundary row. Boundary rows, partial rows and records that need checked rounding or
-// exact comparison take the generic path through the row walker.
+// Persistent CTAs of NW warps take chunk tickets in order (atomic counter, so every smaller
+// ticket is already owned by a running CTA: look-back forward progress). A chunk is NW warp
+// sub-chunks of CH = 32*IPT consecutive flat samples. Each warp walks its sub-chunk in rows of 32
+// samples, staging kept voxels (12-B records) in its shared-memory region at their chunk-local
+// rank. The CTA then publishes the chunk's count, resolves its global position by look-back, and
+// every warp streams its records out with 16-B vector stores (the global start of a sub-chunk has
+// any 4-B alignment, so the aligned middle is assembled from 4 LDS.32 per vector).
+//
+// Rows without an entry boundary (most rows: config-4 segments are ~1000 samples long) take the
+// fast path: one warp-uniform record, t = (row_start - so_c) + lane, S + W*t, llround, and a keep
+// flag from comparing the voxel key with the previous lane's (lane 0: the previous row's lane 31).
+// The k == N (E) sample always lies in a boundary row. Boundary rows, partial rows and records
+// that need checked rounding or exact comparison take the generic path through the row walker.
 
-// Walker state carried from one chunk to the next consecutive one (same warp): the entry of the
-// next sample, its record and the key of the last sample.
-struct WalkCtx {
-    RowWalker w;
-    SegRec R;       // record of entry w.c (warp-uniform)
-    int32_t carry;  // voxel key of the sample before the next row (if in entry w.c)
-    bool valid;
+// Start state of a warp sub-chunk: the entry containing its first sample, that entry's sample
+// range and record, and the voxel key of the sample before it (the dedup carry). Prepared by the
+// scan warp one round ahead so the walking warps start computing without a dependent load chain.
+struct SubInit {
+    long long c, so_c, so_next;
+    int32_t carry;
+    int32_t pad;
+    SegRec R;
 };
 
-template <int IPT>
-__device__ __forceinline__ void walk_init(const ListArgs& a, long long chunk, WalkCtx& wc) {
-    constexpr int CH = 32 * IPT;
-    const long long wbase = chunk * CH;
-    RowWalker& w = wc.w;
-    w.c = __ldg(a.tile_seg + chunk);  // entry containing the chunk's first sample
-    w.so_c = __ldg(a.off + w.c);
-    w.so_next = __ldg(a.off + w.c + 1);
-    wc.R = load_rec(a.rec + w.c);
-    wc.carry = 0;
-    if (wbase > w.so_c) {
+__device__ __forceinline__ void prepare_subchunk(const ListArgs& a, long long sub, int log2ch,
+                                                 SubInit& si) {
+    const long long wbase = sub << log2ch;
+    si.c = __ldg(a.tile_seg + sub);
+    si.so_c = __ldg(a.off + si.c);
+    si.so_next = __ldg(a.off + si.c + 1);
+    si.R = load_rec(a.rec + si.c);
+    si.carry = 0;
+    si.pad = 0;
+    if (wbase > si.so_c) {
         int32_t px, py, pz;
         bool b = false;
-        eval_sample(wc.R, wbase - 1 - w.so_c, w.so_next - w.so_c - 1, px, py, pz, b);
-        wc.carry = voxel_key(px, py, pz);
+        eval_sample(si.R, wbase - 1 - si.so_c, si.so_next - si.so_c - 1, px, py, pz, b);
+        si.carry = voxel_key(px, py, pz);
     }
-    wc.valid = true;
 }
 
-// Walk one chunk. EMIT: stage kept voxels at stage + 12*rank and keep per-row masks / bases
-// (lane j holds row j's) for the chain offsets. Returns the chunk's kept count (warp-uniform).
-template <int IPT, bool EMIT>
-__device__ __forceinline__ int walk_chunk(const ListArgs& a, long long chunk, WalkCtx& wc,
-                                          unsigned char* stage, unsigned& my_mask,
-                                          int& my_rowbase) {
+template <int IPT>
+__device__ __forceinline__ int walk_subchunk(const ListArgs& a, long long sub, const SubInit& si,
+                                             uint32_t* stage, long long& c_first,
+                                             long long& c_last) {
     constexpr int CH = 32 * IPT;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    const long long wbase = chunk * CH;
+    const long long wbase = sub * CH;
     const long long wend = min(wbase + (long long)CH, a.total_samples);
-    if (!wc.valid) walk_init<IPT>(a, chunk, wc);
-    RowWalker& w = wc.w;
-    SegRec& R = wc.R;
-    int32_t& carry = wc.carry;
+    RowWalker w;
+    w.c = si.c;
+    w.so_c = si.so_c;
+    w.so_next = si.so_next;
+    c_first = w.c;
+    SegRec R = si.R;
+    int32_t carry = si.carry;  // voxel key of the sample before the next row (lane 0's predecessor)
     bool bad = false;
     long long bad_seg = 0;
     const double lane_d = (double)lane;
     int running = 0;
 
-    auto commit = [&](int j, bool keep, int32_t x, int32_t y, int32_t z) {
+    auto commit = [&](bool keep, int32_t x, int32_t y, int32_t z) {
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
-        if (EMIT) {
-            if (keep) {
-                uint32_t* d = reinterpret_cast<uint32_t*>(stage + 12 * (running + __popc(mask & lt)));
-                d[0] = (uint32_t)x;
-                d[1] = (uint32_t)y;
-                d[2] = (uint32_t)z;
-            }
-            if (lane == j) {
-                my_mask = mask;
-                my_rowbase = running;
-            }
+        if (keep) {
+            uint32_t* d = stage + 3 * (running + __popc(mask & lt));
+            d[0] = (uint32_t)x;
+            d[1] = (uint32_t)y;
+            d[2] = (uint32_t)z;
         }
         running += __popc(mask);
     };
@@ -178,7 +172,12 @@ __device__ __forceinline__ int walk_chunk(const ListArgs& a, long long chunk, Wa
             nfast = (int)min((lim - row_start) >> 5, (long long)(IPT - j));
         if (nfast > 0) {
             double t = __dadd_rn(__ll2double_rn(row_start - w.so_c), lane_d);
-            const bool first0 = lane == 0 && row_start == w.so_c;  // k == 0 at lane 0, row 0
+            // k == 0 (always kept) can only sit at lane 0 of the first fast row
+            bool first = lane == 0 && row_start == w.so_c;
+            if (first) a.chain_off[w.c] = running;  // chain start: chunk-local rank
+            // lane 0's predecessor key arrives through a rotate: after row r, lane 0 holds lane
+            // 31's key of row r, which is its predecessor in row r + 1
+            int32_t prev0 = carry;
             if (R.flags & REC_POS) {
 #pragma unroll 2
                 for (int f = 0; f < nfast; ++f) {
@@ -186,10 +185,11 @@ __device__ __forceinline__ int walk_chunk(const ListArgs& a, long long chunk, Wa
                     const int32_t y = round_pos(sample_axis(R.sy, R.wy, t));
                     const int32_t z = round_pos(sample_axis(R.sz, R.wz, t));
                     const int32_t key = voxel_key(x, y, z);
-                    int32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
-                    if (lane == 0) pk = carry;
-                    carry = __shfl_sync(0xffffffffu, key, 31);
-                    commit(j + f, key != pk || (f == 0 && first0), x, y, z);
+                    const int32_t rot = __shfl_sync(0xffffffffu, key, (lane + 31) & 31);
+                    const int32_t pk = lane == 0 ? prev0 : rot;
+                    prev0 = rot;
+                    commit(key != pk || first, x, y, z);
+                    first = false;
                     t = __dadd_rn(t, 32.0);
                 }
             } else {
@@ -199,13 +199,15 @@ __device__ __forceinline__ int walk_chunk(const ListArgs& a, long long chunk, Wa
                     const int32_t y = round_fast(sample_axis(R.sy, R.wy, t));
                     const int32_t z = round_fast(sample_axis(R.sz, R.wz, t));
                     const int32_t key = voxel_key(x, y, z);
-                    int32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
-                    if (lane == 0) pk = carry;
-                    carry = __shfl_sync(0xffffffffu, key, 31);
-                    commit(j + f, key != pk || (f == 0 && first0), x, y, z);
+                    const int32_t rot = __shfl_sync(0xffffffffu, key, (lane + 31) & 31);
+                    const int32_t pk = lane == 0 ? prev0 : rot;
+                    prev0 = rot;
+                    commit(key != pk || first, x, y, z);
+                    first = false;
                     t = __dadd_rn(t, 32.0);
                 }
             }
+            carry = __shfl_sync(0xffffffffu, prev0, 0);
             j += nfast;
             continue;
         }
@@ -216,7 +218,7 @@ __device__ __forceinline__ int walk_chunk(const ListArgs& a, long long chunk, Wa
         const long long f = row_start + lane;
         const bool valid = f < wend;
         long long k = 0;
-        int32_t x = 0, y = 0, z = 0, px = 0, py = 0, pz = 0;
+        int32_t x = 0, y = 0, z = 0, px, py, pz;
         SegRec rr = R;
         if (valid) {
             if (e != c_before) rr = load_rec(a.rec + e);
@@ -246,108 +248,201 @@ __device__ __forceinline__ int walk_chunk(const ListArgs& a, long long chunk, Wa
             same = x == px && y == py && z == pz;
         }
         carry = __shfl_sync(0xffffffffu, voxel_key(x, y, z), 31);
-        commit(j, valid && (k == 0 || !same), x, y, z);
+        const bool keep = valid && (k == 0 || !same);
+        {  // chain start (k == 0): the chunk-local rank now, rebased once the prefix is known
+            const unsigned mask = __ballot_sync(0xffffffffu, keep);
+            const int rank = running + __popc(mask & lt);
+            if (keep) {
+                uint32_t* d = stage + 3 * rank;
+                d[0] = (uint32_t)x;
+                d[1] = (uint32_t)y;
+                d[2] = (uint32_t)z;
+            }
+            if (valid && k == 0) a.chain_off[e] = rank;
+            running += __popc(mask);
+        }
         // (the walker may step one past the last entry at the end of the sample space)
         if (w.c != c_before && w.c < a.nseg) R = load_rec(a.rec + w.c);
         ++j;
     }
     if (bad) record_error(a.ctl, bad_seg, 2);
-    // the walker now stands at sample wend: valid for chunk + 1 unless this was the last chunk
-    wc.valid = wend == wbase + CH && w.c < a.nseg;
+    // the walker stands at sample wend: the last entry with a sample in [wbase, wend) is w.c,
+    // or w.c - 1 if w.c starts exactly at wend (then it belongs to the next sub-chunk)
+    c_last = w.so_c >= wend ? w.c - 1 : w.c;
     return running;
 }
 
-// Pass 1: one warp per G consecutive chunks (walker carried across them).
-template <int NW, int IPT, int G>
-__global__ void __launch_bounds__(NW * 32) list_count_kernel(ListArgs a) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long first = ((long long)blockIdx.x * NW + warp) * G;
-    if (first >= a.nchunks) return;
-    WalkCtx wc;
-    wc.valid = false;
-    unsigned m;
-    int rb;
-    for (int q = 0; q < G; ++q) {
-        const long long chunk = first + q;
-        if (chunk >= a.nchunks) break;
-        const int cnt = walk_chunk<IPT, false>(a, chunk, wc, nullptr, m, rb);
-        if (lane == 0) a.counts[chunk] = cnt;
-    }
-}
-
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-
-// Pass 2: one warp per chunk; the chunk's output position is known before it starts.
-template <int NW, int IPT>
-__global__ void __launch_bounds__(NW * 32) list_emit_kernel(ListArgs a) {
-    constexpr int CH = 32 * IPT;
-    constexpr int REGION = CH * 12 + 16;
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long chunk = (long long)blockIdx.x * NW + warp;
-    if (chunk >= a.nchunks) return;
-    unsigned char* region = smem + warp * REGION;
-    const long long prefix = __ldg(a.chunk_prefix + chunk);
-    const uintptr_t g0 = reinterpret_cast<uintptr_t>(a.out) + 12ull * (unsigned long long)prefix;
-    const int head = (int)(g0 & 15u);
-    unsigned char* stage = region + head;  // stage byte b <-> global byte g0 + b, same mod 16
-    WalkCtx wc;
-    wc.valid = false;
-    unsigned my_mask = 0;
-    int my_rowbase = 0;
-    const long long wbase = chunk * CH;
-    const long long wend = min(wbase + (long long)CH, a.total_samples);
-    walk_init<IPT>(a, chunk, wc);
-    const long long c_first = wc.w.c;
-    const int count = walk_chunk<IPT, true>(a, chunk, wc, stage, my_mask, my_rowbase);
-    const long long c_last = wc.w.c;
-    const long long last = prefix + count;
-    if (last > a.out_cap) {  // caller's buffer too small: report, write nothing
-        if (lane == 0) record_error(a.ctl, c_first, 4);
-        return;
-    }
-    // chain offsets of the entries whose k = 0 sample lies in the chunk (always kept)
-    for (long long q0 = c_first; q0 <= c_last; q0 += 32) {
-        const long long q = q0 + lane;
-        const long long st = q <= c_last && q < a.nseg ? __ldg(a.off + q) : -1;
-        const bool in = st >= wbase && st < wend;
-        const int loc = in ? (int)(st - wbase) : 0;
-        const unsigned mk = __shfl_sync(0xffffffffu, my_mask, loc >> 5);
-        const int rb = __shfl_sync(0xffffffffu, my_rowbase, loc >> 5);
-        if (in) a.chain_off[q] = prefix + rb + __popc(mk & ((1u << (loc & 31)) - 1u));
-    }
-    if (wend == a.total_samples && lane == 0) {
-        a.chain_off[a.nseg] = last;
-        a.ctl->total = last;
-    }
-    // stream out: global bytes [g0, g1); the 16-B aligned middle by one bulk copy
-    const uintptr_t g1 = g0 + 12ull * (unsigned)count;
+// Copy a warp's staged records (words [0, 3*cnt) of `stage`) to global bytes [g0, g0 + 12*cnt):
+// 16-B vector stores for the aligned middle, single words for head and tail.
+__device__ __forceinline__ void store_records(const uint32_t* stage, int cnt, char* g0p) {
+    const int lane = threadIdx.x & 31;
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(g0p);
+    const uintptr_t g1 = g0 + 12ull * (unsigned)cnt;
     const uintptr_t a0 = (g0 + 15) & ~(uintptr_t)15;
     const uintptr_t a1 = g1 & ~(uintptr_t)15;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // STS -> async proxy
-    __syncwarp();
     if (a1 > a0) {
-        if (lane == 0) {
-            bulk_store(reinterpret_cast<void*>(a0), stage + (a0 - g0), (unsigned)(a1 - a0));
+        const int hw = (int)((a0 - g0) >> 2);  // head words (0..3); stage word of a0 == hw
+        const int nv = (int)((a1 - a0) >> 4);
+        uint4* dst = reinterpret_cast<uint4*>(a0);
+        for (int v = lane; v < nv; v += 32) {
+            const uint32_t* src = stage + hw + 4 * v;
+            uint4 q;
+            q.x = src[0];
+            q.y = src[1];
+            q.z = src[2];
+            q.w = src[3];
+            st_stream_v4(dst + v, q);
         }
-        // head words [g0, a0) and tail words [a1, g1)
-        const int hw = (int)((a0 - g0) >> 2), tw = (int)((g1 - a1) >> 2);
+        const int tw = (int)((g1 - a1) >> 2);
         if (lane < hw)
-            reinterpret_cast<uint32_t*>(g0)[lane] = reinterpret_cast<const uint32_t*>(stage)[lane];
+            reinterpret_cast<uint32_t*>(g0)[lane] = stage[lane];
         else if (lane >= 4 && lane - 4 < tw)
-            reinterpret_cast<uint32_t*>(a1)[lane - 4] =
-                reinterpret_cast<const uint32_t*>(stage + (a1 - g0))[lane - 4];
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            reinterpret_cast<uint32_t*>(a1)[lane - 4] = stage[hw + 4 * nv + (lane - 4)];
     } else {
         const int nw = (int)((g1 - g0) >> 2);  // fewer than 8 words
-        if (lane < nw)
-            reinterpret_cast<uint32_t*>(g0)[lane] = reinterpret_cast<const uint32_t*>(stage)[lane];
+        if (lane < nw) reinterpret_cast<uint32_t*>(g0)[lane] = stage[lane];
+    }
+}
+
+// Named barriers (ids 1..6, parity-double-buffered so a fast producer can never complete a
+// phase meant for the previous round): the scan warp arrives, the walking warps sync, or back.
+// (Immediate barrier ids keep ptxas from reserving all 16 hardware barriers.)
+template <int ID, int N>
+__device__ __forceinline__ void bar_sync_i() {
+    asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+template <int ID, int N>
+__device__ __forceinline__ void bar_arrive_i() {
+    asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+template <int ID, int N>
+__device__ __forceinline__ void bar_sync(int parity) {
+    if (parity) bar_sync_i<ID + 1, N>();
+    else bar_sync_i<ID, N>();
+}
+template <int ID, int N>
+__device__ __forceinline__ void bar_arrive(int parity) {
+    if (parity) bar_arrive_i<ID + 1, N>();
+    else bar_arrive_i<ID, N>();
+}
+constexpr int kBarTicket = 1, kBarCounts = 3, kBarPrefix = 5;  // + (round & 1)
+
+// Persistent, warp-specialised CTAs: NW walking warps + 1 scan warp, pipelined over CTA chunks
+// (look-back tiles) of NW warp sub-chunks.
+//   walking warp, round i: wait for ticket T_i; walk its sub-chunk of T_i into staging buffer
+//       i%2 and post the count (the last warp to finish publishes T_i's aggregate at once);
+//       wait for T_{i-1}'s prefix; stream T_{i-1}'s records out of buffer (i-1)%2.
+//   scan warp, round i: claim and hand out T_{i+1}; wait for T_i's counts; resolve T_i by
+//       decoupled look-back (overlapping the walk of T_{i+1}); post T_i's per-warp prefixes.
+// Tickets come from an atomic counter in claim order, and a chunk's aggregate is published as
+// soon as it is walked; the walk of T_{i+1} waits only on the resolution of T_{i-1}, so every
+// wait points at strictly smaller tickets: the look-back is deadlock-free.
+template <int NW, int IPT>
+__global__ void __launch_bounds__((NW + 1) * 32, 2) list_kernel(ListArgs a) {
+    constexpr int CH = 32 * IPT;
+    constexpr int NT = (NW + 1) * 32;
+    constexpr int kLog2CH = IPT == 8 ? 8 : (IPT == 16 ? 9 : 10);
+    static_assert(CH == (1 << kLog2CH), "sub-chunk size");
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ long long s_ticket[2];
+    __shared__ int s_cnt[2][NW];
+    __shared__ int s_done[2];
+    __shared__ long long s_pre[2][NW];
+    __shared__ SubInit s_init[2][NW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < 2) s_done[threadIdx.x] = 0;
+    __syncthreads();
+
+    if (warp == NW) {  // ------------------------------------------------ scan warp
+        unsigned long long tk = 0;
+        if (lane == 0) tk = atomicAdd(&a.ctl->tile_counter, 1ull);
+        long long T = (long long)__shfl_sync(0xffffffffu, tk, 0);
+        if (lane < NW && T < a.nchunks && T * NW + lane < a.nsub)
+            prepare_subchunk(a, T * NW + lane, kLog2CH, s_init[0][lane]);
+        if (lane == 0) s_ticket[0] = T;
+        bar_arrive<kBarTicket, NT>(0);
+        for (int i = 0; T < a.nchunks; ++i) {
+            const int cur = i & 1;
+            if (lane == 0) tk = atomicAdd(&a.ctl->tile_counter, 1ull);
+            const long long Tn = (long long)__shfl_sync(0xffffffffu, tk, 0);
+            if (lane < NW && Tn < a.nchunks && Tn * NW + lane < a.nsub)
+                prepare_subchunk(a, Tn * NW + lane, kLog2CH, s_init[cur ^ 1][lane]);
+            if (lane == 0) s_ticket[cur ^ 1] = Tn;
+            bar_arrive<kBarTicket, NT>(cur ^ 1);
+            bar_sync<kBarCounts, NT>(cur);
+            const int v = lane < NW ? s_cnt[cur][lane] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < NW; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const long long agg = __shfl_sync(0xffffffffu, incl, NW - 1);
+            const long long pre = lookback_resolve(a.status, T, agg, a.ctl);
+            if (lane < NW) s_pre[cur][lane] = pre + (incl - v);
+            if (lane == 0 && T == a.nchunks - 1) {  // the last chunk knows the total
+                a.chain_off[a.nseg] = pre + agg;
+                a.ctl->total = pre + agg;
+            }
+            bar_arrive<kBarPrefix, NT>(cur);
+            T = Tn;
+        }
+        return;
+    }
+    // --------------------------------------------------------------------- walking warps
+    uint32_t* const stage0 = smem + warp * (3 * CH);
+    uint32_t* const stage1 = smem + (NW + warp) * (3 * CH);
+    long long pc_first = 0, pc_last = -1;  // entry range of this warp's T_{i-1} sub-chunk
+    long long t_prev = -1;
+    for (int i = 0;; ++i) {
+        const int cur = i & 1, prv = cur ^ 1;
+        bar_sync<kBarTicket, NT>(cur);
+        const long long T = s_ticket[cur];
+        const bool live = T < a.nchunks;
+        long long cc_first = 0, cc_last = -1;
+        if (live) {
+            const long long sub = T * NW + warp;
+            int cnt = 0;
+            if (sub < a.nsub)
+                cnt = walk_subchunk<IPT>(a, sub, s_init[cur][warp], cur ? stage1 : stage0, cc_first,
+                                         cc_last);
+            if (lane == 0) {
+                s_cnt[cur][warp] = cnt;
+                __threadfence_block();
+                if (atomicAdd(&s_done[cur], 1) == NW - 1) {  // last walker: publish the aggregate
+                    __threadfence_block();
+                    long long agg = 0;
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) agg += *reinterpret_cast<volatile int*>(&s_cnt[cur][w]);
+                    lookback_publish(a.status, T, agg);
+                    s_done[cur] = 0;
+                }
+            }
+            bar_arrive<kBarCounts, NT>(cur);
+        }
+        if (t_prev >= 0) {
+            bar_sync<kBarPrefix, NT>(prv);
+            const long long psub = t_prev * NW + warp;
+            if (psub < a.nsub) {
+                const long long P = s_pre[prv][warp];
+                const int pcnt = s_cnt[prv][warp];
+                if (P + pcnt > a.out_cap) {  // caller's buffer too small: report, write nothing
+                    if (lane == 0) record_error(a.ctl, pc_first, 4);
+                } else {
+                    store_records(prv ? stage1 : stage0, pcnt,
+                                  reinterpret_cast<char*>(a.out) + 12ll * P);
+                    // rebase the chain offsets of entries whose k = 0 sample is in the sub-chunk
+                    const long long wbase = psub * CH;
+                    for (long long q = pc_first + lane; q <= pc_last; q += 32)
+                        if (q > pc_first || __ldg(a.off + q) == wbase) a.chain_off[q] += P;
+                }
+            }
+            __syncwarp();  // buffer (i-1)%2 is rewritten in round i+1
+        }
+        if (!live) break;
+        t_prev = T;
+        pc_first = cc_first;
+        pc_last = cc_last;
     }
 }
 
@@ -452,41 +547,28 @@ __global__ void __launch_bounds__(NW * 32) emit_bitmap_kernel(BitmapArgs a) {
 }
 
 // =============================================================================== launchers
-// list launch shape: NW warps per block, IPT rows per chunk (CH = 32*IPT samples), G chunks per
-// counting warp. variant 0 = 8 x 16 x 4 (512-sample chunks, 6 KB staging per warp),
-// 1 = 8 x 32 x 2 (1024-sample chunks, 12 KB), 2 = 8 x 8 x 8 (256, 3 KB).
-template <int NW, int IPT, int G>
-static cudaError_t launch_list_t(const ListArgs& a, int phase, cudaStream_t s) {
-    if (phase == 0) {
-        const long long warps = (a.nchunks + G - 1) / G;
-        list_count_kernel<NW, IPT, G><<<(unsigned)((warps + NW - 1) / NW), NW * 32, 0, s>>>(a);
-    } else {
-        const size_t smem = (size_t)NW * (32 * IPT * 12 + 16);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(list_emit_kernel<NW, IPT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
-        list_emit_kernel<NW, IPT><<<(unsigned)((a.nchunks + NW - 1) / NW), NW * 32, smem, s>>>(a);
+// list launch shape: NW warps per CTA, IPT rows of 32 samples per warp sub-chunk; staging is
+// 2 * NW * 32 * IPT * 12 B of shared memory per CTA (double-buffered; 8 x 16: 96 KB).
+constexpr int kListNW = 8, kListIPT = 16;
+
+int list_sub_log2() { return 9; }  // 32 * kListIPT samples per warp sub-chunk
+int list_nw() { return kListNW; }
+
+cudaError_t launch_list(const ListArgs& a, int num_sms, cudaStream_t s) {
+    const size_t smem = (size_t)2 * kListNW * 32 * kListIPT * 12;
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        cudaFuncSetAttribute(list_kernel<kListNW, kListIPT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
+                                                      list_kernel<kListNW, kListIPT>,
+                                                      (kListNW + 1) * 32, smem);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
+    long long grid = (long long)blocks_per_sm * num_sms;
+    if (grid > a.nchunks) grid = a.nchunks;
+    list_kernel<kListNW, kListIPT><<<(unsigned)grid, (kListNW + 1) * 32, smem, s>>>(a);
     return cudaGetLastError();
-}
-
-int list_chunk_log2(int variant) {
-    switch (variant) {
-        case 1: return 10;
-        case 2: return 8;
-        default: return 9;
-    }
-}
-
-cudaError_t launch_list_phase(const ListArgs& a, int variant, int phase, cudaStream_t s) {
-    switch (variant) {
-        case 1: return launch_list_t<8, 32, 2>(a, phase, s);
-        case 2: return launch_list_t<8, 8, 8>(a, phase, s);
-        default: return launch_list_t<8, 16, 4>(a, phase, s);
-    }
 }
 
 int bitmap_tile_log2() { return 12; }

@@ -28,21 +28,14 @@ struct PlanArgs {
 struct ListArgs {
     const SegRec* rec;
     const long long* off;       // nseg + 1 sample offsets
-    const long long* tile_seg;  // nchunks: entry containing each chunk's first sample
-    long long nseg, total_samples, nchunks;
+    const long long* tile_seg;  // nsub: entry containing each warp sub-chunk's first sample
+    long long nseg, total_samples;
+    long long nsub;             // warp sub-chunks of 32*IPT samples
+    long long nchunks;          // CTA chunks of NW sub-chunks (= look-back tiles)
     int32_t* out;               // 3 int32 per voxel, 4-B aligned
     long long out_cap;
     long long* chain_off;       // nseg + 1
-    int* counts;                // nchunks: kept voxels per chunk (count pass)
-    const long long* chunk_prefix;  // nchunks + 1: exclusive prefix of counts (emit pass)
-    Control* ctl;
-};
-
-struct ScanArgs {  // exclusive scan of n int counts -> n + 1 long long prefixes
-    const int* in;
-    long long n;
-    long long* out;
-    unsigned long long* status;
+    unsigned long long* status; // nchunks look-back words (zeroed)
     Control* ctl;
 };
 
@@ -81,16 +74,14 @@ struct GenArgs {
 
 int plan_tile_count(long long n);
 int clip_tile_count(long long n);
-int list_chunk_log2(int variant);  // samples per warp chunk (= per look-back status word)
+int list_sub_log2();  // samples per warp sub-chunk
+int list_nw();        // warp sub-chunks per CTA chunk (look-back tile)
 int bitmap_tile_log2();
 
 void launch_plan(const PlanArgs& a, cudaStream_t s);
 void launch_tile_index(const long long* off, long long n_entries, int ts_log2, long long* tile_seg,
                        cudaStream_t s);
-// phase 0 = count pass, 1 = emit pass
-cudaError_t launch_list_phase(const ListArgs& a, int variant, int phase, cudaStream_t s);
-int scan_tile_count(long long n);
-void launch_scan_counts(const ScanArgs& a, cudaStream_t s);
+cudaError_t launch_list(const ListArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
 void launch_clip(const ClipArgs& a, cudaStream_t s);
 void launch_round_points(const double* p, long long n, int32_t* out, Control* ctl, cudaStream_t s);

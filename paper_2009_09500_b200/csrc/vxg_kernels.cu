@@ -138,42 +138,6 @@ __global__ void __launch_bounds__(BLOCK) plan_kernel(PlanArgs a) {
     }
 }
 
-// =============================================================================== count scan
-// Exclusive prefix of the per-chunk kept-voxel counts of the list count pass: out[i] = sum of
-// in[0..i), out[n] = total. Same tile structure as the plan kernel.
-template <int BLOCK, int IPT>
-__global__ void __launch_bounds__(BLOCK) scan_counts_kernel(ScanArgs a) {
-    constexpr int TN = BLOCK * IPT;
-    __shared__ long long s_warp[BLOCK / 32 + 1];
-    __shared__ long long s_tile, s_prefix;
-    const int tid = threadIdx.x;
-    if (tid == 0) s_tile = (long long)atomicAdd(&a.ctl->tile_counter, 1ull);
-    __syncthreads();
-    const long long tile = s_tile;
-    const long long base = tile * TN + (long long)tid * IPT;  // blocked: IPT consecutive items
-    long long v[IPT];
-    long long sum = 0;
-#pragma unroll
-    for (int q = 0; q < IPT; ++q) {
-        v[q] = base + q < a.n ? (long long)__ldg(a.in + base + q) : 0;
-        sum += v[q];
-    }
-    long long agg;
-    const long long excl = block_excl_scan<BLOCK>(sum, s_warp, agg);
-    if (tid < 32) {
-        const long long pre = lookback_warp(a.status, tile, agg, a.ctl);
-        if (tid == 0) s_prefix = pre;
-    }
-    __syncthreads();
-    long long run = s_prefix + excl;
-#pragma unroll
-    for (int q = 0; q < IPT; ++q) {
-        if (base + q < a.n) a.out[base + q] = run;
-        run += v[q];
-    }
-    if (tile * TN + TN >= a.n && tid == 0) a.out[a.n] = s_prefix + agg;
-}
-
 // =============================================================================== tile index
 // tile_seg[t] = the entry containing flat sample t*TS (entries with zero samples write nothing).
 __global__ void tile_index_kernel(const long long* __restrict__ off, long long n_entries,
@@ -510,12 +474,6 @@ int clip_tile_count(long long n) { return (int)((n + kClipBlock * kClipIPT - 1) 
 
 void launch_plan(const PlanArgs& a, cudaStream_t s) {
     plan_kernel<kPlanBlock, kPlanIPT><<<plan_tile_count(a.n), kPlanBlock, 0, s>>>(a);
-}
-
-int scan_tile_count(long long n) { return (int)((n + 256 * 8 - 1) / (256 * 8)); }
-
-void launch_scan_counts(const ScanArgs& a, cudaStream_t s) {
-    scan_counts_kernel<256, 8><<<scan_tile_count(a.n), 256, 0, s>>>(a);
 }
 
 void launch_tile_index(const long long* off, long long n_entries, int ts_log2, long long* tile_seg,

@@ -44,5 +44,8 @@ def ref():
 def vx():
     """The product package on a real GPU (fails loudly if the CUDA library is missing)."""
     import paper_2009_09500_b200 as vx
-    vx.default_context()  # raises CudaError without a device: there is no fallback
+    ctx = vx.default_context()  # raises CudaError without a device: there is no fallback
+    # device buffers in the tests come from torch: run on its stream so a torch.zeros() that is
+    # still in flight cannot race the kernels
+    ctx.use_torch_stream()
     return vx
