@@ -153,7 +153,7 @@ struct vxg_batch {
     vxg_context* ctx = nullptr;
     int64_t n = 0;
     const double* d_segs = nullptr;  // owned (segs) or borrowed device pointer
-    DBuf segs, rec, steps, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl;
+    DBuf segs, rec, steps, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl, ranges;
     int64_t max_steps = 0, capacity = 0;
     float plan_ms = 0.f, emit_ms = 0.f, aux_ms = 0.f;  // plan kernel / emit kernel / tile index + clip
     vxg_timing timing{0, 0, 0};
@@ -273,35 +273,33 @@ vxg_status new_batch(vxg_context* ctx, vxg_batch** out) {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Emit the voxel list into device buffers (out: >= out_cap voxels, chain: n+1): tile index +
-// the single-pass list kernel.
+// Emit the voxel list into device buffers (out: >= out_cap voxels, chain: n+1): count pass, range
+// scan, emit pass.
 vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long long* d_chain,
                             int64_t* total) {
     vxg_context* ctx = b->ctx;
-    const int sub_log2 = vxg::list_sub_log2();
-    const int64_t nsub = ceil_div(b->capacity, 1ll << sub_log2);
-    const int64_t nchunks = ceil_div(nsub, vxg::list_nw());
-    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)nsub) ||
-        !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)std::max<int64_t>(nchunks, vxg::plan_tile_count(b->n))))
+    const int64_t blk = 1ll << vxg::list_block_log2();
+    // equal contiguous ranges, one per resident warp, in whole staging blocks
+    int64_t nranges = vxg::list_ranges(ctx->num_sms);
+    const int64_t blocks = ceil_div(b->capacity, blk);
+    int64_t range_len = ceil_div(blocks, nranges) * blk;
+    nranges = ceil_div(b->capacity, range_len);
+    if (!b->ranges.ensure(ctx, sizeof(long long) * (size_t)(2 * nranges + 1)))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
     if ((reinterpret_cast<uintptr_t>(d_out) & 3u) != 0)
         return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_voxelize: output must be 4-byte aligned");
     cudaMemsetAsync(ctl_slot(b, 1), 0, sizeof(Control), ctx->stream);
-    cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)nchunks, ctx->stream);
-    cudaEventRecord(ctx->ev[2], ctx->stream);
-    vxg::launch_tile_index(b->off.as<long long>(), b->n, sub_log2, b->tile_seg.as<long long>(),
-                           ctx->stream);
+    long long* rc = b->ranges.as<long long>();
+    vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->n, b->capacity, nranges,
+                    range_len, rc, rc + nranges, d_out, out_cap, d_chain, ctl_slot(b, 1)};
     cudaEventRecord(ctx->ev[3], ctx->stream);
-    vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->tile_seg.as<long long>(),
-                    b->n, b->capacity, nsub, nchunks, d_out, out_cap, d_chain,
-                    b->status.as<unsigned long long>(), ctl_slot(b, 1)};
-    const cudaError_t e = vxg::launch_list(a, ctx->num_sms, ctx->stream);
-    ctx->launches += 2;
+    const cudaError_t e = vxg::launch_list(a, ctx->stream);
+    ctx->launches += 3;
     cudaEventRecord(ctx->ev[4], ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "list emit");
     Control c;
     vxg_status s = read_ctl(ctx, ctl_slot(b, 1), c, "batch_voxelize");
-    cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);
+    b->aux_ms = 0.f;
     cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);
     if (s) return s;
     *total = c.total;

@@ -84,67 +84,56 @@ __device__ __forceinline__ void walker_row(RowWalker& w, const long long* __rest
 }
 
 // =============================================================================== emit: list
-// ONE pass fusing batch_voxelize's kernel and assemble phases (src/batch.cpp:107-150): every
-// sample is evaluated once, duplicates are dropped in registers, and the kept voxels are
-// compacted into the flat list with a single-pass decoupled look-back over CTA chunks.
+// batch_voxelize's kernel and assemble phases (src/batch.cpp:107-150) as two passes over the flat
+// (segment, k) sample space, which is cut into R equal contiguous ranges, one per resident warp
+// (multiples of 32*IPT samples):
+//   list_count_kernel : every warp walks its range and counts the kept (deduplicated) voxels
+//   range_scan_kernel : exclusive prefix of the R range counts (one CTA)
+//   list_emit_kernel  : every warp walks the same range again from its known output position,
+//                       staging kept voxels in shared memory (12-B records at their rank) and
+//                       streaming each block of 32*IPT samples out with 16-B vector stores; chain
+//                       offsets are written as the k = 0 samples go by
+// No inter-warp waiting anywhere (a single pass would need a look-back whose waits couple every
+// warp to its predecessors). Each warp walks one long contiguous range, so the per-block start-up
+// (entry search, record load, dedup carry) happens once per range, not once per block.
 //
-// Persistent CTAs of NW warps take chunk tickets in order (atomic counter, so every smaller
-// ticket is already owned by a running CTA: look-back forward progress). A chunk is NW warp
-// sub-chunks of CH = 32*IPT consecutive flat samples. Each warp walks its sub-chunk in rows of 32
-// samples, staging kept voxels (12-B records) in its shared-memory region at their chunk-local
-// rank. The CTA then publishes the chunk's count, resolves its global position by look-back, and
-// every warp streams its records out with 16-B vector stores (the global start of a sub-chunk has
-// any 4-B alignment, so the aligned middle is assembled from 4 LDS.32 per vector).
-//
-// Rows without an entry boundary (most rows: config-4 segments are ~1000 samples long) take the
-// fast path: one warp-uniform record, t = (row_start - so_c) + lane, S + W*t, llround, and a keep
-// flag from comparing the voxel key with the previous lane's (lane 0: the previous row's lane 31).
-// The k == N (E) sample always lies in a boundary row. Boundary rows, partial rows and records
-// that need checked rounding or exact comparison take the generic path through the row walker.
+// A warp walks rows of 32 consecutive samples (lane L holds sample row_start + L). Rows without an
+// entry boundary (most rows: config-4 segments are ~1000 samples long) take the fast path: one
+// warp-uniform record, t = (row_start - so_c) + lane, S + W*t, llround, and a keep flag from
+// comparing the voxel key with the previous lane's (lane 0: the previous row's lane 31). The
+// k == N (E) sample always lies in a boundary row. Boundary rows, partial rows and records that
+// need checked rounding or exact comparison take the generic path through the row walker.
 
-// Start state of a warp sub-chunk: the entry containing its first sample, that entry's sample
-// range and record, and the voxel key of the sample before it (the dedup carry). Prepared by the
-// scan warp one round ahead so the walking warps start computing without a dependent load chain.
-struct SubInit {
-    long long c, so_c, so_next;
-    int32_t carry;
-    int32_t pad;
-    SegRec R;
+// Walker state carried from block to block along a warp's range.
+struct Walk {
+    RowWalker w;
+    SegRec R;       // record of entry w.c (warp-uniform)
+    int32_t carry;  // voxel key of the sample before the next row (lane 0's predecessor)
 };
 
-__device__ __forceinline__ void prepare_subchunk(const ListArgs& a, long long sub, int log2ch,
-                                                 SubInit& si) {
-    const long long wbase = sub << log2ch;
-    si.c = __ldg(a.tile_seg + sub);
-    si.so_c = __ldg(a.off + si.c);
-    si.so_next = __ldg(a.off + si.c + 1);
-    si.R = load_rec(a.rec + si.c);
-    si.carry = 0;
-    si.pad = 0;
-    if (wbase > si.so_c) {
+__device__ __forceinline__ void walk_start(const ListArgs& a, long long f0, Walk& W) {
+    walker_init(W.w, a.off, 0, a.nseg - 1, f0);
+    W.R = load_rec(a.rec + W.w.c);
+    W.carry = 0;
+    if (f0 > W.w.so_c) {
         int32_t px, py, pz;
         bool b = false;
-        eval_sample(si.R, wbase - 1 - si.so_c, si.so_next - si.so_c - 1, px, py, pz, b);
-        si.carry = voxel_key(px, py, pz);
+        eval_sample(W.R, f0 - 1 - W.w.so_c, W.w.so_next - W.w.so_c - 1, px, py, pz, b);
+        W.carry = voxel_key(px, py, pz);
     }
 }
 
-template <int IPT>
-__device__ __forceinline__ int walk_subchunk(const ListArgs& a, long long sub, const SubInit& si,
-                                             uint32_t* stage, long long& c_first,
-                                             long long& c_last) {
-    constexpr int CH = 32 * IPT;
+// Walk samples [wbase, wend) (wbase a multiple of 32, wend - wbase <= 32*IPT). EMIT: stage kept
+// voxels at stage + 3*rank and write chain_off[e] = pos + rank for every k = 0 sample. Returns the
+// number of kept voxels (warp-uniform). The walker is left standing at sample wend.
+template <int IPT, bool EMIT>
+__device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long wbase,
+                                          long long wend, uint32_t* stage, long long pos) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    const long long wbase = sub * CH;
-    const long long wend = min(wbase + (long long)CH, a.total_samples);
-    RowWalker w;
-    w.c = si.c;
-    w.so_c = si.so_c;
-    w.so_next = si.so_next;
-    c_first = w.c;
-    SegRec R = si.R;
-    int32_t carry = si.carry;  // voxel key of the sample before the next row (lane 0's predecessor)
+    RowWalker& w = W.w;
+    SegRec& R = W.R;
+    int32_t& carry = W.carry;
     bool bad = false;
     long long bad_seg = 0;
     const double lane_d = (double)lane;
@@ -152,7 +141,7 @@ __device__ __forceinline__ int walk_subchunk(const ListArgs& a, long long sub, c
 
     auto commit = [&](bool keep, int32_t x, int32_t y, int32_t z) {
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
-        if (keep) {
+        if (EMIT && keep) {
             uint32_t* d = stage + 3 * (running + __popc(mask & lt));
             d[0] = (uint32_t)x;
             d[1] = (uint32_t)y;
@@ -174,12 +163,12 @@ __device__ __forceinline__ int walk_subchunk(const ListArgs& a, long long sub, c
             double t = __dadd_rn(__ll2double_rn(row_start - w.so_c), lane_d);
             // k == 0 (always kept) can only sit at lane 0 of the first fast row
             bool first = lane == 0 && row_start == w.so_c;
-            if (first) a.chain_off[w.c] = running;  // chain start: chunk-local rank
+            if (EMIT && first) a.chain_off[w.c] = pos + running;
             // lane 0's predecessor key arrives through a rotate: after row r, lane 0 holds lane
             // 31's key of row r, which is its predecessor in row r + 1
             int32_t prev0 = carry;
             if (R.flags & REC_POS) {
-#pragma unroll 2
+#pragma unroll 4
                 for (int f = 0; f < nfast; ++f) {
                     const int32_t x = round_pos(sample_axis(R.sx, R.wx, t));
                     const int32_t y = round_pos(sample_axis(R.sy, R.wy, t));
@@ -211,6 +200,75 @@ __device__ __forceinline__ int walk_subchunk(const ListArgs& a, long long sub, c
             j += nfast;
             continue;
         }
+        // ---- boundary row: the row holds entry c's last sample (E) at lane d-1 and, if d < 32,
+        // the first 32-d samples of entry c+1, which continues past the row. Same arithmetic as a
+        // fast row with a per-lane choice of record; rows with more boundaries, partial rows and
+        // records that need checked rounding or exact comparison take the generic path below.
+        if ((R.flags & (REC_CHECK | REC_WIDE | REC_POS)) == REC_POS && row_start + 32 <= wend) {
+            const int d = (int)(w.so_next - row_start);  // 1..32 (the row is not fast)
+            const long long c1 = w.c + 1;
+            bool ok = true;
+            long long so2 = 0;
+            SegRec R2 = R;
+            if (d < 32) {
+                ok = c1 < a.nseg;
+                if (ok) {
+                    so2 = __ldg(a.off + c1 + 1);
+                    ok = so2 > row_start + 32;
+                }
+                if (ok) {
+                    R2 = load_rec(a.rec + c1);
+                    ok = (R2.flags & (REC_CHECK | REC_WIDE | REC_POS)) == REC_POS;
+                }
+            }
+            if (ok) {
+                const bool in_c = lane < d;
+                const long long kk = in_c ? row_start - w.so_c + lane : (long long)(lane - d);
+                const double t = __ll2double_rn(kk);
+                const bool isE = lane == d - 1;  // k == N_c: the sample is E itself
+                const double sx = in_c ? R.sx : R2.sx, sy = in_c ? R.sy : R2.sy,
+                             sz = in_c ? R.sz : R2.sz;
+                const double wx = in_c ? R.wx : R2.wx, wy = in_c ? R.wy : R2.wy,
+                             wz = in_c ? R.wz : R2.wz;
+                int32_t x = round_pos(sample_axis(sx, wx, t));
+                int32_t y = round_pos(sample_axis(sy, wy, t));
+                int32_t z = round_pos(sample_axis(sz, wz, t));
+                if (isE) {
+                    x = R.ex;
+                    y = R.ey;
+                    z = R.ez;
+                }
+                const int32_t key = voxel_key(x, y, z);
+                const int32_t rot = __shfl_sync(0xffffffffu, key, (lane + 31) & 31);
+                const bool start = (lane == d && d < 32) || (lane == 0 && row_start == w.so_c);
+                const bool keep = start || key != (lane == 0 ? carry : rot);
+                const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                const int rank = running + __popc(mask & lt);
+                if (EMIT) {
+                    if (keep) {
+                        uint32_t* dd = stage + 3 * rank;
+                        dd[0] = (uint32_t)x;
+                        dd[1] = (uint32_t)y;
+                        dd[2] = (uint32_t)z;
+                    }
+                    if (start) a.chain_off[in_c ? w.c : c1] = pos + rank;  // chain start
+                }
+                running += __popc(mask);
+                carry = __shfl_sync(0xffffffffu, key, 31);
+                // the walker moves to entry c+1 (which holds the next row's first sample)
+                w.c = c1;
+                w.so_c = w.so_next;
+                if (d < 32) {
+                    w.so_next = so2;
+                    R = R2;
+                } else if (c1 < a.nseg) {
+                    w.so_next = __ldg(a.off + c1 + 1);
+                    R = load_rec(a.rec + c1);
+                }
+                ++j;
+                continue;
+            }
+        }
         // ---- generic row: entry boundaries, the k == N sample, partial rows, checked records
         const long long c_before = w.c;
         long long e, st, nx;
@@ -219,9 +277,10 @@ __device__ __forceinline__ int walk_subchunk(const ListArgs& a, long long sub, c
         const bool valid = f < wend;
         long long k = 0;
         int32_t x = 0, y = 0, z = 0, px, py, pz;
-        SegRec rr = R;
+        SegRec rr;
+        if (e != c_before) rr = load_rec(a.rec + min(e, a.nseg - 1));
+        else rr = R;
         if (valid) {
-            if (e != c_before) rr = load_rec(a.rec + e);
             k = f - st;
             bool b = false;
             eval_sample(rr, k, nx - st - 1, x, y, z, b);
@@ -249,16 +308,18 @@ __device__ __forceinline__ int walk_subchunk(const ListArgs& a, long long sub, c
         }
         carry = __shfl_sync(0xffffffffu, voxel_key(x, y, z), 31);
         const bool keep = valid && (k == 0 || !same);
-        {  // chain start (k == 0): the chunk-local rank now, rebased once the prefix is known
+        {
             const unsigned mask = __ballot_sync(0xffffffffu, keep);
             const int rank = running + __popc(mask & lt);
-            if (keep) {
-                uint32_t* d = stage + 3 * rank;
-                d[0] = (uint32_t)x;
-                d[1] = (uint32_t)y;
-                d[2] = (uint32_t)z;
+            if (EMIT) {
+                if (keep) {
+                    uint32_t* d = stage + 3 * rank;
+                    d[0] = (uint32_t)x;
+                    d[1] = (uint32_t)y;
+                    d[2] = (uint32_t)z;
+                }
+                if (valid && k == 0) a.chain_off[e] = pos + rank;  // chain start
             }
-            if (valid && k == 0) a.chain_off[e] = rank;
             running += __popc(mask);
         }
         // (the walker may step one past the last entry at the end of the sample space)
@@ -266,9 +327,6 @@ __device__ __forceinline__ int walk_subchunk(const ListArgs& a, long long sub, c
         ++j;
     }
     if (bad) record_error(a.ctl, bad_seg, 2);
-    // the walker stands at sample wend: the last entry with a sample in [wbase, wend) is w.c,
-    // or w.c - 1 if w.c starts exactly at wend (then it belongs to the next sub-chunk)
-    c_last = w.so_c >= wend ? w.c - 1 : w.c;
     return running;
 }
 
@@ -304,145 +362,88 @@ __device__ __forceinline__ void store_records(const uint32_t* stage, int cnt, ch
     }
 }
 
-// Named barriers (ids 1..6, parity-double-buffered so a fast producer can never complete a
-// phase meant for the previous round): the scan warp arrives, the walking warps sync, or back.
-// (Immediate barrier ids keep ptxas from reserving all 16 hardware barriers.)
-template <int ID, int N>
-__device__ __forceinline__ void bar_sync_i() {
-    asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
+// Pass 1: kept voxels of every warp range.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 3) list_count_kernel(ListArgs a) {
+    const int lane = threadIdx.x & 31;
+    const long long r = (long long)blockIdx.x * NW + (threadIdx.x >> 5);
+    if (r >= a.nranges) return;
+    const long long f0 = r * a.range_len, f1 = min(f0 + a.range_len, a.total_samples);
+    long long cnt = 0;
+    if (f0 < f1) {  // one walk over the whole range: fast runs span whole segments
+        Walk W;
+        walk_start(a, f0, W);
+        cnt = walk_block<(1 << 30), false>(a, W, f0, f1, nullptr, 0);
+    }
+    if (lane == 0) a.range_cnt[r] = cnt;
 }
-template <int ID, int N>
-__device__ __forceinline__ void bar_arrive_i() {
-    asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(N) : "memory");
-}
-template <int ID, int N>
-__device__ __forceinline__ void bar_sync(int parity) {
-    if (parity) bar_sync_i<ID + 1, N>();
-    else bar_sync_i<ID, N>();
-}
-template <int ID, int N>
-__device__ __forceinline__ void bar_arrive(int parity) {
-    if (parity) bar_arrive_i<ID + 1, N>();
-    else bar_arrive_i<ID, N>();
-}
-constexpr int kBarTicket = 1, kBarCounts = 3, kBarPrefix = 5;  // + (round & 1)
 
-// Persistent, warp-specialised CTAs: NW walking warps + 1 scan warp, pipelined over CTA chunks
-// (look-back tiles) of NW warp sub-chunks.
-//   walking warp, round i: wait for ticket T_i; walk its sub-chunk of T_i into staging buffer
-//       i%2 and post the count (the last warp to finish publishes T_i's aggregate at once);
-//       wait for T_{i-1}'s prefix; stream T_{i-1}'s records out of buffer (i-1)%2.
-//   scan warp, round i: claim and hand out T_{i+1}; wait for T_i's counts; resolve T_i by
-//       decoupled look-back (overlapping the walk of T_{i+1}); post T_i's per-warp prefixes.
-// Tickets come from an atomic counter in claim order, and a chunk's aggregate is published as
-// soon as it is walked; the walk of T_{i+1} waits only on the resolution of T_{i-1}, so every
-// wait points at strictly smaller tickets: the look-back is deadlock-free.
-template <int NW, int IPT>
-__global__ void __launch_bounds__((NW + 1) * 32, 2) list_kernel(ListArgs a) {
-    constexpr int CH = 32 * IPT;
-    constexpr int NT = (NW + 1) * 32;
-    constexpr int kLog2CH = IPT == 8 ? 8 : (IPT == 16 ? 9 : 10);
-    static_assert(CH == (1 << kLog2CH), "sub-chunk size");
-    extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ long long s_ticket[2];
-    __shared__ int s_cnt[2][NW];
-    __shared__ int s_done[2];
-    __shared__ long long s_pre[2][NW];
-    __shared__ SubInit s_init[2][NW];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x < 2) s_done[threadIdx.x] = 0;
+// Exclusive prefix of the range counts (one CTA of 1024 threads, any number of ranges).
+__global__ void __launch_bounds__(1024) range_scan_kernel(ListArgs a) {
+    __shared__ long long s_warp[33];
+    __shared__ long long s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
     __syncthreads();
-
-    if (warp == NW) {  // ------------------------------------------------ scan warp
-        unsigned long long tk = 0;
-        if (lane == 0) tk = atomicAdd(&a.ctl->tile_counter, 1ull);
-        long long T = (long long)__shfl_sync(0xffffffffu, tk, 0);
-        if (lane < NW && T < a.nchunks && T * NW + lane < a.nsub)
-            prepare_subchunk(a, T * NW + lane, kLog2CH, s_init[0][lane]);
-        if (lane == 0) s_ticket[0] = T;
-        bar_arrive<kBarTicket, NT>(0);
-        for (int i = 0; T < a.nchunks; ++i) {
-            const int cur = i & 1;
-            if (lane == 0) tk = atomicAdd(&a.ctl->tile_counter, 1ull);
-            const long long Tn = (long long)__shfl_sync(0xffffffffu, tk, 0);
-            if (lane < NW && Tn < a.nchunks && Tn * NW + lane < a.nsub)
-                prepare_subchunk(a, Tn * NW + lane, kLog2CH, s_init[cur ^ 1][lane]);
-            if (lane == 0) s_ticket[cur ^ 1] = Tn;
-            bar_arrive<kBarTicket, NT>(cur ^ 1);
-            bar_sync<kBarCounts, NT>(cur);
-            const int v = lane < NW ? s_cnt[cur][lane] : 0;
-            int incl = v;
+    for (long long base = 0; base < a.nranges; base += 1024) {
+        const long long i = base + tid;
+        const long long v = i < a.nranges ? a.range_cnt[i] : 0;
+        long long incl = v;
 #pragma unroll
-            for (int o = 1; o < NW; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            const long long agg = __shfl_sync(0xffffffffu, incl, NW - 1);
-            const long long pre = lookback_resolve(a.status, T, agg, a.ctl);
-            if (lane < NW) s_pre[cur][lane] = pre + (incl - v);
-            if (lane == 0 && T == a.nchunks - 1) {  // the last chunk knows the total
-                a.chain_off[a.nseg] = pre + agg;
-                a.ctl->total = pre + agg;
-            }
-            bar_arrive<kBarPrefix, NT>(cur);
-            T = Tn;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
         }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const long long x = s_warp[lane];
+            long long xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long t = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += t;
+            }
+            s_warp[lane] = xi - x;
+            if (lane == 31) s_warp[32] = xi;
+        }
+        __syncthreads();
+        if (i < a.nranges) a.range_pre[i] = s_carry + s_warp[warp] + incl - v;
+        __syncthreads();
+        if (tid == 0) s_carry += s_warp[32];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        a.range_pre[a.nranges] = s_carry;
+        a.chain_off[a.nseg] = s_carry;
+        a.ctl->total = s_carry;
+    }
+}
+
+// Pass 2: the same ranges again, now from their known output positions.
+template <int NW, int IPT>
+__global__ void __launch_bounds__(NW * 32, 3) list_emit_kernel(ListArgs a) {
+    constexpr int CH = 32 * IPT;
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long r = (long long)blockIdx.x * NW + warp;
+    if (r >= a.nranges) return;
+    const long long f0 = r * a.range_len, f1 = min(f0 + a.range_len, a.total_samples);
+    if (f0 >= f1) return;
+    uint32_t* stage = smem + warp * (3 * CH);
+    long long pos = __ldg(a.range_pre + r);
+    if (__ldg(a.range_pre + r + 1) > a.out_cap) {  // caller's buffer too small: write nothing
+        if (lane == 0) record_error(a.ctl, 0, 4);
         return;
     }
-    // --------------------------------------------------------------------- walking warps
-    uint32_t* const stage0 = smem + warp * (3 * CH);
-    uint32_t* const stage1 = smem + (NW + warp) * (3 * CH);
-    long long pc_first = 0, pc_last = -1;  // entry range of this warp's T_{i-1} sub-chunk
-    long long t_prev = -1;
-    for (int i = 0;; ++i) {
-        const int cur = i & 1, prv = cur ^ 1;
-        bar_sync<kBarTicket, NT>(cur);
-        const long long T = s_ticket[cur];
-        const bool live = T < a.nchunks;
-        long long cc_first = 0, cc_last = -1;
-        if (live) {
-            const long long sub = T * NW + warp;
-            int cnt = 0;
-            if (sub < a.nsub)
-                cnt = walk_subchunk<IPT>(a, sub, s_init[cur][warp], cur ? stage1 : stage0, cc_first,
-                                         cc_last);
-            if (lane == 0) {
-                s_cnt[cur][warp] = cnt;
-                __threadfence_block();
-                if (atomicAdd(&s_done[cur], 1) == NW - 1) {  // last walker: publish the aggregate
-                    __threadfence_block();
-                    long long agg = 0;
-#pragma unroll
-                    for (int w = 0; w < NW; ++w) agg += *reinterpret_cast<volatile int*>(&s_cnt[cur][w]);
-                    lookback_publish(a.status, T, agg);
-                    s_done[cur] = 0;
-                }
-            }
-            bar_arrive<kBarCounts, NT>(cur);
-        }
-        if (t_prev >= 0) {
-            bar_sync<kBarPrefix, NT>(prv);
-            const long long psub = t_prev * NW + warp;
-            if (psub < a.nsub) {
-                const long long P = s_pre[prv][warp];
-                const int pcnt = s_cnt[prv][warp];
-                if (P + pcnt > a.out_cap) {  // caller's buffer too small: report, write nothing
-                    if (lane == 0) record_error(a.ctl, pc_first, 4);
-                } else {
-                    store_records(prv ? stage1 : stage0, pcnt,
-                                  reinterpret_cast<char*>(a.out) + 12ll * P);
-                    // rebase the chain offsets of entries whose k = 0 sample is in the sub-chunk
-                    const long long wbase = psub * CH;
-                    for (long long q = pc_first + lane; q <= pc_last; q += 32)
-                        if (q > pc_first || __ldg(a.off + q) == wbase) a.chain_off[q] += P;
-                }
-            }
-            __syncwarp();  // buffer (i-1)%2 is rewritten in round i+1
-        }
-        if (!live) break;
-        t_prev = T;
-        pc_first = cc_first;
-        pc_last = cc_last;
+    Walk W;
+    walk_start(a, f0, W);
+    for (long long b = f0; b < f1; b += CH) {
+        const int cnt = walk_block<IPT, true>(a, W, b, min(b + CH, f1), stage, pos);
+        __syncwarp();
+        store_records(stage, cnt, reinterpret_cast<char*>(a.out) + 12ll * pos);
+        __syncwarp();  // the staging is rewritten by the next block
+        pos += cnt;
     }
 }
 
@@ -547,27 +548,38 @@ __global__ void __launch_bounds__(NW * 32) emit_bitmap_kernel(BitmapArgs a) {
 }
 
 // =============================================================================== launchers
-// list launch shape: NW warps per CTA, IPT rows of 32 samples per warp sub-chunk; staging is
-// 2 * NW * 32 * IPT * 12 B of shared memory per CTA (double-buffered; 8 x 16: 96 KB).
+// list launch shape: NW warps per CTA, IPT rows of 32 samples per staged block (staging
+// NW * 32 * IPT * 12 B of shared memory per emit CTA: 8 x 16 -> 48 KB).
 constexpr int kListNW = 8, kListIPT = 16;
 
-int list_sub_log2() { return 9; }  // 32 * kListIPT samples per warp sub-chunk
-int list_nw() { return kListNW; }
+template <typename K>
+static int resident_ctas(K kernel, int threads, size_t smem, int num_sms) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    return (per_sm < 1 ? 1 : per_sm) * num_sms;
+}
 
-cudaError_t launch_list(const ListArgs& a, int num_sms, cudaStream_t s) {
-    const size_t smem = (size_t)2 * kListNW * 32 * kListIPT * 12;
-    static int blocks_per_sm = 0;
-    if (!blocks_per_sm) {
-        cudaFuncSetAttribute(list_kernel<kListNW, kListIPT>,
+int list_block_log2() { return 9; }  // 32 * kListIPT
+
+// One range per resident emit warp (the count pass uses the same ranges).
+long long list_ranges(int num_sms) {
+    static long long n = 0;
+    if (!n) {
+        const size_t smem = (size_t)kListNW * 32 * kListIPT * 12;
+        cudaFuncSetAttribute(list_emit_kernel<kListNW, kListIPT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm,
-                                                      list_kernel<kListNW, kListIPT>,
-                                                      (kListNW + 1) * 32, smem);
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
+        n = (long long)resident_ctas(list_emit_kernel<kListNW, kListIPT>, kListNW * 32, smem,
+                                     num_sms) * kListNW;
     }
-    long long grid = (long long)blocks_per_sm * num_sms;
-    if (grid > a.nchunks) grid = a.nchunks;
-    list_kernel<kListNW, kListIPT><<<(unsigned)grid, (kListNW + 1) * 32, smem, s>>>(a);
+    return n;
+}
+
+cudaError_t launch_list(const ListArgs& a, cudaStream_t s) {
+    const unsigned grid = (unsigned)((a.nranges + kListNW - 1) / kListNW);
+    const size_t smem = (size_t)kListNW * 32 * kListIPT * 12;
+    list_count_kernel<kListNW><<<grid, kListNW * 32, 0, s>>>(a);
+    range_scan_kernel<<<1, 1024, 0, s>>>(a);
+    list_emit_kernel<kListNW, kListIPT><<<grid, kListNW * 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -28,14 +28,14 @@ struct PlanArgs {
 struct ListArgs {
     const SegRec* rec;
     const long long* off;       // nseg + 1 sample offsets
-    const long long* tile_seg;  // nsub: entry containing each warp sub-chunk's first sample
     long long nseg, total_samples;
-    long long nsub;             // warp sub-chunks of 32*IPT samples
-    long long nchunks;          // CTA chunks of NW sub-chunks (= look-back tiles)
+    long long nranges;          // contiguous sample ranges, one per resident emit warp
+    long long range_len;        // samples per range (a multiple of the staging block)
+    long long* range_cnt;       // nranges: kept voxels per range (count pass)
+    long long* range_pre;       // nranges + 1: exclusive prefix (range scan)
     int32_t* out;               // 3 int32 per voxel, 4-B aligned
     long long out_cap;
     long long* chain_off;       // nseg + 1
-    unsigned long long* status; // nchunks look-back words (zeroed)
     Control* ctl;
 };
 
@@ -74,14 +74,14 @@ struct GenArgs {
 
 int plan_tile_count(long long n);
 int clip_tile_count(long long n);
-int list_sub_log2();  // samples per warp sub-chunk
-int list_nw();        // warp sub-chunks per CTA chunk (look-back tile)
+int list_block_log2();                 // samples per staged block
+long long list_ranges(int num_sms);     // warp ranges of the list passes
 int bitmap_tile_log2();
 
 void launch_plan(const PlanArgs& a, cudaStream_t s);
 void launch_tile_index(const long long* off, long long n_entries, int ts_log2, long long* tile_seg,
                        cudaStream_t s);
-cudaError_t launch_list(const ListArgs& a, int num_sms, cudaStream_t s);
+cudaError_t launch_list(const ListArgs& a, cudaStream_t s);  // count, scan, emit
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
 void launch_clip(const ClipArgs& a, cudaStream_t s);
 void launch_round_points(const double* p, long long n, int32_t* out, Control* ctl, cudaStream_t s);

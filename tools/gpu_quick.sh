@@ -11,5 +11,5 @@ for w in cfg4 cfg1; do
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
   --log-file $out/launches_cfg4.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $out/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
-  -o $out/$k python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu "$@" > $out/ncu_$k.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 2 -c 2 \
+  -o $out/prof python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu "$@" > $out/ncu_$k.log 2>&1

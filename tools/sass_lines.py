@@ -15,14 +15,19 @@ ap.add_argument("rep")
 ap.add_argument("cubin")
 ap.add_argument("kernel")
 ap.add_argument("--top", type=int, default=40)
+ap.add_argument("-k", default=None, help="kernel name filter when the report holds several")
 args = ap.parse_args()
-out = subprocess.run(["ncu", "-i", args.rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", args.rep, "--page", "source", "--csv", "--print-source", "sass"]
+if args.k:
+    cmd[3:3] = ["-k", args.k]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
 ix = {h: i for i, h in enumerate(hdr)}
 prof = []
 for r in rows[2:]:
+    if r and r[0] in ("Kernel Name", "Address"):
+        break  # a second launch of the kernel: keep the first
     if len(r) < len(hdr):
         continue
     prof.append((int(r[ix["Address"]], 16), int(r[ix["Instructions Executed"]] or 0),
