@@ -336,7 +336,8 @@ vxg_status run_clip(vxg_batch* b, int64_t z_lo, int64_t z_hi, int64_t* n_entries
     return VXG_OK;
 }
 
-vxg_status emit_bitmap_device(vxg_batch* b, unsigned long long* d_words, int64_t V, int64_t z_lo,
+// Generic path (any V): every sample ORs its bit into the bitmap with a global atomic.
+vxg_status emit_bitmap_atomic(vxg_batch* b, unsigned long long* d_words, int64_t V, int64_t z_lo,
                               int64_t z_hi, int clip, int64_t* outside) {
     vxg_context* ctx = b->ctx;
     const int ts_log2 = vxg::bitmap_tile_log2();
@@ -373,6 +374,69 @@ vxg_status emit_bitmap_device(vxg_batch* b, unsigned long long* d_words, int64_t
     if (s) return s;
     if (outside) *outside = (int64_t)c.outside;
     return VXG_OK;
+}
+
+
+// Tile-binned path (vxg_bitmap.cu): V a multiple of 128, every N_i < 2^31.
+vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t V, int64_t z_lo,
+                             int64_t z_hi, int64_t* outside) {
+    vxg_context* ctx = b->ctx;
+    vxg::TileArgs g{};
+    g.rec = b->rec.as<SegRec>();
+    g.off = b->off.as<long long>();
+    g.n = b->n;
+    g.V = V;
+    g.z_lo = z_lo;
+    g.z_hi = z_hi;
+    vxg::tile_dims(V, z_hi - z_lo, g.tx, g.ty, g.tz);
+    g.ntx = ceil_div(V, g.tx);
+    g.nty = ceil_div(V, g.ty);
+    g.ntz = ceil_div(z_hi - z_lo, g.tz);
+    g.ntiles = g.ntx * g.nty * g.ntz;
+    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)(2 * g.ntiles + 1)))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
+    g.tile_cnt = b->tile_seg.as<long long>();
+    g.tile_off = g.tile_cnt + g.ntiles;
+    g.words = d_words;
+    g.ctl = ctl_slot(b, 3);
+    cudaEventRecord(ctx->ev[2], ctx->stream);
+    cudaMemsetAsync(g.ctl, 0, sizeof(Control), ctx->stream);
+    cudaMemsetAsync(g.tile_cnt, 0, sizeof(long long) * (size_t)g.ntiles, ctx->stream);
+    vxg::launch_tiles_count(g, ctx->stream);
+    vxg::launch_tiles_scan(g, ctx->stream);
+    ctx->launches += 2;
+    Control c;
+    vxg_status s = read_ctl(ctx, g.ctl, c, "bitmap");
+    if (s) return s;
+    const long long npieces = c.n_entries;
+    const long long in_box = (long long)c.outside;  // samples inside the slab box
+    if (outside) *outside = b->capacity - c.total;
+    if (npieces == 0) {
+        b->emit_ms = b->aux_ms = 0.f;
+        return VXG_OK;
+    }
+    if (!b->entries.ensure(ctx, sizeof(uint4) * (size_t)npieces))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory (%lld pieces)",
+                         npieces);
+    g.pieces = b->entries.as<uint4>();
+    vxg::launch_tiles_scatter(g, ctx->stream);
+    cudaEventRecord(ctx->ev[3], ctx->stream);
+    const cudaError_t e = vxg::launch_tiles_fill(g, ctx->num_sms, (double)in_box / (double)npieces,
+                                                ctx->stream);
+    ctx->launches += 2;
+    cudaEventRecord(ctx->ev[4], ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "tiles_fill_kernel");
+    s = read_ctl(ctx, g.ctl, c, "bitmap");
+    cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);
+    return s;
+}
+
+vxg_status emit_bitmap_device(vxg_batch* b, unsigned long long* d_words, int64_t V, int64_t z_lo,
+                              int64_t z_hi, int clip, int64_t* outside) {
+    if (V % 128 == 0 && b->max_steps < (1ll << 31) && z_hi > z_lo && !std::getenv("VXG_BITMAP_ATOMIC"))
+        return emit_bitmap_tiles(b, d_words, V, z_lo, z_hi, outside);
+    return emit_bitmap_atomic(b, d_words, V, z_lo, z_hi, clip, outside);
 }
 
 }  // namespace

@@ -1,0 +1,489 @@
+// vxg_bitmap.cu -- occupancy bitmap of a batch's samples, tile-binned through shared memory.
+//
+// The bitmap (bit b = x + V*(y + V*(z - z_lo)) of 64-bit words, include/voxgpu.h) of a 4096^3
+// volume is 8 GiB, far beyond L2, and every sector of it is hit by dozens of unrelated segments:
+// a global atomicOr per sample turns the write into random DRAM read-modify-write. Instead the
+// volume is cut into tiles of TX x TY x TZ voxels (TX = 256: a tile row is one 32-B sector) that
+// fit one CTA's shared memory, and the work is binned by tile:
+//
+//   tiles_count_kernel   walk every segment through the tiles it visits (each axis' rounded
+//                        coordinate is monotone in k, so a segment's in-tile samples are one
+//                        k-range, a "piece"), count pieces per tile and in-volume samples
+//   tiles_scan_kernel    exclusive prefix of the per-tile piece counts
+//   tiles_scatter_kernel walk again and write every piece into its tile's bin
+//   tiles_fill_kernel    persistent CTAs claim tiles: OR every piece's sample voxels into the
+//                        tile's shared-memory bits (shared atomics, no DRAM traffic), then OR the
+//                        tile into the bitmap with full-sector 16-B accesses, once per tile
+//
+// Samples are evaluated exactly as the list path does (include/voxline/parametric.hpp:41-48,
+// FMA-free, llround), so the set of bits equals the set of chain voxels of the reference.
+#include <cstdint>
+#include <cstdlib>
+
+#include "vxg_device.cuh"
+#include "vxg_internal.h"
+
+namespace vxg {
+
+// Exact rounded coordinate of sample k < N on one axis (any sign).
+__device__ __forceinline__ long long axis_round(double s, double w, long long k) {
+    return (long long)round_fast(sample_axis(s, w, __ll2double_rn(k)));
+}
+
+// First k in [lo, hi) with pred(k), hi if none; pred monotone (false...true) on [lo, hi).
+// pred(k): dir > 0 -> round(s + w*k) >= B, dir < 0 -> round(s + w*k) < B.
+// An analytic guess from the reciprocal (any error is fixed up exactly), a few exact steps, and a
+// binary-search fallback.
+__device__ __forceinline__ long long axis_cross(double s, double w, double inv_w, long long lo,
+                                                long long hi, long long B, int dir) {
+    if (lo >= hi) return hi;
+    auto pred = [&](long long k) {
+        const long long r = axis_round(s, w, k);
+        return dir > 0 ? r >= B : r < B;
+    };
+    if (w == 0.0) return pred(lo) ? lo : hi;
+    double gd = ((double)B - 0.5 - s) * inv_w;  // real k where s + w*k crosses B - 0.5
+    gd = ceil(gd);
+    gd = fmin(fmax(gd, (double)lo), (double)hi);
+    long long g = (long long)gd;
+    int steps = 0;
+    while (g > lo && pred(g - 1) && steps < 3) {
+        --g;
+        ++steps;
+    }
+    while (g < hi && !pred(g) && steps < 6) {
+        ++g;
+        ++steps;
+    }
+    if ((g == hi || pred(g)) && (g == lo || !pred(g - 1))) return g;
+    long long a = lo, b = hi;  // exact fallback
+    while (a < b) {
+        const long long m = a + ((b - a) >> 1);
+        if (pred(m)) b = m;
+        else a = m + 1;
+    }
+    return a;
+}
+
+// k-range [klo, khi) of samples k < N whose rounded coordinate on one axis lies in [lo, hi).
+__device__ __forceinline__ void axis_range(double s, double w, double inv_w, long long N,
+                                           long long lo, long long hi, long long& klo,
+                                           long long& khi) {
+    if (w >= 0.0) {
+        klo = axis_cross(s, w, inv_w, 0, N, lo, +1);
+        khi = axis_cross(s, w, inv_w, klo, N, hi, +1);
+    } else {
+        klo = axis_cross(s, w, inv_w, 0, N, hi, -1);
+        khi = axis_cross(s, w, inv_w, klo, N, lo, -1);
+    }
+}
+
+// Inside the box every coordinate is >= 0 (rounds > -0.5): the one-DADD rounding applies.
+__device__ __forceinline__ long long axis_round_pos(double s, double w, long long k) {
+    return (long long)round_pos(sample_axis(s, w, __ll2double_rn(k)));
+}
+
+// axis_cross for the tile walk: the samples of [lo, hi) are inside the box. The analytic guess is
+// verified with two exact evaluations (it is right unless (B - 0.5 - s)/w is within a few ulp of
+// an integer); anything else falls back to the exact search.
+__device__ __forceinline__ long long walk_cross(double s, double w, double inv_w, long long lo,
+                                                long long hi, long long B, int dir) {
+    double gd = ceil(((double)B - 0.5 - s) * inv_w);
+    gd = fmin(fmax(gd, (double)lo), (double)hi);
+    const long long g = (long long)gd;
+    const long long rg = g < hi ? axis_round_pos(s, w, g) : 0;
+    const long long rp = g > lo ? axis_round_pos(s, w, g - 1) : 0;
+    const bool at = g == hi || (dir > 0 ? rg >= B : rg < B);
+    const bool before = g == lo || !(dir > 0 ? rp >= B : rp < B);
+    if (at && before) return g;
+    return axis_cross(s, w, inv_w, lo, hi, B, dir);
+}
+
+// Visit the pieces of one segment inside the box [0,V)^2 x [z_lo,z_hi): sink(tile, ka, len, hasE)
+// for every maximal k-range in one tile (hasE: its last sample is k = N, i.e. E itself).
+// Also returns the number of the segment's samples inside [0, V)^3 (for the outside count).
+// Written to keep a warp's lanes (one segment each) on one instruction stream: every step
+// advances exactly one axis through one verified crossing, with the axis chosen by selects.
+template <typename Sink>
+__device__ __forceinline__ long long walk_pieces(const SegRec& r, long long N, const TileArgs& g,
+                                                 Sink&& sink) {
+    const double invx = r.wx != 0.0 ? 1.0 / r.wx : 0.0;
+    const double invy = r.wy != 0.0 ? 1.0 / r.wy : 0.0;
+    const double invz = r.wz != 0.0 ? 1.0 / r.wz : 0.0;
+    const bool e_vol = r.ex >= 0 && r.ex < g.V && r.ey >= 0 && r.ey < g.V && r.ez >= 0 &&
+                       r.ez < g.V;
+    // S itself is sample 0 (S + W*0 == S); sample N-1 (not E, which may sit a rounding away)
+    // bounds the monotone k < N samples on every axis.
+    const long long nl = N > 0 ? N - 1 : 0;
+    const long long s0x = axis_round(r.sx, r.wx, 0), s0y = axis_round(r.sy, r.wy, 0),
+                    s0z = axis_round(r.sz, r.wz, 0);
+    const long long slx = axis_round(r.sx, r.wx, nl), sly = axis_round(r.sy, r.wy, nl),
+                    slz = axis_round(r.sz, r.wz, nl);
+    const bool s_vol = s0x >= 0 && s0x < g.V && s0y >= 0 && s0y < g.V && s0z >= 0 && s0z < g.V;
+    const bool l_vol = slx >= 0 && slx < g.V && sly >= 0 && sly < g.V && slz >= 0 && slz < g.V;
+    long long klo, khi, inside;
+    long long az0 = 0, az1 = N;
+    if (s_vol && l_vol && e_vol) {  // the whole segment is inside the volume
+        inside = N + 1;
+        if (g.z_lo > 0 || g.z_hi < g.V) axis_range(r.sz, r.wz, invz, N, g.z_lo, g.z_hi, az0, az1);
+        klo = az0;
+        khi = az1;
+    } else {
+        long long ax0, ax1, ay0, ay1;
+        axis_range(r.sx, r.wx, invx, N, 0, g.V, ax0, ax1);
+        axis_range(r.sy, r.wy, invy, N, 0, g.V, ay0, ay1);
+        klo = max(ax0, ay0);
+        khi = min(ax1, ay1);
+        inside = 0;
+        if (klo < khi) {
+            long long v0, v1;
+            axis_range(r.sz, r.wz, invz, N, 0, g.V, v0, v1);
+            inside = max(0ll, min(khi, v1) - max(klo, v0));
+            if (g.z_lo == 0 && g.z_hi == g.V) {
+                az0 = v0;
+                az1 = v1;
+            } else {
+                axis_range(r.sz, r.wz, invz, N, g.z_lo, g.z_hi, az0, az1);
+            }
+            klo = max(klo, az0);
+            khi = min(khi, az1);
+        }
+        if (e_vol) ++inside;
+    }
+    const bool e_in = e_vol && r.ez >= g.z_lo && r.ez < g.z_hi;
+    long long last_tile = -1, last_ka = 0, last_end = -1;
+    if (klo < khi) {
+        // per axis: tile index q, direction, next crossing (khi: none)
+        const long long tsz[3] = {g.tx, g.ty, g.tz};
+        const long long org[3] = {0, 0, g.z_lo};
+        const double sa[3] = {r.sx, r.sy, r.sz}, wa[3] = {r.wx, r.wy, r.wz},
+                     ia[3] = {invx, invy, invz};
+        long long q[3], nx[3];
+        int dr[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            q[i] = (axis_round_pos(sa[i], wa[i], klo) - org[i]) / tsz[i];
+            const long long qe = (axis_round_pos(sa[i], wa[i], khi - 1) - org[i]) / tsz[i];
+            dr[i] = qe > q[i] ? 1 : (qe < q[i] ? -1 : 0);  // (an axis that stays never crosses)
+            nx[i] = khi;
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if (dr[i] != 0) {
+                const long long B = org[i] + (dr[i] > 0 ? q[i] + 1 : q[i]) * tsz[i];
+                nx[i] = walk_cross(sa[i], wa[i], ia[i], klo, khi, B, dr[i]);
+            }
+        }
+        long long k = klo;
+        while (true) {
+            const long long kn = min(nx[0], min(nx[1], nx[2]));
+            if (kn > k) {  // (kn == k: two axes cross at once, the piece is empty)
+                const long long tile = (q[2] * g.nty + q[1]) * g.ntx + q[0];
+                if (last_tile >= 0) sink(last_tile, last_ka, last_end - last_ka, false);
+                last_tile = tile;
+                last_ka = k;
+                last_end = kn;
+                k = kn;
+            }
+            if (k >= khi) break;
+            // advance the (first) axis crossing at k: one crossing per step, chosen by selects
+            const int i = nx[0] == k ? 0 : (nx[1] == k ? 1 : 2);
+            const double si = i == 0 ? sa[0] : (i == 1 ? sa[1] : sa[2]);
+            const double wi = i == 0 ? wa[0] : (i == 1 ? wa[1] : wa[2]);
+            const double ii = i == 0 ? ia[0] : (i == 1 ? ia[1] : ia[2]);
+            const int di = i == 0 ? dr[0] : (i == 1 ? dr[1] : dr[2]);
+            const long long qi = (i == 0 ? q[0] : (i == 1 ? q[1] : q[2])) + di;
+            const long long ti = i == 0 ? tsz[0] : (i == 1 ? tsz[1] : tsz[2]);
+            const long long oi = i == 0 ? org[0] : (i == 1 ? org[1] : org[2]);
+            const long long B = oi + (di > 0 ? qi + 1 : qi) * ti;
+            const long long nn = walk_cross(si, wi, ii, k, khi, B, di);
+            if (i == 0) { q[0] = qi; nx[0] = nn; }
+            else if (i == 1) { q[1] = qi; nx[1] = nn; }
+            else { q[2] = qi; nx[2] = nn; }
+        }
+    }
+    if (e_in) {
+        const long long tE = ((r.ez - g.z_lo) / g.tz * g.nty + r.ey / g.ty) * g.ntx + r.ex / g.tx;
+        if (last_tile == tE && last_end == N) {
+            sink(last_tile, last_ka, last_end - last_ka + 1, true);
+            last_tile = -1;
+        } else {
+            if (last_tile >= 0) sink(last_tile, last_ka, last_end - last_ka, false);
+            last_tile = -1;
+            sink(tE, N, 1, true);
+        }
+    }
+    if (last_tile >= 0) sink(last_tile, last_ka, last_end - last_ka, false);
+    return inside;
+}
+
+__device__ __forceinline__ long long seg_steps(const TileArgs& g, long long i) {
+    return __ldg(g.off + i + 1) - __ldg(g.off + i) - 1;
+}
+
+// Pass A: pieces per tile, in-volume samples.
+__global__ void __launch_bounds__(256) tiles_count_kernel(TileArgs g) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long inside = 0, inbox = 0;
+    if (i < g.n) {
+        const SegRec r = load_rec(g.rec + i);
+        inside = walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long, long long len, bool) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + t, 1ull);
+            inbox += len;
+        });
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        inside += __shfl_xor_sync(0xffffffffu, inside, o);
+        inbox += __shfl_xor_sync(0xffffffffu, inbox, o);
+    }
+    if ((threadIdx.x & 31) == 0 && inbox) atomicAdd(&g.ctl->outside, (unsigned long long)inbox);
+    if ((threadIdx.x & 31) == 0 && inside)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g.ctl->total), (unsigned long long)inside);
+}
+
+// Exclusive prefix of the tile piece counts (one CTA); tile_off[ntiles] = total pieces.
+__global__ void __launch_bounds__(1024) tiles_scan_kernel(TileArgs g) {
+    __shared__ long long s_warp[33];
+    __shared__ long long s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (long long base = 0; base < g.ntiles; base += 1024) {
+        const long long i = base + tid;
+        const long long v = i < g.ntiles ? g.tile_cnt[i] : 0;
+        long long incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const long long x = s_warp[lane];
+            long long xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long t = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += t;
+            }
+            s_warp[lane] = xi - x;
+            if (lane == 31) s_warp[32] = xi;
+        }
+        __syncthreads();
+        if (i < g.ntiles) {
+            g.tile_off[i] = s_carry + s_warp[warp] + incl - v;
+            g.tile_cnt[i] = 0;  // becomes the scatter cursor
+        }
+        __syncthreads();
+        if (tid == 0) s_carry += s_warp[32];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        g.tile_off[g.ntiles] = s_carry;
+        g.ctl->n_entries = s_carry;
+    }
+}
+
+// Pass B: write the pieces into their tiles' bins.
+__global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const SegRec r = load_rec(g.rec + i);
+    walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long ka, long long len, bool hasE) {
+        const unsigned long long slot =
+            atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + t, 1ull);
+        uint4 p;
+        p.x = (uint32_t)i;
+        p.y = (uint32_t)ka;
+        p.z = (uint32_t)len | (hasE ? 0x80000000u : 0u);
+        p.w = 0;
+        g.pieces[__ldg(g.tile_off + t) + (long long)slot] = p;
+    });
+}
+
+// Persistent CTAs: claim a tile, set its samples' bits in shared memory, OR it into the bitmap.
+//
+// Shared layout: a row of TX bits is TX/32 words; a z-slice of TY rows is padded by one word so
+// a step in z moves to the next bank (without the pad, samples of a segment running along z hit
+// the same bank with different words: up to 32-way conflicts on the shared atomics).
+// Work split: a warp takes 32/G pieces at a time, G lanes per piece (G from the mean piece
+// length: short pieces would leave most of a full warp idle).
+// Tile shape (voxels): a row of 256 is one 32-B sector of the bitmap; 80 x 80 rows fill ~200 KB.
+constexpr int kTX = 256, kTY = 80, kTZ = 80;
+constexpr int kRW = kTX / 32;          // 32-bit words per row
+constexpr int kSS = kRW * kTY + 1;     // words per z-slice (padded by one: bank skew per z step)
+constexpr int kTileWords = kSS * kTZ;
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+struct PieceRef {  // a decoded piece and its segment's record
+    SegRec r;
+    long long ka;
+    int len;    // samples S + W*k (the E sample, if any, is extra)
+    bool hasE;
+};
+
+__device__ __forceinline__ void load_piece(const TileArgs& g, long long p, long long p1,
+                                           PieceRef& q) {
+    q.len = 0;
+    q.hasE = false;
+    q.ka = 0;
+    if (p < p1) {
+        const uint4 pc = g.pieces[p];
+        q.r = load_rec(g.rec + pc.x);
+        q.ka = pc.y;
+        q.hasE = (pc.z >> 31) != 0;
+        q.len = (int)(pc.z & 0x7fffffffu) - (q.hasE ? 1 : 0);
+    }
+}
+
+// Set the bits of one piece group (G lanes per piece, 32/G pieces per warp).
+template <int G>
+__device__ __forceinline__ void fill_piece(uint32_t* bits, const PieceRef& q, int gl, int base) {
+    int mx = q.len;
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    double t = __ll2double_rn(q.ka + gl);
+    const int steps = (mx + G - 1) / G;
+    int j = gl;
+    for (int st = 0; st < steps; ++st) {
+        if (j < q.len) {
+            const int32_t x = round_pos(sample_axis(q.r.sx, q.r.wx, t));
+            const int32_t y = round_pos(sample_axis(q.r.sy, q.r.wy, t));
+            const int32_t z = round_pos(sample_axis(q.r.sz, q.r.wz, t));
+            atomicOr(bits + (z * kSS + y * kRW + (x >> 5) - base), 1u << (x & 31));
+        }
+        t = __dadd_rn(t, (double)G);
+        j += G;
+    }
+    if (q.hasE && gl == 0)
+        atomicOr(bits + (q.r.ez * kSS + q.r.ey * kRW + (q.r.ex >> 5) - base), 1u << (q.r.ex & 31));
+}
+
+// Persistent CTAs: claim a tile, set its samples' bits in shared memory, OR it into the bitmap.
+//
+// Shared layout: a row of kTX bits is kRW words; a z-slice of kTY rows is padded by one word so
+// a step in z moves to the next bank (without the pad, samples of a segment running along z hit
+// the same bank with different words: up to 32-way conflicts on the shared atomics).
+// Work split: a warp takes 32/G pieces at a time, G lanes per piece (G from the mean piece
+// length), with the next pieces and their segments' records in flight while the current ones
+// are evaluated (two register sets, no copies).
+template <int NW, int G>
+__global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
+    extern __shared__ __align__(16) uint32_t bits[];
+    __shared__ long long s_tile[2];
+    constexpr int PPW = 32 / G;      // pieces per warp step
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned long long V = (unsigned long long)g.V;
+    const int grp = lane / G, gl = lane % G;
+    for (int w = tid; w < kTileWords; w += NW * 32) bits[w] = 0u;
+    for (int it = 0;; ++it) {
+        // (parity-buffered ticket: a fast thread 0 may claim the next tile before a slow thread
+        // has read this one's)
+        if (tid == 0) s_tile[it & 1] = (long long)atomicAdd(&g.ctl->tile_counter, 1ull);
+        __syncthreads();  // (also orders the clearing of the previous tile's bits)
+        const long long tile = s_tile[it & 1];
+        if (tile >= g.ntiles) break;
+        const long long p0 = __ldg(g.tile_off + tile), p1 = __ldg(g.tile_off + tile + 1);
+        if (p0 == p1) continue;  // no samples: the bitmap keeps its words
+        const long long txi = tile % g.ntx, tyi = (tile / g.ntx) % g.nty, tzi = tile / (g.ntx * g.nty);
+        const int x0 = (int)(txi * kTX), y0 = (int)(tyi * kTY), z0 = (int)(g.z_lo + tzi * kTZ);
+        const int base = z0 * kSS + y0 * kRW + (x0 >> 5);  // (x0 is a multiple of 32)
+        // warp steps of 32/G pieces (G lanes per piece); a step's pieces load together
+        constexpr long long step = (long long)NW * PPW;
+        for (long long pb = p0 + (long long)warp * PPW; pb < p1; pb += step) {
+            PieceRef q;
+            load_piece(g, pb + grp, p1, q);
+            fill_piece<G>(bits, q, gl, base);
+        }
+        __syncthreads();
+        // OR the tile into the bitmap: a row of kTX bits is 4 words = 2 x 16 B; each thread
+        // handles rows r = tid, tid + NW*32, ... with all loads issued before the stores.
+        const int xw = (int)min((unsigned long long)kTX, V - x0) / 64;  // words inside the volume
+        constexpr int kRows = kTY * kTZ;
+        constexpr int kBatch = 4;  // rows per thread in flight
+        for (int half = 0; half < 2; ++half) {  // 16-B pairs 0 and 1 of every row
+            for (int r0 = tid; r0 < kRows; r0 += kBatch * NW * 32) {
+                ulonglong2 cur[kBatch];
+                unsigned long long wa[kBatch], wb[kBatch];
+                ulonglong2* dst[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int row = r0 + u * NW * 32;
+                    wa[u] = wb[u] = 0;
+                    dst[u] = nullptr;
+                    if (row >= kRows) continue;
+                    const int ly = row % kTY, lz = row / kTY;
+                    uint32_t* sw = bits + lz * kSS + ly * kRW + 4 * half;
+                    wa[u] = (unsigned long long)sw[0] | ((unsigned long long)sw[1] << 32);
+                    wb[u] = (unsigned long long)sw[2] | ((unsigned long long)sw[3] << 32);
+                    sw[0] = sw[1] = sw[2] = sw[3] = 0u;
+                    const long long y = y0 + ly, z = z0 + lz;
+                    if (y >= (long long)V || z >= g.z_hi || 2 * half >= xw || (wa[u] | wb[u]) == 0)
+                        continue;
+                    // (rows are 16-B aligned: V and x0 are multiples of 128)
+                    dst[u] = reinterpret_cast<ulonglong2*>(
+                        g.words + ((((unsigned long long)(z - g.z_lo) * V + y) * V + x0) >> 6) +
+                        2 * half);
+                    cur[u] = *dst[u];
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u)
+                    if (dst[u]) *dst[u] = make_ulonglong2(cur[u].x | wa[u], cur[u].y | wb[u]);
+            }
+        }
+        // (the next iteration's __syncthreads orders these clears before new atomics)
+    }
+}
+
+// =============================================================================== launchers
+int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz) {
+    tx = kTX;
+    ty = kTY;
+    tz = kTZ;
+    (void)V;
+    (void)depth;
+    return kTileWords * 4;  // shared-memory bytes (padded z-slices)
+}
+
+void launch_tiles_count(const TileArgs& g, cudaStream_t s) {
+    tiles_count_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(g);
+}
+void launch_tiles_scan(const TileArgs& g, cudaStream_t s) { tiles_scan_kernel<<<1, 1024, 0, s>>>(g); }
+void launch_tiles_scatter(const TileArgs& g, cudaStream_t s) {
+    tiles_scatter_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(g);
+}
+template <int G>
+static cudaError_t launch_fill_g(const TileArgs& g, int num_sms, cudaStream_t s) {
+    constexpr int NW = 32;
+    const size_t smem = (size_t)kTileWords * 4;
+    cudaFuncSetAttribute(tiles_fill_kernel<NW, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiles_fill_kernel<NW, G>, NW * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    long long grid = (long long)per_sm * num_sms;
+    if (grid > g.ntiles) grid = g.ntiles;
+    tiles_fill_kernel<NW, G><<<(unsigned)grid, NW * 32, smem, s>>>(g);
+    return cudaGetLastError();
+}
+
+// mean_len: mean samples per piece -> lanes per piece (VXG_FILL_G overrides: 8, 16 or 32)
+cudaError_t launch_tiles_fill(const TileArgs& g, int num_sms, double mean_len, cudaStream_t s) {
+    // (measured: G = 8 is best for the config-3 (28) and config-5 (70) means)
+    int G = mean_len < 160.0 ? 8 : (mean_len < 320.0 ? 16 : 32);
+    if (const char* e = getenv("VXG_FILL_G")) G = atoi(e);
+    if (G == 8) return launch_fill_g<8>(g, num_sms, s);
+    if (G == 16) return launch_fill_g<16>(g, num_sms, s);
+    return launch_fill_g<32>(g, num_sms, s);
+}
+
+}  // namespace vxg

@@ -50,6 +50,20 @@ struct BitmapArgs {
     Control* ctl;
 };
 
+struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
+    const SegRec* rec;
+    const long long* off;  // n + 1 sample offsets (full plan)
+    long long n;
+    long long V, z_lo, z_hi;
+    int tx, ty, tz;                   // tile size in voxels (tx = 256: one sector per row)
+    long long ntx, nty, ntz, ntiles;  // tiles per axis of the box [0,V)^2 x [z_lo,z_hi)
+    long long* tile_cnt;              // ntiles (zeroed): pieces per tile, then scatter cursor
+    long long* tile_off;              // ntiles + 1: exclusive prefix
+    uint4* pieces;                    // {segment, ka, len | hasE << 31, 0} binned by tile
+    unsigned long long* words;        // the slab's bitmap (OR-ed into)
+    Control* ctl;                     // total: in-volume samples, n_entries: pieces
+};
+
 struct ClipArgs {
     const SegRec* rec;
     const long long* off;  // n + 1 (full plan)
@@ -84,6 +98,11 @@ void launch_tile_index(const long long* off, long long n_entries, int ts_log2, l
 cudaError_t launch_list(const ListArgs& a, cudaStream_t s);  // count, scan, emit
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
 void launch_clip(const ClipArgs& a, cudaStream_t s);
+int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz);  // -> smem bytes
+void launch_tiles_count(const TileArgs& g, cudaStream_t s);
+void launch_tiles_scan(const TileArgs& g, cudaStream_t s);
+void launch_tiles_scatter(const TileArgs& g, cudaStream_t s);
+cudaError_t launch_tiles_fill(const TileArgs& g, int num_sms, double mean_len, cudaStream_t s);
 void launch_round_points(const double* p, long long n, int32_t* out, Control* ctl, cudaStream_t s);
 void launch_segment_lengths(const double* segs, long long n, double* out, cudaStream_t s);
 void launch_export_plans(const SegRec* rec, const long long* off, long long n,

@@ -13,7 +13,7 @@ ap.add_argument("rep")
 ap.add_argument("k")
 ap.add_argument("--top", type=int, default=25)
 args = ap.parse_args()
-out = subprocess.run(["ncu", "-i", args.rep, "-k", args.k, "--page", "source", "--csv",
+out = subprocess.run(["ncu", "-i", args.rep, "-k", "regex:" + args.k, "--page", "source", "--csv",
                       "--print-source", "sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
