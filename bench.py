@@ -127,21 +127,13 @@ def dist_setup(args):
 
 
 def barrier_max(torch, value: float, world: int) -> float:
-    if world == 1:
-        return value
-    import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2009_09500_b200.shard import max_over_ranks
+    return max_over_ranks(value) if world > 1 else value
 
 
 def barrier_sum(torch, value: float, world: int) -> float:
-    if world == 1:
-        return value
-    import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    from paper_2009_09500_b200.shard import sum_over_ranks
+    return sum_over_ranks(value) if world > 1 else value
 
 
 def barrier(world):
@@ -253,8 +245,9 @@ def main():
     ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, cfg["len_fixed"], cfg["len_max"],
                                        cfg["V"], seed, d_segs.data_ptr(), 1))
     V = cfg["V"]
-    if kind == "slab":
-        z_lo, z_hi = rank * V // world, (rank + 1) * V // world
+    if kind == "slab":  # the z-slab partitioner: rank r owns one slab
+        from paper_2009_09500_b200.shard import slab_bounds
+        z_lo, z_hi = slab_bounds(V, world, rank)
     else:
         z_lo, z_hi = 0, V
 

@@ -1,0 +1,112 @@
+"""Multi-GPU partitioning of the hot path: host-side logic only.
+
+One process per GPU (torch.distributed; "nccl" on the B200 box, "gloo" in the CPU tests).
+The path shards without a data-path collective:
+
+* voxel lists (configs 1, 4): chains never interact (src/batch.cpp:139-142), so each rank owns a
+  contiguous segment range; `sample_balanced_cuts` cuts the offsets scan at k * total / world so
+  ranks get equal sample counts (the work), not equal segment counts;
+* bitmaps (configs 3, 5): each rank owns the z-slab `slab_bounds(V, world, rank)`; the device
+  walk clips every segment to its slab (vxg_bitmap.cu), slabs are disjoint, no reduction.
+
+The collectives here are for verification and reporting only: `gather_bitmap` / `gather_list`
+reassemble the full result on every rank, `max_over_ranks` / `sum_over_ranks` reduce scalars
+(bench.py times each step as the max over ranks).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def slab_bounds(V: int, world: int, rank: int) -> tuple[int, int]:
+    """z-slab [z_lo, z_hi) of a V^3 volume owned by `rank` of `world` (contiguous, disjoint,
+    covering [0, V); sizes differ by at most one plane)."""
+    if not (0 <= rank < world):
+        raise ValueError(f"rank {rank} outside world {world}")
+    return rank * V // world, (rank + 1) * V // world
+
+
+def sample_balanced_cuts(offsets: np.ndarray, world: int) -> np.ndarray:
+    """Segment cut points c_0 = 0 <= c_1 <= ... <= c_world = n for a plan's sample offsets
+    (n + 1 entries, offsets[n] = capacity): rank r owns segments [c_r, c_{r+1}), whose samples
+    are within one segment of capacity / world."""
+    off = np.asarray(offsets, dtype=np.int64)
+    n = off.shape[0] - 1
+    total = int(off[-1])
+    targets = (np.arange(world + 1, dtype=np.int64) * total) // world
+    cuts = np.searchsorted(off, targets, side="left").astype(np.int64)
+    cuts[0], cuts[-1] = 0, n
+    return np.minimum(np.maximum.accumulate(cuts), n)
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+def _device(group=None):
+    import torch
+    dist = _dist()
+    return torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+
+def max_over_ranks(value: float, group=None) -> float:
+    import torch
+    dist = _dist()
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_device(group))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float, group=None) -> float:
+    import torch
+    dist = _dist()
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_device(group))
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return float(t.item())
+
+
+def _all_gather_padded(t, group=None):
+    """all_gather of 1-D tensors of different lengths -> list of the ranks' tensors."""
+    import torch
+    dist = _dist()
+    world = dist.get_world_size(group)
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    sizes = [int(s.item()) for s in sizes]
+    m = max(sizes)
+    pad = torch.zeros(m, dtype=t.dtype, device=t.device)
+    pad[: t.numel()] = t
+    parts = [torch.zeros(m, dtype=t.dtype, device=t.device) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return [p[:s] for p, s in zip(parts, sizes)]
+
+
+def gather_bitmap(words, V: int, group=None):
+    """Concatenate the ranks' z-slab bitmaps (uint64 words as an int64 tensor of V*V*depth/64
+    words, rank order == z order) into the full V^3 bitmap on every rank (verification)."""
+    import torch
+    if (V * V) % 64:
+        raise ValueError("slab gathering needs whole words per plane (V*V % 64 == 0)")
+    parts = _all_gather_padded(words.reshape(-1), group)
+    return torch.cat(parts)
+
+
+def gather_list(voxels, chain_off, group=None):
+    """Concatenate the ranks' voxel lists ((M_r, 3) int32) and chain offsets ((n_r + 1,) int64,
+    each starting at 0) in rank order; offsets are rebased onto the concatenated list."""
+    import torch
+    vparts = _all_gather_padded(voxels.reshape(-1), group)
+    oparts = _all_gather_padded(chain_off.reshape(-1), group)
+    base = 0
+    offs = []
+    for i, o in enumerate(oparts):
+        offs.append((o[:-1] if i + 1 < len(oparts) else o) + base)
+        base += int(o[-1].item())
+    return torch.cat(vparts).reshape(-1, 3), torch.cat(offs)

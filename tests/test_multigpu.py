@@ -1,0 +1,113 @@
+"""Multi-GPU host logic (paper_2009_09500_b200/shard.py) on CPU: world_size-2 gloo process groups
+stand in for the 8xB200 NVSwitch box (this run's GPU boxes have one GPU).
+
+The oracle computes each rank's shard (the kernels are covered by the -m gpu tests: the device
+slab clip is checked against the unclipped bitmap there); here the partitioning and the
+verification gathers must reassemble exactly the single-rank result.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2009_09500_b200 import shard
+
+
+def test_slab_bounds_partition():
+    for V in (64, 100, 128, 4096):
+        for world in range(1, 9):
+            b = [shard.slab_bounds(V, world, r) for r in range(world)]
+            assert b[0][0] == 0 and b[-1][1] == V
+            assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+            sizes = [hi - lo for lo, hi in b]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard.slab_bounds(64, 2, 2)
+
+
+def test_sample_balanced_cuts(oracle):
+    segs = oracle.gen_batch(5000, 0, 2048, 4096, 0x5EED0004)
+    steps, _, off, nmax, cap = _plan(oracle, segs)
+    for world in (1, 2, 3, 8):
+        c = shard.sample_balanced_cuts(off, world)
+        assert c[0] == 0 and c[-1] == len(segs) and np.all(np.diff(c) >= 0)
+        work = np.diff(off[c])
+        assert work.sum() == cap
+        assert work.max() - cap / world <= nmax + 1  # within one segment of balanced
+
+
+def _plan(oracle, segs):
+    import ctypes as C
+    n = segs.shape[0]
+    steps = np.zeros(n, np.int64)
+    w3 = np.zeros((n, 3))
+    off = np.zeros(n + 1, np.int64)
+    nmax, cap = C.c_int64(), C.c_int64()
+    p = lambda a, t: a.ctypes.data_as(C.POINTER(t))  # noqa: E731
+    assert oracle.lib.vo_batch_preprocess(p(np.ascontiguousarray(segs), C.c_double), n,
+                                          p(steps, C.c_int64), p(w3, C.c_double),
+                                          p(off, C.c_int64), C.byref(nmax), C.byref(cap)) == 0
+    off[n] = cap.value
+    return steps, w3, off, nmax.value, cap.value
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle.pyoracle import Oracle
+        o = Oracle()
+        V = 128
+        segs = o.gen_batch(3000, 0, 96, V, 77 + 0)  # identical inputs on every rank
+        # ---- bitmap: z-slab per rank, gathered == the full bitmap
+        z_lo, z_hi = shard.slab_bounds(V, world, rank)
+        words, _ = o.bitmap(segs, V, z_lo, z_hi)
+        full = shard.gather_bitmap(torch.from_numpy(words.view(np.int64)), V)
+        ref, _ = o.bitmap(segs, V)
+        ok_bitmap = np.array_equal(full.numpy().view(np.uint64), ref)
+        # ---- list: sample-balanced segment ranges, gathered == the single-rank list
+        _, _, off, _, _ = _plan(o, segs)
+        c = shard.sample_balanced_cuts(off, world)
+        mine = segs[c[rank]:c[rank + 1]]
+        vox, choff, total = o.run_batch(mine)
+        gv, go = shard.gather_list(torch.from_numpy(vox), torch.from_numpy(choff))
+        rv, ro, rt = o.run_batch(segs)
+        ok_list = np.array_equal(gv.numpy(), rv) and np.array_equal(go.numpy(), ro)
+        # ---- scalar reductions used by bench.py (max-over-ranks timing, summed work)
+        mx = shard.max_over_ranks(float(rank + 1))
+        sm = shard.sum_over_ranks(float(total))
+        ok_reduce = mx == float(world) and sm == float(rt)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, ok_bitmap, ok_list, ok_reduce, None))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, False, False, False, repr(e)))
+
+
+def test_gloo_world2_slabs_and_lists():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok_b, ok_l, ok_r, err in sorted(results):
+        assert err is None, f"rank {rank}: {err}"
+        assert ok_b, f"rank {rank}: gathered slab bitmaps differ from the full bitmap"
+        assert ok_l, f"rank {rank}: gathered list shards differ from the single-rank list"
+        assert ok_r, f"rank {rank}: max/sum over ranks wrong"

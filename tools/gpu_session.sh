@@ -1,5 +1,6 @@
 #!/bin/bash
-# One GPU-box session: tests, bench lines per workload, ncu launch list of the default bench.
+# One GPU-box session: tests, bench lines per workload (with the CPU reference baseline), the
+# reference arm, launch lists and one ncu --set full capture of each dominant kernel.
 # Usage (from the repo root, under gpurun): bash tools/gpu_session.sh [tag]
 tag=${1:-s}
 out=gpurun_out/$tag
@@ -9,7 +10,14 @@ nproc > $out/nproc.txt; lscpu > $out/lscpu.txt 2>&1
 timeout 900 python -m pytest tests -x -q -m gpu > $out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1; echo "smoke rc=$?" >> $out/smoke.log
 for w in cfg4 cfg1 cfg3 cfg5 cfg2; do
-  timeout 600 python bench.py --workload $w --steps 5 --warmup 3 > $out/bench_$w.json 2> $out/bench_$w.err
+  timeout 900 python bench.py --workload $w --steps 5 --warmup 3 > $out/bench_$w.json 2> $out/bench_$w.err
 done
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_reference_cfg4.json 2> $out/bench_reference.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
   --log-file $out/launches_cfg4.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $out/ncu_bench.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
+  --log-file $out/launches_cfg5.csv python bench.py --workload cfg5 --steps 1 --warmup 3 --no-e2e --no-cpu > $out/ncu_bench5.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"list_(count|emit)_kernel" -s 2 -c 2 \
+  -o $out/prof_cfg4 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tiles_(count|scatter|fill)" -s 3 -c 3 \
+  -o $out/prof_cfg5 python bench.py --workload cfg5 --segments 8388608 --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof5.log 2>&1
