@@ -143,13 +143,14 @@ def barrier(world):
 
 
 def load_traffic(workload: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+    """(dram bytes per launch of the dominant kernel, source) from the committed ncu capture."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(workload)
+            t = json.load(f).get(workload)
+        return (t["bytes"], t["source"]) if t else (None, None)
     except Exception:
-        return None
+        return None, None
 
 
 # ============================================================================ reference arm
@@ -269,12 +270,12 @@ def main():
         else:
             b.emit_bitmap_device(words.data_ptr(), V, z_lo, z_hi, clip=(kind == "slab"))
             units = None
-        plan_ns, emit_ns = b.gpu_timing()
+        plan_ns, emit_ns, aux_ns = b.gpu_timing()
         b.close()
-        return units, plan_ns, emit_ns
+        return units, plan_ns, emit_ns, aux_ns
 
     for _ in range(args.warmup):
-        units, _, _ = step()
+        units, _, _, _ = step()
     if kind in ("bitmap", "slab"):
         bb = vx.Batch(None, ctx=ctx, device_ptr=d_segs.data_ptr(), n=n)
         units = bb.slab_samples(z_lo, z_hi) if kind == "slab" else bb.capacity
@@ -284,15 +285,16 @@ def main():
 
     launches0 = ctx.launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    emit_ms, plan_ms = [], []
+    emit_ms, plan_ms, aux_ms = [], [], []
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         barrier(world)
         ev0.record(stream)
         for _ in range(args.steps):
-            u, p_ns, e_ns = step()
+            u, p_ns, e_ns, a_ns = step()
             plan_ms.append(p_ns / 1e6)
             emit_ms.append(e_ns / 1e6)
+            aux_ms.append(a_ns / 1e6)
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier(world)
@@ -308,14 +310,16 @@ def main():
     emit_avg = statistics.mean(emit_ms)
     if kind in ("list", "single"):
         alg_bytes = 12 * units + 8 * (n + 1) + 48 * n
-        dominant = "emit_list_kernel"
+        dominant = "list_emit_kernel"
     else:
         alg_bytes = 8 * ((V * V * (z_hi - z_lo) + 63) // 64) + 48 * n
-        dominant = "emit_bitmap_kernel"
+        dominant = "tiles_fill_kernel"
     achieved = alg_bytes / (emit_avg / 1e3) / 1e9
+    traffic, traffic_src = load_traffic(args.workload)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": load_traffic(args.workload),
+                "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": dominant, "kernel_ms": emit_avg, "plan_kernel_ms": statistics.mean(plan_ms),
+                "aux_kernels_ms": statistics.mean(aux_ms),
                 "algorithmic_bytes": alg_bytes, "peak_source": peak_src,
                 "step_share": emit_avg / ms}
 

@@ -153,8 +153,9 @@ VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t 
 /* Samples of the batch whose rounded z lies in [z_lo, z_hi) (the slab's work). */
 VXG_API vxg_status vxg_batch_slab_samples(vxg_batch* b, int64_t z_lo, int64_t z_hi,
                                           int64_t* samples);
-/* GPU time (ns, CUDA events) of the last plan kernel (preprocess_ns), emit kernel (kernel_ns) and
- * the auxiliary tile-index / slab-clip kernels (assemble_ns) on this batch. */
+/* GPU time (ns, CUDA events) on this batch of the last plan kernel + offset scan (preprocess_ns),
+ * the dominant output kernel (kernel_ns: list emit pass or bitmap tile fill) and the auxiliary
+ * passes before it (assemble_ns: list count pass + range scan, or the bitmap binning passes). */
 VXG_API vxg_status vxg_batch_timing(const vxg_batch* b, vxg_timing* t);
 
 /* run_batch (src/batch.cpp:154-162) with host buffers: upload, plan, emit, read back.

@@ -217,9 +217,12 @@ class Batch:
         return (int(out[0]), int(out[1]), int(out[2])) if live.value else None
 
     def gpu_timing(self):
+        """CUDA-event times (ns) of the last calls on this batch: (plan kernel + offset scan,
+        dominant output kernel, auxiliary passes: list count pass + range scan, or the bitmap's
+        binning passes)."""
         t = vxg_timing()
         self.ctx.check(self.ctx.lib.vxg_batch_timing(self.h, C.byref(t)))
-        return t.preprocess_ns, t.kernel_ns
+        return t.preprocess_ns, t.kernel_ns, t.assemble_ns
 
     def close(self):
         if getattr(self, "h", None):
@@ -290,7 +293,8 @@ def batch_voxelize(plan: BatchPlan, workers: int = 1, group_size: int = 64) -> d
     t0 = time.perf_counter_ns()
     vox, off, total = plan._batch.emit_list()
     t1 = time.perf_counter_ns()
-    _, kernel_ns = plan._batch.gpu_timing()
+    _, emit_ns, aux_ns = plan._batch.gpu_timing()
+    kernel_ns = emit_ns + aux_ns  # every GPU pass of the kernel phase
     timing = {"preprocess_ns": 0, "kernel_ns": int(kernel_ns),
               "assemble_ns": int(max(t1 - t0 - kernel_ns, 0))}
     return _result_dict(vox, off, total, timing)

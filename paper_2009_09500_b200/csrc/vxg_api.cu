@@ -278,7 +278,7 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long long* d_chain,
                             int64_t* total) {
     vxg_context* ctx = b->ctx;
-    const int64_t blk = 1ll << vxg::list_block_log2();
+    const int64_t blk = vxg::list_block_samples();
     // equal contiguous ranges, one per resident warp, in whole staging blocks
     int64_t nranges = vxg::list_ranges(ctx->num_sms);
     const int64_t blocks = ceil_div(b->capacity, blk);
@@ -292,15 +292,17 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
     long long* rc = b->ranges.as<long long>();
     vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->n, b->capacity, nranges,
                     range_len, rc, rc + nranges, d_out, out_cap, d_chain, ctl_slot(b, 1)};
+    cudaEventRecord(ctx->ev[2], ctx->stream);
+    cudaError_t e = vxg::launch_list_count(a, ctx->stream);
     cudaEventRecord(ctx->ev[3], ctx->stream);
-    const cudaError_t e = vxg::launch_list(a, ctx->stream);
+    if (e == cudaSuccess) e = vxg::launch_list_emit(a, ctx->stream);
     ctx->launches += 3;
     cudaEventRecord(ctx->ev[4], ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "list emit");
     Control c;
     vxg_status s = read_ctl(ctx, ctl_slot(b, 1), c, "batch_voxelize");
-    b->aux_ms = 0.f;
-    cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);
+    cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);   // count pass + range scan
+    cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);  // emit pass
     if (s) return s;
     *total = c.total;
     return VXG_OK;

@@ -420,17 +420,29 @@ __global__ void __launch_bounds__(1024) range_scan_kernel(ListArgs a) {
     }
 }
 
-// Pass 2: the same ranges again, now from their known output positions.
+// Pass 2: the same ranges again, now from their known output positions. The block's output
+// position is known before it is walked, so the records are staged at the global address's
+// offset mod 16: the 16-B-aligned middle of the block's output then leaves shared memory in ONE
+// bulk copy (cp.async.bulk, the TMA engine), only the head and tail words go through registers.
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 template <int NW, int IPT>
 __global__ void __launch_bounds__(NW * 32, 3) list_emit_kernel(ListArgs a) {
     constexpr int CH = 32 * IPT;
+    constexpr int REGION = 3 * CH + 4;  // words per warp: records + up to 3 words of skew
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long r = (long long)blockIdx.x * NW + warp;
     if (r >= a.nranges) return;
     const long long f0 = r * a.range_len, f1 = min(f0 + a.range_len, a.total_samples);
     if (f0 >= f1) return;
-    uint32_t* stage = smem + warp * (3 * CH);
+    uint32_t* region = smem + warp * REGION;
     long long pos = __ldg(a.range_pre + r);
     if (__ldg(a.range_pre + r + 1) > a.out_cap) {  // caller's buffer too small: write nothing
         if (lane == 0) record_error(a.ctl, 0, 4);
@@ -439,12 +451,32 @@ __global__ void __launch_bounds__(NW * 32, 3) list_emit_kernel(ListArgs a) {
     Walk W;
     walk_start(a, f0, W);
     for (long long b = f0; b < f1; b += CH) {
-        const int cnt = walk_block<IPT, true>(a, W, b, min(b + CH, f1), stage, pos);
+        const uintptr_t g0 = reinterpret_cast<uintptr_t>(a.out) + 12ull * (unsigned long long)pos;
+        const int skew = (int)((g0 & 15u) >> 2);  // stage word i <-> global word g0/4 + i
+        uint32_t* stage = region + skew;
+        // the previous block's bulk copy must have read the staging before it is rewritten
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-        store_records(stage, cnt, reinterpret_cast<char*>(a.out) + 12ll * pos);
-        __syncwarp();  // the staging is rewritten by the next block
+        const int cnt = walk_block<IPT, true>(a, W, b, min(b + CH, f1), stage, pos);
+        const uintptr_t g1 = g0 + 12ull * (unsigned)cnt;
+        const uintptr_t a0 = (g0 + 15) & ~(uintptr_t)15;
+        const uintptr_t a1 = g1 & ~(uintptr_t)15;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // STS -> async proxy
+        __syncwarp();
+        if (a1 > a0) {
+            const int hw = (int)((a0 - g0) >> 2), tw = (int)((g1 - a1) >> 2);
+            if (lane == 0) bulk_store(reinterpret_cast<void*>(a0), stage + hw, (unsigned)(a1 - a0));
+            if (lane < hw) reinterpret_cast<uint32_t*>(g0)[lane] = stage[lane];
+            else if (lane >= 4 && lane - 4 < tw)
+                reinterpret_cast<uint32_t*>(a1)[lane - 4] =
+                    stage[hw + (int)((a1 - a0) >> 2) + (lane - 4)];
+        } else {
+            const int nw = (int)((g1 - g0) >> 2);  // fewer than 8 words
+            if (lane < nw) reinterpret_cast<uint32_t*>(g0)[lane] = stage[lane];
+        }
         pos += cnt;
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // =============================================================================== emit: bitmap
@@ -549,8 +581,8 @@ __global__ void __launch_bounds__(NW * 32) emit_bitmap_kernel(BitmapArgs a) {
 
 // =============================================================================== launchers
 // list launch shape: NW warps per CTA, IPT rows of 32 samples per staged block (staging
-// NW * 32 * IPT * 12 B of shared memory per emit CTA: 8 x 16 -> 48 KB).
-constexpr int kListNW = 8, kListIPT = 16;
+// NW * (32 * IPT * 12 + 16) B of shared memory per emit CTA: 8 x 24 -> 74 KB, 3 CTAs per SM).
+constexpr int kListNW = 8, kListIPT = 24;
 
 template <typename K>
 static int resident_ctas(K kernel, int threads, size_t smem, int num_sms) {
@@ -559,13 +591,13 @@ static int resident_ctas(K kernel, int threads, size_t smem, int num_sms) {
     return (per_sm < 1 ? 1 : per_sm) * num_sms;
 }
 
-int list_block_log2() { return 9; }  // 32 * kListIPT
+int list_block_samples() { return 32 * kListIPT; }
 
 // One range per resident emit warp (the count pass uses the same ranges).
 long long list_ranges(int num_sms) {
     static long long n = 0;
     if (!n) {
-        const size_t smem = (size_t)kListNW * 32 * kListIPT * 12;
+        const size_t smem = (size_t)kListNW * (3 * 32 * kListIPT + 4) * 4;
         cudaFuncSetAttribute(list_emit_kernel<kListNW, kListIPT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         n = (long long)resident_ctas(list_emit_kernel<kListNW, kListIPT>, kListNW * 32, smem,
@@ -574,11 +606,16 @@ long long list_ranges(int num_sms) {
     return n;
 }
 
-cudaError_t launch_list(const ListArgs& a, cudaStream_t s) {
+cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s) {
     const unsigned grid = (unsigned)((a.nranges + kListNW - 1) / kListNW);
-    const size_t smem = (size_t)kListNW * 32 * kListIPT * 12;
     list_count_kernel<kListNW><<<grid, kListNW * 32, 0, s>>>(a);
     range_scan_kernel<<<1, 1024, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s) {
+    const unsigned grid = (unsigned)((a.nranges + kListNW - 1) / kListNW);
+    const size_t smem = (size_t)kListNW * (3 * 32 * kListIPT + 4) * 4;
     list_emit_kernel<kListNW, kListIPT><<<grid, kListNW * 32, smem, s>>>(a);
     return cudaGetLastError();
 }

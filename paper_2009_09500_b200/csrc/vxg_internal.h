@@ -88,14 +88,15 @@ struct GenArgs {
 
 int plan_tile_count(long long n);
 int clip_tile_count(long long n);
-int list_block_log2();                 // samples per staged block
+int list_block_samples();              // samples per staged block
 long long list_ranges(int num_sms);     // warp ranges of the list passes
 int bitmap_tile_log2();
 
 void launch_plan(const PlanArgs& a, cudaStream_t s);
 void launch_tile_index(const long long* off, long long n_entries, int ts_log2, long long* tile_seg,
                        cudaStream_t s);
-cudaError_t launch_list(const ListArgs& a, cudaStream_t s);  // count, scan, emit
+cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s);  // count pass + range scan
+cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s);   // emit pass
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
 void launch_clip(const ClipArgs& a, cudaStream_t s);
 int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz);  // -> smem bytes
