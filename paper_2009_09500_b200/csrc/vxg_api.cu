@@ -284,14 +284,14 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
     const int64_t blocks = ceil_div(b->capacity, blk);
     int64_t range_len = ceil_div(blocks, nranges) * blk;
     nranges = ceil_div(b->capacity, range_len);
-    if (!b->ranges.ensure(ctx, sizeof(long long) * (size_t)(2 * nranges + 1)))
+    if (!b->ranges.ensure(ctx, sizeof(long long) * (size_t)(4 * nranges + 1)))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
     if ((reinterpret_cast<uintptr_t>(d_out) & 3u) != 0)
         return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_voxelize: output must be 4-byte aligned");
     cudaMemsetAsync(ctl_slot(b, 1), 0, sizeof(Control), ctx->stream);
     long long* rc = b->ranges.as<long long>();
     vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->n, b->capacity, nranges,
-                    range_len, rc, rc + nranges, d_out, out_cap, d_chain, ctl_slot(b, 1)};
+                    range_len, rc, rc + 3 * nranges, d_out, out_cap, d_chain, ctl_slot(b, 1)};
     cudaEventRecord(ctx->ev[2], ctx->stream);
     cudaError_t e = vxg::launch_list_count(a, ctx->stream);
     cudaEventRecord(ctx->ev[3], ctx->stream);

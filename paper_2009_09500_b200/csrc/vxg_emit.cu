@@ -104,21 +104,22 @@ __device__ __forceinline__ void walker_row(RowWalker& w, const long long* __rest
 // k == N (E) sample always lies in a boundary row. Boundary rows, partial rows and records that
 // need checked rounding or exact comparison take the generic path through the row walker.
 
-// Walker state carried from block to block along a warp's range.
+// Walker state carried from block to block along a warp's range. Records are not carried:
+// each fast run / boundary row loads the record(s) it needs (a uniform 64-B load that hits L1
+// after the first row of a segment), which keeps the register count low enough for 24 warps.
 struct Walk {
     RowWalker w;
-    SegRec R;       // record of entry w.c (warp-uniform)
     int32_t carry;  // voxel key of the sample before the next row (lane 0's predecessor)
 };
 
 __device__ __forceinline__ void walk_start(const ListArgs& a, long long f0, Walk& W) {
     walker_init(W.w, a.off, 0, a.nseg - 1, f0);
-    W.R = load_rec(a.rec + W.w.c);
     W.carry = 0;
     if (f0 > W.w.so_c) {
+        const SegRec R = load_rec(a.rec + W.w.c);
         int32_t px, py, pz;
         bool b = false;
-        eval_sample(W.R, f0 - 1 - W.w.so_c, W.w.so_next - W.w.so_c - 1, px, py, pz, b);
+        eval_sample(R, f0 - 1 - W.w.so_c, W.w.so_next - W.w.so_c - 1, px, py, pz, b);
         W.carry = voxel_key(px, py, pz);
     }
 }
@@ -132,11 +133,9 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     RowWalker& w = W.w;
-    SegRec& R = W.R;
     int32_t& carry = W.carry;
     bool bad = false;
     long long bad_seg = 0;
-    const double lane_d = (double)lane;
     int running = 0;
 
     auto commit = [&](bool keep, int32_t x, int32_t y, int32_t z) {
@@ -154,20 +153,23 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
     while (j < IPT) {
         const long long row_start = wbase + (long long)j * 32;
         if (row_start >= wend) break;
+        // (the walker may stand one past the last entry only at the end of the sample space)
+        const uint32_t flags = __ldg(&a.rec[w.c].flags);
         // ---- fast rows: row r is fast iff row_start_r + 32 <= min(so_next - 1, wend)
         const long long lim = min(w.so_next - 1, wend);
         int nfast = 0;
-        if (!(R.flags & (REC_CHECK | REC_WIDE)) && lim >= row_start + 32)
+        if (!(flags & (REC_CHECK | REC_WIDE)) && lim >= row_start + 32)
             nfast = (int)min((lim - row_start) >> 5, (long long)(IPT - j));
         if (nfast > 0) {
-            double t = __dadd_rn(__ll2double_rn(row_start - w.so_c), lane_d);
+            const SegRec R = load_rec(a.rec + w.c);
+            double t = __ll2double_rn(row_start - w.so_c + lane);
             // k == 0 (always kept) can only sit at lane 0 of the first fast row
             bool first = lane == 0 && row_start == w.so_c;
             if (EMIT && first) a.chain_off[w.c] = pos + running;
             // lane 0's predecessor key arrives through a rotate: after row r, lane 0 holds lane
             // 31's key of row r, which is its predecessor in row r + 1
             int32_t prev0 = carry;
-            if (R.flags & REC_POS) {
+            if (flags & REC_POS) {
 #pragma unroll 4
                 for (int f = 0; f < nfast; ++f) {
                     const int32_t x = round_pos(sample_axis(R.sx, R.wx, t));
@@ -202,41 +204,34 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
         }
         // ---- boundary row: the row holds entry c's last sample (E) at lane d-1 and, if d < 32,
         // the first 32-d samples of entry c+1, which continues past the row. Same arithmetic as a
-        // fast row with a per-lane choice of record; rows with more boundaries, partial rows and
-        // records that need checked rounding or exact comparison take the generic path below.
-        if ((R.flags & (REC_CHECK | REC_WIDE | REC_POS)) == REC_POS && row_start + 32 <= wend) {
+        // fast row; every lane loads the record of its own entry. Rows with more boundaries,
+        // partial rows and records that need checked rounding or exact comparison take the
+        // generic path below.
+        if ((flags & (REC_CHECK | REC_WIDE | REC_POS)) == REC_POS && row_start + 32 <= wend) {
             const int d = (int)(w.so_next - row_start);  // 1..32 (the row is not fast)
             const long long c1 = w.c + 1;
             bool ok = true;
             long long so2 = 0;
-            SegRec R2 = R;
             if (d < 32) {
                 ok = c1 < a.nseg;
                 if (ok) {
                     so2 = __ldg(a.off + c1 + 1);
-                    ok = so2 > row_start + 32;
-                }
-                if (ok) {
-                    R2 = load_rec(a.rec + c1);
-                    ok = (R2.flags & (REC_CHECK | REC_WIDE | REC_POS)) == REC_POS;
+                    const uint32_t f2 = __ldg(&a.rec[c1].flags);
+                    ok = so2 > row_start + 32 && (f2 & (REC_CHECK | REC_WIDE | REC_POS)) == REC_POS;
                 }
             }
             if (ok) {
                 const bool in_c = lane < d;
+                const SegRec M = load_rec(a.rec + (in_c ? w.c : c1));
                 const long long kk = in_c ? row_start - w.so_c + lane : (long long)(lane - d);
                 const double t = __ll2double_rn(kk);
-                const bool isE = lane == d - 1;  // k == N_c: the sample is E itself
-                const double sx = in_c ? R.sx : R2.sx, sy = in_c ? R.sy : R2.sy,
-                             sz = in_c ? R.sz : R2.sz;
-                const double wx = in_c ? R.wx : R2.wx, wy = in_c ? R.wy : R2.wy,
-                             wz = in_c ? R.wz : R2.wz;
-                int32_t x = round_pos(sample_axis(sx, wx, t));
-                int32_t y = round_pos(sample_axis(sy, wy, t));
-                int32_t z = round_pos(sample_axis(sz, wz, t));
-                if (isE) {
-                    x = R.ex;
-                    y = R.ey;
-                    z = R.ez;
+                int32_t x = round_pos(sample_axis(M.sx, M.wx, t));
+                int32_t y = round_pos(sample_axis(M.sy, M.wy, t));
+                int32_t z = round_pos(sample_axis(M.sz, M.wz, t));
+                if (lane == d - 1) {  // k == N_c: the sample is E itself
+                    x = M.ex;
+                    y = M.ey;
+                    z = M.ez;
                 }
                 const int32_t key = voxel_key(x, y, z);
                 const int32_t rot = __shfl_sync(0xffffffffu, key, (lane + 31) & 31);
@@ -258,28 +253,20 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
                 // the walker moves to entry c+1 (which holds the next row's first sample)
                 w.c = c1;
                 w.so_c = w.so_next;
-                if (d < 32) {
-                    w.so_next = so2;
-                    R = R2;
-                } else if (c1 < a.nseg) {
-                    w.so_next = __ldg(a.off + c1 + 1);
-                    R = load_rec(a.rec + c1);
-                }
+                if (d < 32) w.so_next = so2;
+                else if (c1 < a.nseg) w.so_next = __ldg(a.off + c1 + 1);
                 ++j;
                 continue;
             }
         }
         // ---- generic row: entry boundaries, the k == N sample, partial rows, checked records
-        const long long c_before = w.c;
         long long e, st, nx;
         walker_row(w, a.off, a.nseg, row_start, e, st, nx);
         const long long f = row_start + lane;
         const bool valid = f < wend;
         long long k = 0;
         int32_t x = 0, y = 0, z = 0, px, py, pz;
-        SegRec rr;
-        if (e != c_before) rr = load_rec(a.rec + min(e, a.nseg - 1));
-        else rr = R;
+        const SegRec rr = load_rec(a.rec + min(e, a.nseg - 1));
         if (valid) {
             k = f - st;
             bool b = false;
@@ -322,8 +309,6 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
             }
             running += __popc(mask);
         }
-        // (the walker may step one past the last entry at the end of the sample space)
-        if (w.c != c_before && w.c < a.nseg) R = load_rec(a.rec + w.c);
         ++j;
     }
     if (bad) record_error(a.ctl, bad_seg, 2);
@@ -362,20 +347,27 @@ __device__ __forceinline__ void store_records(const uint32_t* stage, int cnt, ch
     }
 }
 
-// Pass 1: kept voxels of every warp range.
+// Pass 1: kept voxels of every warp range, counted by kCountSplit warps per range (the count
+// pass needs no shared memory, so it can run more warps than the emit pass has ranges).
+constexpr int kCountSplit = 2;
+
 template <int NW>
-__global__ void __launch_bounds__(NW * 32, 3) list_count_kernel(ListArgs a) {
+__global__ void __launch_bounds__(NW * 32, 4) list_count_kernel(ListArgs a) {
     const int lane = threadIdx.x & 31;
-    const long long r = (long long)blockIdx.x * NW + (threadIdx.x >> 5);
+    const long long q = (long long)blockIdx.x * NW + (threadIdx.x >> 5);
+    const long long r = q / kCountSplit;
     if (r >= a.nranges) return;
-    const long long f0 = r * a.range_len, f1 = min(f0 + a.range_len, a.total_samples);
+    const long long r0 = r * a.range_len, r1 = min(r0 + a.range_len, a.total_samples);
+    const long long part = ((a.range_len / kCountSplit) + 31) & ~31ll;  // whole rows
+    const long long f0 = min(r0 + (q % kCountSplit) * part, r1);
+    const long long f1 = (q % kCountSplit) == kCountSplit - 1 ? r1 : min(f0 + part, r1);
     long long cnt = 0;
-    if (f0 < f1) {  // one walk over the whole range: fast runs span whole segments
+    if (f0 < f1) {  // one walk over the whole part: fast runs span whole segments
         Walk W;
         walk_start(a, f0, W);
         cnt = walk_block<(1 << 30), false>(a, W, f0, f1, nullptr, 0);
     }
-    if (lane == 0) a.range_cnt[r] = cnt;
+    if (lane == 0) a.range_cnt[q] = cnt;
 }
 
 // Exclusive prefix of the range counts (one CTA of 1024 threads, any number of ranges).
@@ -387,7 +379,9 @@ __global__ void __launch_bounds__(1024) range_scan_kernel(ListArgs a) {
     __syncthreads();
     for (long long base = 0; base < a.nranges; base += 1024) {
         const long long i = base + tid;
-        const long long v = i < a.nranges ? a.range_cnt[i] : 0;
+        long long v = 0;
+        if (i < a.nranges)
+            for (int h = 0; h < kCountSplit; ++h) v += a.range_cnt[kCountSplit * i + h];
         long long incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -607,7 +601,7 @@ long long list_ranges(int num_sms) {
 }
 
 cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s) {
-    const unsigned grid = (unsigned)((a.nranges + kListNW - 1) / kListNW);
+    const unsigned grid = (unsigned)((a.nranges * kCountSplit + kListNW - 1) / kListNW);
     list_count_kernel<kListNW><<<grid, kListNW * 32, 0, s>>>(a);
     range_scan_kernel<<<1, 1024, 0, s>>>(a);
     return cudaGetLastError();

@@ -31,7 +31,7 @@ struct ListArgs {
     long long nseg, total_samples;
     long long nranges;          // contiguous sample ranges, one per resident emit warp
     long long range_len;        // samples per range (a multiple of the staging block)
-    long long* range_cnt;       // nranges: kept voxels per range (count pass)
+    long long* range_cnt;       // kCountSplit * nranges: kept voxels per range part (count pass)
     long long* range_pre;       // nranges + 1: exclusive prefix (range scan)
     int32_t* out;               // 3 int32 per voxel, 4-B aligned
     long long out_cap;
