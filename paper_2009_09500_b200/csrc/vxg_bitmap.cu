@@ -86,6 +86,20 @@ __device__ __forceinline__ long long axis_round_pos(double s, double w, long lon
 // axis_cross for the tile walk: the samples of [lo, hi) are inside the box. The analytic guess is
 // verified with two exact evaluations (it is right unless (B - 0.5 - s)/w is within a few ulp of
 // an integer); anything else falls back to the exact search.
+// 32-bit form of walk_cross for the tile walk (every N < 2^31 on the tile path).
+__device__ __forceinline__ int walk_cross32(double s, double w, double inv_w, int lo, int hi, int B,
+                                            int dir) {
+    double gd = ceil(((double)B - 0.5 - s) * inv_w);
+    gd = fmin(fmax(gd, (double)lo), (double)hi);
+    const int g = (int)gd;
+    const int rg = g < hi ? round_pos(sample_axis(s, w, __int2double_rn(g))) : 0;
+    const int rp = g > lo ? round_pos(sample_axis(s, w, __int2double_rn(g - 1))) : 0;
+    const bool at = g == hi || (dir > 0 ? rg >= B : rg < B);
+    const bool before = g == lo || !(dir > 0 ? rp >= B : rp < B);
+    if (at && before) return g;
+    return (int)axis_cross(s, w, inv_w, lo, hi, B, dir);
+}
+
 __device__ __forceinline__ long long walk_cross(double s, double w, double inv_w, long long lo,
                                                 long long hi, long long B, int dir) {
     double gd = ceil(((double)B - 0.5 - s) * inv_w);
@@ -153,53 +167,50 @@ __device__ __forceinline__ long long walk_pieces(const SegRec& r, long long N, c
     const bool e_in = e_vol && r.ez >= g.z_lo && r.ez < g.z_hi;
     long long last_tile = -1, last_ka = 0, last_end = -1;
     if (klo < khi) {
-        // per axis: tile index q, direction, next crossing (khi: none)
-        const long long tsz[3] = {g.tx, g.ty, g.tz};
-        const long long org[3] = {0, 0, g.z_lo};
+        // 32-bit walk (the tile path requires every N < 2^31): per axis the direction, the next
+        // tile boundary B and the first k past it (khi: none); the tile id moves by strides.
+        const int k0 = (int)klo, k1 = (int)khi;
+        const int tsz[3] = {g.tx, g.ty, g.tz};
+        const int org[3] = {0, 0, (int)g.z_lo};
+        const int stride[3] = {1, (int)g.ntx, (int)(g.ntx * g.nty)};
         const double sa[3] = {r.sx, r.sy, r.sz}, wa[3] = {r.wx, r.wy, r.wz},
                      ia[3] = {invx, invy, invz};
-        long long q[3], nx[3];
-        int dr[3];
+        int nx[3], dr[3], Bn[3];
+        int tile = 0;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            q[i] = (axis_round_pos(sa[i], wa[i], klo) - org[i]) / tsz[i];
-            const long long qe = (axis_round_pos(sa[i], wa[i], khi - 1) - org[i]) / tsz[i];
-            dr[i] = qe > q[i] ? 1 : (qe < q[i] ? -1 : 0);  // (an axis that stays never crosses)
-            nx[i] = khi;
+            const int q = (int)(axis_round_pos(sa[i], wa[i], k0) - org[i]) / tsz[i];
+            const int qe = (int)(axis_round_pos(sa[i], wa[i], k1 - 1) - org[i]) / tsz[i];
+            dr[i] = qe > q ? 1 : (qe < q ? -1 : 0);  // (an axis that stays never crosses)
+            tile += q * stride[i];
+            Bn[i] = org[i] + (dr[i] > 0 ? q + 1 : q) * tsz[i];
+            nx[i] = dr[i] != 0 ? walk_cross32(sa[i], wa[i], ia[i], k0, k1, Bn[i], dr[i]) : k1;
         }
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            if (dr[i] != 0) {
-                const long long B = org[i] + (dr[i] > 0 ? q[i] + 1 : q[i]) * tsz[i];
-                nx[i] = walk_cross(sa[i], wa[i], ia[i], klo, khi, B, dr[i]);
-            }
-        }
-        long long k = klo;
+        int k = k0;
         while (true) {
-            const long long kn = min(nx[0], min(nx[1], nx[2]));
+            const int kn = min(nx[0], min(nx[1], nx[2]));
             if (kn > k) {  // (kn == k: two axes cross at once, the piece is empty)
-                const long long tile = (q[2] * g.nty + q[1]) * g.ntx + q[0];
                 if (last_tile >= 0) sink(last_tile, last_ka, last_end - last_ka, false);
                 last_tile = tile;
                 last_ka = k;
                 last_end = kn;
                 k = kn;
             }
-            if (k >= khi) break;
+            if (k >= k1) break;
             // advance the (first) axis crossing at k: one crossing per step, chosen by selects
             const int i = nx[0] == k ? 0 : (nx[1] == k ? 1 : 2);
             const double si = i == 0 ? sa[0] : (i == 1 ? sa[1] : sa[2]);
             const double wi = i == 0 ? wa[0] : (i == 1 ? wa[1] : wa[2]);
             const double ii = i == 0 ? ia[0] : (i == 1 ? ia[1] : ia[2]);
             const int di = i == 0 ? dr[0] : (i == 1 ? dr[1] : dr[2]);
-            const long long qi = (i == 0 ? q[0] : (i == 1 ? q[1] : q[2])) + di;
-            const long long ti = i == 0 ? tsz[0] : (i == 1 ? tsz[1] : tsz[2]);
-            const long long oi = i == 0 ? org[0] : (i == 1 ? org[1] : org[2]);
-            const long long B = oi + (di > 0 ? qi + 1 : qi) * ti;
-            const long long nn = walk_cross(si, wi, ii, k, khi, B, di);
-            if (i == 0) { q[0] = qi; nx[0] = nn; }
-            else if (i == 1) { q[1] = qi; nx[1] = nn; }
-            else { q[2] = qi; nx[2] = nn; }
+            const int ti = i == 0 ? tsz[0] : (i == 1 ? tsz[1] : tsz[2]);
+            const int st = i == 0 ? stride[0] : (i == 1 ? stride[1] : stride[2]);
+            const int B = (i == 0 ? Bn[0] : (i == 1 ? Bn[1] : Bn[2])) + di * ti;
+            const int nn = walk_cross32(si, wi, ii, k, k1, B, di);
+            tile += di * st;
+            if (i == 0) { Bn[0] = B; nx[0] = nn; }
+            else if (i == 1) { Bn[1] = B; nx[1] = nn; }
+            else { Bn[2] = B; nx[2] = nn; }
         }
     }
     if (e_in) {
