@@ -50,7 +50,8 @@ typedef enum vxg_status {
     VXG_OUT_OF_RANGE = 3,     /* std::out_of_range (kernel_work_item indices) */
     VXG_LOGIC_ERROR = 4,      /* std::logic_error (malformed plan, capacity mismatch) */
     VXG_CUDA_ERROR = 5,       /* CUDA runtime failure */
-    VXG_OUT_OF_MEMORY = 6     /* device or pinned allocation failed */
+    VXG_OUT_OF_MEMORY = 6,    /* device or pinned allocation failed */
+    VXG_IO_ERROR = 7          /* file cannot be opened / read / written (the CLI's IoError) */
 } vxg_status;
 
 typedef enum vxg_mem { VXG_MEM_HOST = 0, VXG_MEM_DEVICE = 1 } vxg_mem;
@@ -177,6 +178,20 @@ VXG_API vxg_status vxg_gen_segments(vxg_context* ctx, int64_t n, const int64_t* 
 /* gen_arbitrary_batch (src/bench.cpp:85-136): host length planning, GPU segment generation. */
 VXG_API vxg_status vxg_gen_arbitrary_batch(vxg_context* ctx, int64_t total, int64_t count,
                                            uint64_t seed, vxg_segment* out);
+
+/* ---------------------------------------------------------------- formats (host, native) */
+/* read_segments_csv (src/formats.cpp:92-132) of a file: six finite decimal fields per line
+ * (sx,sy,sz,ex,ey,ez), '#' and blank lines skipped. On success *out holds *n segments (malloc'd:
+ * release with vxg_free). A malformed line -> VXG_INVALID_ARGUMENT with its 1-based number in
+ * *bad_line (the first one, as the reference's serial parser reports); no file -> VXG_IO_ERROR. */
+VXG_API vxg_status vxg_read_segments_csv(const char* path, vxg_segment** out, int64_t* n,
+                                         int64_t* bad_line);
+VXG_API void vxg_free(void* p);
+/* write_vox3_multi (format 0, VOX3 version 2) / write_xyz_multi (format 1)
+ * (src/formats.cpp:140-185) of n chains given as a flat list + chain offsets (n + 1 entries), as
+ * vxg_batch_emit_list returns them. Byte-identical to the reference's writers. */
+VXG_API vxg_status vxg_write_chains(const char* path, int format, const vxg_voxel* voxels,
+                                    const int64_t* chain_off, int64_t n);
 
 #ifdef __cplusplus
 }

@@ -240,6 +240,9 @@ class RefOracle:
         L.ref_splitmix_next.argtypes = [_u64p]
         L.ref_compute_mvps.restype = C.c_double
         L.ref_compute_mvps.argtypes = [C.c_int64, C.c_double, C.POINTER(C.c_int)]
+        L.ref_read_segments_csv.argtypes = [C.c_char_p, _f64p, C.c_int64, _i64p, C.c_char_p,
+                                            C.c_int64]
+        L.ref_batch_write.argtypes = [_f64p, C.c_int64, C.c_char_p, C.c_int]
 
     def splitmix(self, seed: int, count: int) -> list[int]:
         st = C.c_uint64(seed)
@@ -338,3 +341,22 @@ class RefOracle:
         v = self.lib.ref_compute_mvps(total, ms, C.byref(err))
         _check(err.value, "compute_mvps")
         return v
+
+    # --- formats (src/formats.cpp) ------------------------------------------------
+    def read_segments_csv(self, path: str):
+        """-> (float64 (n, 6), None) or (None, the reference's invalid_argument message)."""
+        n = C.c_int64()
+        msg = C.create_string_buffer(512)
+        rc = self.lib.ref_read_segments_csv(str(path).encode(), None, 0, C.byref(n), msg, 512)
+        if rc:
+            return None, msg.value.decode()
+        out = np.zeros((max(n.value, 1), 6))
+        rc = self.lib.ref_read_segments_csv(str(path).encode(), _p(out, _f64p), n.value,
+                                            C.byref(n), msg, 512)
+        return out[: n.value], None
+
+    def batch_write(self, segs, path: str, fmt: str = "vox3"):
+        """The reference CLI's batch output: run_batch + write_vox3_multi / write_xyz_multi."""
+        s = as_segments(segs)
+        _check(self.lib.ref_batch_write(_p(s, _f64p), s.shape[0], str(path).encode(),
+                                        {"vox3": 0, "xyz": 1}[fmt]), "batch_write")

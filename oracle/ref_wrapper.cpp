@@ -1,7 +1,7 @@
 // ref_wrapper.cpp -- flat extern "C" view of the UNMODIFIED reference implementation.
 //
 // TEST INFRASTRUCTURE. oracle/Makefile compiles this file together with the reference's own
-// sources (/root/reference/proj/src/{geometry,parametric,batch,bench}.cpp, read in place, never
+// sources (/root/reference/proj/src/{geometry,parametric,batch,bench,formats}.cpp, read in place, never
 // copied) into oracle/_ref/libref_voxline.so. It is used to (1) pin the C restatement in
 // oracle/voxline_oracle.c, (2) generate tests/golden fixtures, and (3) serve as the CPU
 // baseline ("kind": "reference") in bench.py. Exceptions are mapped to the codes in
@@ -11,8 +11,12 @@
 #include <stdexcept>
 #include <vector>
 
+#include <fstream>
+#include <sstream>
+
 #include "voxline/batch.hpp"
 #include "voxline/bench.hpp"
+#include "voxline/formats.hpp"
 #include "voxline/geometry.hpp"
 #include "voxline/parametric.hpp"
 
@@ -186,6 +190,46 @@ double ref_compute_mvps(int64_t total, double ms, int* err) {
     double v = 0.0;
     *err = guarded([&] { v = voxline::compute_mvps(total, ms); });
     return v;
+}
+
+// read_segments_csv (src/formats.cpp:92-132) of a file: up to cap segments into out, the count
+// in *n; on a malformed line returns 1 with the reference's message in msg (size msg_cap).
+int ref_read_segments_csv(const char* path, double* out, int64_t cap, int64_t* n, char* msg,
+                          int64_t msg_cap) {
+    if (msg && msg_cap > 0) msg[0] = 0;
+    try {
+        std::ifstream in(path);
+        const std::vector<voxline::Segment> v = voxline::read_segments_csv(in);
+        *n = static_cast<int64_t>(v.size());
+        for (int64_t i = 0; i < *n && i < cap; ++i) {
+            const voxline::Segment& s = v[static_cast<std::size_t>(i)];
+            const double q[6] = {s.start.x, s.start.y, s.start.z, s.end.x, s.end.y, s.end.z};
+            std::memcpy(out + 6 * i, q, sizeof q);
+        }
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        if (msg && msg_cap > 0) {
+            std::strncpy(msg, e.what(), static_cast<std::size_t>(msg_cap - 1));
+            msg[msg_cap - 1] = 0;
+        }
+        return 1;
+    } catch (...) {
+        return 5;
+    }
+}
+
+// The CLI's batch output (tools/voxline_cli.cpp:101-129 + 46-70): run_batch, then
+// write_vox3_multi (format 0) or write_xyz_multi (format 1) to path.
+int ref_batch_write(const double* segs, int64_t n, const char* path, int format) {
+    return guarded([&] {
+        const voxline::BatchResult r = voxline::run_batch(to_segments(segs, n), {64, 1});
+        std::vector<std::vector<voxline::Voxel>> chains;
+        chains.reserve(r.chains.size());
+        for (const auto& c : r.chains) chains.push_back(c.voxels);
+        std::ofstream out(path, std::ios::binary);
+        if (format == 1) voxline::write_xyz_multi(out, chains);
+        else voxline::write_vox3_multi(out, chains);
+    });
 }
 
 }  // extern "C"

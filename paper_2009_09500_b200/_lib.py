@@ -23,6 +23,7 @@ VXG_OUT_OF_RANGE = 3
 VXG_LOGIC_ERROR = 4
 VXG_CUDA_ERROR = 5
 VXG_OUT_OF_MEMORY = 6
+VXG_IO_ERROR = 7
 MEM_HOST = 0
 MEM_DEVICE = 1
 
@@ -61,8 +62,12 @@ class DeviceOutOfMemory(VoxGpuError, MemoryError):
     code = VXG_OUT_OF_MEMORY
 
 
+class IoError(VoxGpuError, OSError):  # the CLI's IoError (tools/voxline_cli.cpp:237-240)
+    code = VXG_IO_ERROR
+
+
 _EXC = {c.code: c for c in (InvalidArgument, RangeError, OutOfRange, LogicError, CudaError,
-                            DeviceOutOfMemory)}
+                            DeviceOutOfMemory, IoError)}
 
 
 class vxg_segment(C.Structure):
@@ -120,6 +125,9 @@ SIGNATURES = {
     "vxg_gen_segments": (C.c_int, [_vp, _i64, _vp, _vp, _i64, _i64, _i64, C.c_uint64, _vp,
                                    C.c_int]),
     "vxg_gen_arbitrary_batch": (C.c_int, [_vp, _i64, _i64, C.c_uint64, _vp]),
+    "vxg_read_segments_csv": (C.c_int, [C.c_char_p, C.POINTER(_vp), _i64p, _i64p]),
+    "vxg_free": (None, [_vp]),
+    "vxg_write_chains": (C.c_int, [C.c_char_p, C.c_int, _vp, _vp, _i64]),
 }
 
 _lib = None

@@ -28,6 +28,7 @@ __all__ = [
     "effective_item_count", "gen_arbitrary_batch", "gen_segment_of_length", "kernel_work_item",
     "make_plan", "round_point", "run_batch", "segment_length", "voxelize_parametric",
     "run_batch_flat", "voxelize_bitmap", "gen_segments", "pinned_empty", "Batch",
+    "read_segments_csv", "write_chains", "batch_to_file",
 ]
 
 
@@ -381,4 +382,50 @@ def compute_mvps(total_voxels: int, elapsed_ms: float) -> float:
     if total_voxels < 0:
         raise InvalidArgument("compute_mvps: negative voxel count")
     return float(total_voxels) / (elapsed_ms / 1000.0) / 1e6
+
+
+# ----------------------------------------------------------------------------- formats
+def read_segments_csv(path: str) -> np.ndarray:
+    """read_segments_csv (src/formats.cpp:92-132) -> float64 (n, 6). Malformed line ->
+    InvalidArgument naming it (the reference's message); unreadable file -> IoError."""
+    lib = _lib.load()
+    out = C.c_void_p()
+    n, bad = C.c_int64(), C.c_int64()
+    st = lib.vxg_read_segments_csv(str(path).encode(), C.byref(out), C.byref(n), C.byref(bad))
+    if st == _lib.VXG_INVALID_ARGUMENT:
+        raise InvalidArgument(f"segments csv: line {bad.value}: expected 6 finite decimal fields "
+                              "(sx,sy,sz,ex,ey,ez)")
+    if st == _lib.VXG_IO_ERROR:
+        raise _lib.IoError(f"cannot read input file: {path}")
+    if st != _lib.VXG_OK:
+        raise _lib.VoxGpuError(f"read_segments_csv: status {st}")
+    try:
+        if n.value == 0:
+            return np.zeros((0, 6))
+        buf = (C.c_double * (6 * n.value)).from_address(out.value)
+        return np.frombuffer(buf, dtype=np.float64).reshape(n.value, 6).copy()
+    finally:
+        lib.vxg_free(out)
+
+
+def write_chains(path: str, voxels: np.ndarray, chain_off: np.ndarray, format: str = "vox3"):
+    """write_vox3_multi / write_xyz_multi (src/formats.cpp:140-185) of a flat list + offsets."""
+    lib = _lib.load()
+    v = np.ascontiguousarray(voxels, dtype=np.int32).reshape(-1, 3)
+    o = np.ascontiguousarray(chain_off, dtype=np.int64)
+    fmt = {"vox3": 0, "xyz": 1}[format]
+    st = lib.vxg_write_chains(str(path).encode(), fmt, _ptr(v) if v.size else None, _ptr(o),
+                              o.shape[0] - 1)
+    if st == _lib.VXG_IO_ERROR:
+        raise _lib.IoError(f"cannot open output file: {path}")
+    if st != _lib.VXG_OK:
+        raise _lib.VoxGpuError(f"write_chains: status {st}")
+
+
+def batch_to_file(segments, path: str, format: str = "vox3") -> int:
+    """The CLI's `batch` (tools/voxline_cli.cpp:101-129) on the GPU: voxelize the batch and
+    write every chain; returns total_voxels."""
+    vox, off, total = run_batch_flat(segments)
+    write_chains(path, vox, off, format)
+    return total
 
