@@ -395,15 +395,16 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     g.nty = ceil_div(V, g.ty);
     g.ntz = ceil_div(z_hi - z_lo, g.tz);
     g.ntiles = g.ntx * g.nty * g.ntz;
-    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)(2 * g.ntiles + 1)))
+    const long long nbins = g.ntiles * vxg::tile_len_classes();
+    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)(2 * nbins + 1)))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
     g.tile_cnt = b->tile_seg.as<long long>();
-    g.tile_off = g.tile_cnt + g.ntiles;
+    g.tile_off = g.tile_cnt + nbins;
     g.words = d_words;
     g.ctl = ctl_slot(b, 3);
     cudaEventRecord(ctx->ev[2], ctx->stream);
     cudaMemsetAsync(g.ctl, 0, sizeof(Control), ctx->stream);
-    cudaMemsetAsync(g.tile_cnt, 0, sizeof(long long) * (size_t)g.ntiles, ctx->stream);
+    cudaMemsetAsync(g.tile_cnt, 0, sizeof(long long) * (size_t)nbins, ctx->stream);
     vxg::launch_tiles_count(g, ctx->stream);
     vxg::launch_tiles_scan(g, ctx->stream);
     ctx->launches += 2;

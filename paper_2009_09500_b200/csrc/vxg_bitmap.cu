@@ -228,6 +228,14 @@ __device__ __forceinline__ long long walk_pieces(const SegRec& r, long long N, c
     return inside;
 }
 
+// Bins are (tile, length class): a tile's pieces are stored grouped by length (classes of 16
+// samples), so the fill's warp steps, which run as long as their longest piece, get pieces of
+// nearly equal length. A tile's bins are consecutive: its pieces are still one CSR range.
+constexpr int kLenClasses = 16;
+__device__ __forceinline__ long long bin_of(long long tile, long long len) {
+    return tile * kLenClasses + min((len - 1) >> 4, (long long)(kLenClasses - 1));
+}
+
 __device__ __forceinline__ long long seg_steps(const TileArgs& g, long long i) {
     return __ldg(g.off + i + 1) - __ldg(g.off + i) - 1;
 }
@@ -239,7 +247,7 @@ __global__ void __launch_bounds__(256) tiles_count_kernel(TileArgs g) {
     if (i < g.n) {
         const SegRec r = load_rec(g.rec + i);
         inside = walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long, long long len, bool) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + t, 1ull);
+            atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + bin_of(t, len), 1ull);
             inbox += len;
         });
     }
@@ -253,16 +261,17 @@ __global__ void __launch_bounds__(256) tiles_count_kernel(TileArgs g) {
         atomicAdd(reinterpret_cast<unsigned long long*>(&g.ctl->total), (unsigned long long)inside);
 }
 
-// Exclusive prefix of the tile piece counts (one CTA); tile_off[ntiles] = total pieces.
+// Exclusive prefix of the (tile, class) piece counts (one CTA); tile_off[nbins] = total pieces.
 __global__ void __launch_bounds__(1024) tiles_scan_kernel(TileArgs g) {
     __shared__ long long s_warp[33];
     __shared__ long long s_carry;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const long long nbins = g.ntiles * kLenClasses;
     if (tid == 0) s_carry = 0;
     __syncthreads();
-    for (long long base = 0; base < g.ntiles; base += 1024) {
+    for (long long base = 0; base < nbins; base += 1024) {
         const long long i = base + tid;
-        const long long v = i < g.ntiles ? g.tile_cnt[i] : 0;
+        const long long v = i < nbins ? g.tile_cnt[i] : 0;
         long long incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -283,7 +292,7 @@ __global__ void __launch_bounds__(1024) tiles_scan_kernel(TileArgs g) {
             if (lane == 31) s_warp[32] = xi;
         }
         __syncthreads();
-        if (i < g.ntiles) {
+        if (i < nbins) {
             g.tile_off[i] = s_carry + s_warp[warp] + incl - v;
             g.tile_cnt[i] = 0;  // becomes the scatter cursor
         }
@@ -292,7 +301,7 @@ __global__ void __launch_bounds__(1024) tiles_scan_kernel(TileArgs g) {
         __syncthreads();
     }
     if (tid == 0) {
-        g.tile_off[g.ntiles] = s_carry;
+        g.tile_off[nbins] = s_carry;
         g.ctl->n_entries = s_carry;
     }
 }
@@ -303,14 +312,15 @@ __global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
     if (i >= g.n) return;
     const SegRec r = load_rec(g.rec + i);
     walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long ka, long long len, bool hasE) {
+        const long long bin = bin_of(t, len);
         const unsigned long long slot =
-            atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + t, 1ull);
+            atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + bin, 1ull);
         uint4 p;
         p.x = (uint32_t)i;
         p.y = (uint32_t)ka;
         p.z = (uint32_t)len | (hasE ? 0x80000000u : 0u);
         p.w = 0;
-        g.pieces[__ldg(g.tile_off + t) + (long long)slot] = p;
+        g.pieces[__ldg(g.tile_off + bin) + (long long)slot] = p;
     });
 }
 
@@ -403,7 +413,8 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         __syncthreads();  // (also orders the clearing of the previous tile's bits)
         const long long tile = s_tile[it & 1];
         if (tile >= g.ntiles) break;
-        const long long p0 = __ldg(g.tile_off + tile), p1 = __ldg(g.tile_off + tile + 1);
+        const long long p0 = __ldg(g.tile_off + tile * kLenClasses),
+                        p1 = __ldg(g.tile_off + (tile + 1) * kLenClasses);
         if (p0 == p1) continue;  // no samples: the bitmap keeps its words
         const long long txi = tile % g.ntx, tyi = (tile / g.ntx) % g.nty, tzi = tile / (g.ntx * g.nty);
         const int x0 = (int)(txi * kTX), y0 = (int)(tyi * kTY), z0 = (int)(g.z_lo + tzi * kTZ);
@@ -456,6 +467,8 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
 }
 
 // =============================================================================== launchers
+int tile_len_classes() { return kLenClasses; }
+
 int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz) {
     tx = kTX;
     ty = kTY;

@@ -57,8 +57,8 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     long long V, z_lo, z_hi;
     int tx, ty, tz;                   // tile size in voxels (tx = 256: one sector per row)
     long long ntx, nty, ntz, ntiles;  // tiles per axis of the box [0,V)^2 x [z_lo,z_hi)
-    long long* tile_cnt;              // ntiles (zeroed): pieces per tile, then scatter cursor
-    long long* tile_off;              // ntiles + 1: exclusive prefix
+    long long* tile_cnt;              // ntiles * classes (zeroed): pieces per bin, then cursor
+    long long* tile_off;              // ntiles * classes + 1: exclusive prefix
     uint4* pieces;                    // {segment, ka, len | hasE << 31, 0} binned by tile
     unsigned long long* words;        // the slab's bitmap (OR-ed into)
     Control* ctl;                     // total: in-volume samples, n_entries: pieces
@@ -100,6 +100,7 @@ cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s);   // emit pass
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
 void launch_clip(const ClipArgs& a, cudaStream_t s);
 int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz);  // -> smem bytes
+int tile_len_classes();  // piece bins per tile (length classes)
 void launch_tiles_count(const TileArgs& g, cudaStream_t s);
 void launch_tiles_scan(const TileArgs& g, cudaStream_t s);
 void launch_tiles_scatter(const TileArgs& g, cudaStream_t s);
