@@ -500,11 +500,13 @@ static cudaError_t launch_fill_g(const TileArgs& g, int num_sms, cudaStream_t s)
     return cudaGetLastError();
 }
 
-// mean_len: mean samples per piece -> lanes per piece (VXG_FILL_G overrides: 8, 16 or 32)
+// mean_len: mean samples per piece -> lanes per piece (VXG_FILL_G overrides: 4, 8, 16 or 32)
 cudaError_t launch_tiles_fill(const TileArgs& g, int num_sms, double mean_len, cudaStream_t s) {
-    // (measured: G = 8 is best for the config-3 (28) and config-5 (70) means)
-    int G = mean_len < 160.0 ? 8 : (mean_len < 320.0 ? 16 : 32);
+    // (measured with length-class bins: G = 4 is best for the config-3 (28) and config-5 (70)
+    // means, profiles/r1_fill_G)
+    int G = mean_len < 160.0 ? 4 : (mean_len < 320.0 ? 16 : 32);
     if (const char* e = getenv("VXG_FILL_G")) G = atoi(e);
+    if (G == 4) return launch_fill_g<4>(g, num_sms, s);
     if (G == 8) return launch_fill_g<8>(g, num_sms, s);
     if (G == 16) return launch_fill_g<16>(g, num_sms, s);
     return launch_fill_g<32>(g, num_sms, s);
