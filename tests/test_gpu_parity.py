@@ -265,6 +265,43 @@ def test_bitmap_clip_adversarial(vx, oracle):
         assert np.array_equal(words, ow), (z0, z1)
 
 
+def test_bitmap_tiles_adversarial(vx, oracle):
+    """The tile-binned path (V % 128 == 0): half-integer endpoints (ties on every tile and slab
+    boundary), nearly-flat axes, descending directions, segments leaving the volume, partial
+    x/y/z tiles (V = 384, 640) and slabs that cut tiles; bit-exact against the oracle."""
+    rng = np.random.default_rng(41)
+    for V in (128, 384, 640):
+        segs = np.round(rng.uniform(-20, V + 20, size=(8000, 6)) * 2) / 2
+        segs[::4, 5] = segs[::4, 2] + 1e-13          # flat z
+        segs[1::4, 3] = segs[1::4, 0] - 1e-12         # flat x, descending
+        long_ = rng.uniform(0, V - 1, size=(500, 6))  # long segments across many tiles
+        segs = np.concatenate([segs, long_])
+        words, outside = vx.voxelize_bitmap(segs, V, clip=False)
+        ow, oo = oracle.bitmap(segs, V)
+        assert np.array_equal(words, ow), V
+        assert outside == oo, V
+        for z0, z1 in [(0, 70), (69, min(141, V)), (V // 3, V // 3 + 1), (V - 71, V)]:
+            words, _ = vx.voxelize_bitmap(segs, V, z0, z1, clip=True)
+            ow, _ = oracle.bitmap(segs, V, z0, z1)
+            assert np.array_equal(words, ow), (V, z0, z1)
+
+
+def test_bitmap_tiles_accumulate_and_match_atomic_path(vx, oracle, monkeypatch):
+    """Words are OR-ed into (the caller's bits survive), and the tile path equals the generic
+    global-atomic path on the same batch."""
+    segs = vx.gen_segments(3000, 0, 300, 512, 17)
+    b = vx.Batch(segs)
+    prior = np.zeros(512 ** 3 // 64, np.uint64)
+    prior[::97] = np.uint64(0x8000000000000001)
+    w_tiles, _ = b.emit_bitmap(512, 0, 512, words=prior.copy())
+    monkeypatch.setenv("VXG_BITMAP_ATOMIC", "1")
+    w_atomic, _ = b.emit_bitmap(512, 0, 512, words=prior.copy())
+    b.close()
+    ow, _ = oracle.bitmap(segs, 512)
+    assert np.array_equal(w_tiles, ow | prior)
+    assert np.array_equal(w_atomic, w_tiles)
+
+
 # ------------------------------------------------------------------ device-resident (torch)
 def test_torch_device_buffers(vx, oracle):
     import torch
