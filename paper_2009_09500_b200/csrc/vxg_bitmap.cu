@@ -367,26 +367,37 @@ __device__ __forceinline__ void load_piece(const TileArgs& g, long long p, long 
 }
 
 // Set the bits of one piece group (G lanes per piece, 32/G pieces per warp).
+// OR a bit into the tile through a 32-bit shared address; the predicate keeps the row loop
+// branch-free (lanes past their piece's end compute but do not store).
+__device__ __forceinline__ void red_or_shared(uint32_t saddr, uint32_t bit, bool on) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}"
+                 ::"r"(saddr), "r"(bit), "r"((uint32_t)on)
+                 : "memory");
+}
+
+// Set the bits of one piece group (G lanes per piece, 32/G pieces per warp). sbase: the shared
+// byte address of the tile's word 0 minus 4 * (the tile's global word base).
 template <int G>
-__device__ __forceinline__ void fill_piece(uint32_t* bits, const PieceRef& q, int gl, int base) {
+__device__ __forceinline__ void fill_piece(uint32_t sbase, const PieceRef& q, int gl) {
     int mx = q.len;
 #pragma unroll
     for (int o = G; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     double t = __ll2double_rn(q.ka + gl);
     const int steps = (mx + G - 1) / G;
     int j = gl;
+#pragma unroll 4
     for (int st = 0; st < steps; ++st) {
-        if (j < q.len) {
-            const int32_t x = round_pos(sample_axis(q.r.sx, q.r.wx, t));
-            const int32_t y = round_pos(sample_axis(q.r.sy, q.r.wy, t));
-            const int32_t z = round_pos(sample_axis(q.r.sz, q.r.wz, t));
-            atomicOr(bits + (z * kSS + y * kRW + (x >> 5) - base), 1u << (x & 31));
-        }
+        const int32_t x = round_pos(sample_axis(q.r.sx, q.r.wx, t));
+        const int32_t y = round_pos(sample_axis(q.r.sy, q.r.wy, t));
+        const int32_t z = round_pos(sample_axis(q.r.sz, q.r.wz, t));
+        const uint32_t w = (uint32_t)(z * kSS + y * kRW + (x >> 5));
+        red_or_shared(sbase + 4u * w, 1u << (x & 31), j < q.len);
         t = __dadd_rn(t, (double)G);
         j += G;
     }
     if (q.hasE && gl == 0)
-        atomicOr(bits + (q.r.ez * kSS + q.r.ey * kRW + (q.r.ex >> 5) - base), 1u << (q.r.ex & 31));
+        red_or_shared(sbase + 4u * (uint32_t)(q.r.ez * kSS + q.r.ey * kRW + (q.r.ex >> 5)),
+                      1u << (q.r.ex & 31), true);
 }
 
 // Persistent CTAs: claim a tile, set its samples' bits in shared memory, OR it into the bitmap.
@@ -419,12 +430,13 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         const long long txi = tile % g.ntx, tyi = (tile / g.ntx) % g.nty, tzi = tile / (g.ntx * g.nty);
         const int x0 = (int)(txi * kTX), y0 = (int)(tyi * kTY), z0 = (int)(g.z_lo + tzi * kTZ);
         const int base = z0 * kSS + y0 * kRW + (x0 >> 5);  // (x0 is a multiple of 32)
+        const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bits) - 4u * (uint32_t)base;
         // warp steps of 32/G pieces (G lanes per piece); a step's pieces load together
         constexpr long long step = (long long)NW * PPW;
         for (long long pb = p0 + (long long)warp * PPW; pb < p1; pb += step) {
             PieceRef q;
             load_piece(g, pb + grp, p1, q);
-            fill_piece<G>(bits, q, gl, base);
+            fill_piece<G>(sbase, q, gl);
         }
         __syncthreads();
         // OR the tile into the bitmap: a row of kTX bits is 4 words = 2 x 16 B; each thread
