@@ -405,6 +405,16 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     cudaEventRecord(ctx->ev[2], ctx->stream);
     cudaMemsetAsync(g.ctl, 0, sizeof(Control), ctx->stream);
     cudaMemsetAsync(g.tile_cnt, 0, sizeof(long long) * (size_t)nbins, ctx->stream);
+    // walk order grouped by segment length (pays off when lengths vary: long batches only)
+    if (b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256) {
+        if (!b->ent_off.ensure(ctx, sizeof(int) * (size_t)b->n + 64 * sizeof(long long)))
+            return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
+        g.perm_cur = b->ent_off.as<long long>();
+        g.perm = reinterpret_cast<int*>(g.perm_cur + 64);
+        cudaMemsetAsync(g.perm_cur, 0, 64 * sizeof(long long), ctx->stream);
+        vxg::launch_tiles_perm(g, ctx->stream);
+        ctx->launches += 3;
+    }
     vxg::launch_tiles_count(g, ctx->stream);
     vxg::launch_tiles_scan(g, ctx->stream);
     ctx->launches += 2;

@@ -240,11 +240,71 @@ __device__ __forceinline__ long long seg_steps(const TileArgs& g, long long i) {
     return __ldg(g.off + i + 1) - __ldg(g.off + i) - 1;
 }
 
+// Walk order: segments grouped by length (32 buckets of N / 64), so the 32 segments a warp walks
+// in lock step have similar piece counts (the warp runs as long as its longest walk).
+constexpr int kLenBuckets = 32;
+__device__ __forceinline__ int len_bucket(long long N) { return (int)min(N >> 6, (long long)kLenBuckets - 1); }
+
+__global__ void __launch_bounds__(256) perm_hist_kernel(TileArgs g) {
+    __shared__ unsigned s_h[kLenBuckets];
+    if (threadIdx.x < kLenBuckets) s_h[threadIdx.x] = 0;
+    __syncthreads();
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < g.n) atomicAdd(&s_h[len_bucket(seg_steps(g, i))], 1u);
+    __syncthreads();
+    if (threadIdx.x < kLenBuckets && s_h[threadIdx.x])
+        atomicAdd(reinterpret_cast<unsigned long long*>(g.perm_cur) + threadIdx.x,
+                  (unsigned long long)s_h[threadIdx.x]);
+}
+
+// perm_cur holds the bucket counts on entry; every CTA reserves its range per bucket.
+__global__ void __launch_bounds__(256) perm_scatter_kernel(TileArgs g) {
+    __shared__ unsigned s_h[kLenBuckets];
+    __shared__ unsigned long long s_base[kLenBuckets];
+    if (threadIdx.x < kLenBuckets) s_h[threadIdx.x] = 0;
+    __syncthreads();
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    int b = 0;
+    unsigned rank = 0;
+    if (i < g.n) {
+        b = len_bucket(seg_steps(g, i));
+        rank = atomicAdd(&s_h[b], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < kLenBuckets && s_h[threadIdx.x]) {
+        // bucket start = sum of the counts of the smaller buckets (kept in perm_cur[32..63])
+        s_base[threadIdx.x] = g.perm_cur[kLenBuckets + threadIdx.x] +
+            atomicAdd(reinterpret_cast<unsigned long long*>(g.perm_cur) + threadIdx.x,
+                      (unsigned long long)s_h[threadIdx.x]);
+    }
+    __syncthreads();
+    if (i < g.n) g.perm[s_base[b] + rank] = (int)i;
+}
+
+// Bucket starts from the counts (one warp): perm_cur[32 + b] = exclusive prefix, counts reset.
+__global__ void perm_scan_kernel(TileArgs g) {
+    const int lane = threadIdx.x;
+    const long long v = g.perm_cur[lane];
+    long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    g.perm_cur[kLenBuckets + lane] = incl - v;
+    g.perm_cur[lane] = 0;
+}
+
+__device__ __forceinline__ long long walk_segment(const TileArgs& g, long long t) {
+    return g.perm ? (long long)__ldg(g.perm + t) : t;
+}
+
 // Pass A: pieces per tile, in-volume samples.
 __global__ void __launch_bounds__(256) tiles_count_kernel(TileArgs g) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     long long inside = 0, inbox = 0;
-    if (i < g.n) {
+    if (tix < g.n) {
+        const long long i = walk_segment(g, tix);
         const SegRec r = load_rec(g.rec + i);
         inside = walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long, long long len, bool) {
             atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + bin_of(t, len), 1ull);
@@ -308,8 +368,9 @@ __global__ void __launch_bounds__(1024) tiles_scan_kernel(TileArgs g) {
 
 // Pass B: write the pieces into their tiles' bins.
 __global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= g.n) return;
+    const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tix >= g.n) return;
+    const long long i = walk_segment(g, tix);
     const SegRec r = load_rec(g.rec + i);
     walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long ka, long long len, bool hasE) {
         const long long bin = bin_of(t, len);
@@ -488,6 +549,13 @@ int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz) {
     (void)V;
     (void)depth;
     return kTileWords * 4;  // shared-memory bytes (padded z-slices)
+}
+
+void launch_tiles_perm(const TileArgs& g, cudaStream_t s) {
+    const unsigned grid = (unsigned)((g.n + 255) / 256);
+    perm_hist_kernel<<<grid, 256, 0, s>>>(g);
+    perm_scan_kernel<<<1, 32, 0, s>>>(g);
+    perm_scatter_kernel<<<grid, 256, 0, s>>>(g);
 }
 
 void launch_tiles_count(const TileArgs& g, cudaStream_t s) {

@@ -62,6 +62,8 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     uint4* pieces;                    // {segment, ka, len | hasE << 31, 0} binned by tile
     unsigned long long* words;        // the slab's bitmap (OR-ed into)
     Control* ctl;                     // total: in-volume samples, n_entries: pieces
+    int* perm;                        // walk order (segments grouped by length) or null
+    long long* perm_cur;              // 64: bucket counts / cursors, bucket starts (zeroed)
 };
 
 struct ClipArgs {
@@ -101,6 +103,7 @@ cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
 void launch_clip(const ClipArgs& a, cudaStream_t s);
 int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz);  // -> smem bytes
 int tile_len_classes();  // piece bins per tile (length classes)
+void launch_tiles_perm(const TileArgs& g, cudaStream_t s);  // length-grouped walk order
 void launch_tiles_count(const TileArgs& g, cudaStream_t s);
 void launch_tiles_scan(const TileArgs& g, cudaStream_t s);
 void launch_tiles_scatter(const TileArgs& g, cudaStream_t s);
