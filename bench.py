@@ -217,6 +217,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--segments", type=int, default=0, help="override the segment count")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: ranks may share one GPU (functional test of the N > 1 path)")
     args = ap.parse_args()
     cfg = dict(WORKLOADS[args.workload])
     if args.segments:
@@ -226,10 +228,15 @@ def main():
 
     import torch
     world, rank, local = dist_setup(args)
+    if args.dist_backend == "gloo":  # functional check of the N > 1 path on a one-GPU box
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     import paper_2009_09500_b200 as vx
     ctx = vx.Context(local)
     # one dedicated stream for everything: the library's kernels, torch's allocations and the

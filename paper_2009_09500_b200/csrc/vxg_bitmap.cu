@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(1024) tiles_scan_kernel(TileArgs g) {
         __syncthreads();
         if (i < nbins) {
             g.tile_off[i] = s_carry + s_warp[warp] + incl - v;
-            g.tile_cnt[i] = 0;  // becomes the scatter cursor
+            g.tile_cnt[i] = s_carry + s_warp[warp] + incl - v;  // the scatter's cursor
         }
         __syncthreads();
         if (tid == 0) s_carry += s_warp[32];
@@ -366,23 +366,26 @@ __global__ void __launch_bounds__(1024) tiles_scan_kernel(TileArgs g) {
     }
 }
 
-// Pass B: write the pieces into their tiles' bins.
+// Pass B: write the pieces into their tiles' bins. tile_cnt holds every bin's start on entry (the
+// scan wrote it), so the slot is one atomicAdd; the store of a piece is deferred to the next
+// piece so the atomic's round trip overlaps the walk instead of stalling it.
 __global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
     const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (tix >= g.n) return;
     const long long i = walk_segment(g, tix);
     const SegRec r = load_rec(g.rec + i);
+    bool pending = false;
+    unsigned long long pslot = 0;
+    uint4 pp = make_uint4(0, 0, 0, 0);
     walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long ka, long long len, bool hasE) {
-        const long long bin = bin_of(t, len);
         const unsigned long long slot =
-            atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + bin, 1ull);
-        uint4 p;
-        p.x = (uint32_t)i;
-        p.y = (uint32_t)ka;
-        p.z = (uint32_t)len | (hasE ? 0x80000000u : 0u);
-        p.w = 0;
-        g.pieces[__ldg(g.tile_off + bin) + (long long)slot] = p;
+            atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + bin_of(t, len), 1ull);
+        if (pending) g.pieces[pslot] = pp;
+        pending = true;
+        pslot = slot;
+        pp = make_uint4((uint32_t)i, (uint32_t)ka, (uint32_t)len | (hasE ? 0x80000000u : 0u), 0u);
     });
+    if (pending) g.pieces[pslot] = pp;
 }
 
 // Persistent CTAs: claim a tile, set its samples' bits in shared memory, OR it into the bitmap.
