@@ -317,7 +317,8 @@ def main():
     emit_avg = statistics.mean(emit_ms)
     if kind in ("list", "single"):
         alg_bytes = 12 * units + 8 * (n + 1) + 48 * n
-        dominant = "list_emit_kernel"
+        dominant = "list_fused_kernel (count + emit tasks overlapped)" \
+            if capacity >= 43_000_000 else "list_emit_kernel"
     else:
         alg_bytes = 8 * ((V * V * (z_hi - z_lo) + 63) // 64) + 48 * n
         dominant = "tiles_fill_kernel"

@@ -279,30 +279,48 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
                             int64_t* total) {
     vxg_context* ctx = b->ctx;
     const int64_t blk = vxg::list_block_samples();
-    // equal contiguous ranges, one per resident warp, in whole staging blocks
-    int64_t nranges = vxg::list_ranges(ctx->num_sms);
+    const int64_t warps = vxg::list_resident_warps(ctx->num_sms);
+    // Large batches: the fused kernel over 4 ranges per resident warp (count and emit tasks
+    // overlap); small ones: one range per warp, count pass + scan + emit pass.
+    static const char* mode_env = std::getenv("VXG_LIST_MODE");
+    const bool fused = mode_env ? std::strcmp(mode_env, "fused") == 0
+                                : b->capacity >= (int64_t)warps * 4 * 4 * blk;
+    int64_t nranges = fused ? 4 * warps : warps;
     const int64_t blocks = ceil_div(b->capacity, blk);
     int64_t range_len = ceil_div(blocks, nranges) * blk;
     nranges = ceil_div(b->capacity, range_len);
     if (!b->ranges.ensure(ctx, sizeof(long long) * (size_t)(4 * nranges + 1)))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
+    if (fused && !b->status.ensure(ctx, sizeof(unsigned long long) *
+                                            (size_t)std::max<int64_t>(nranges, vxg::plan_tile_count(b->n))))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
     if ((reinterpret_cast<uintptr_t>(d_out) & 3u) != 0)
         return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_voxelize: output must be 4-byte aligned");
     cudaMemsetAsync(ctl_slot(b, 1), 0, sizeof(Control), ctx->stream);
     long long* rc = b->ranges.as<long long>();
     vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->n, b->capacity, nranges,
-                    range_len, rc, rc + 3 * nranges, d_out, out_cap, d_chain, ctl_slot(b, 1)};
-    cudaEventRecord(ctx->ev[2], ctx->stream);
-    cudaError_t e = vxg::launch_list_count(a, ctx->stream);
-    cudaEventRecord(ctx->ev[3], ctx->stream);
-    if (e == cudaSuccess) e = vxg::launch_list_emit(a, ctx->stream);
-    ctx->launches += 3;
+                    range_len, rc, rc + 3 * nranges, d_out, out_cap, d_chain, ctl_slot(b, 1),
+                    fused ? b->status.as<unsigned long long>() : nullptr, warps};
+    cudaError_t e;
+    if (fused) {
+        cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)nranges, ctx->stream);
+        cudaEventRecord(ctx->ev[2], ctx->stream);
+        cudaEventRecord(ctx->ev[3], ctx->stream);
+        e = vxg::launch_list_fused(a, ctx->num_sms, ctx->stream);
+        ctx->launches += 1;
+    } else {
+        cudaEventRecord(ctx->ev[2], ctx->stream);
+        e = vxg::launch_list_count(a, ctx->stream);
+        cudaEventRecord(ctx->ev[3], ctx->stream);
+        if (e == cudaSuccess) e = vxg::launch_list_emit(a, ctx->stream);
+        ctx->launches += 3;
+    }
     cudaEventRecord(ctx->ev[4], ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "list emit");
     Control c;
     vxg_status s = read_ctl(ctx, ctl_slot(b, 1), c, "batch_voxelize");
     cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);   // count pass + range scan
-    cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);  // emit pass
+    cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);  // emit pass (fused: both)
     if (s) return s;
     *total = c.total;
     return VXG_OK;

@@ -473,6 +473,126 @@ __global__ void __launch_bounds__(NW * 32, 3) list_emit_kernel(ListArgs a) {
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ONE kernel for both passes, overlapping them: every warp takes tasks from two in-order queues
+// over finer ranges -- "count range r" and "emit range r" -- keeping the counts up to LA ranges
+// ahead of the emits. A count task publishes its range's kept count (decoupled look-back status
+// word, flag A); an emit task waits for its own count, resolves its prefix by look-back (the
+// counts are already there) and publishes its inclusive prefix (flag P) before streaming its
+// records out exactly as list_emit_kernel does. The count pass (FP64/issue-bound) and the emit
+// pass (HBM-write-bound) share every SM instead of running back to back.
+// Progress: an emit task whose count has not been claimed claims counts itself until it has, so
+// a warp never waits on work nobody owns; count tasks never wait.
+template <int NW, int IPT>
+__global__ void __launch_bounds__(NW * 32, 3) list_fused_kernel(ListArgs a) {
+    constexpr int CH = 32 * IPT;
+    constexpr int REGION = 3 * CH + 4;
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* region = smem + warp * REGION;
+    unsigned long long* cticket = &a.ctl->tile_counter;
+    unsigned long long* eticket = reinterpret_cast<unsigned long long*>(&a.ctl->pad0);
+    const long long R = a.nranges;
+    auto count_range = [&](long long r) {
+        const long long f0 = r * a.range_len, f1 = min(f0 + a.range_len, a.total_samples);
+        long long cnt = 0;
+        if (f0 < f1) {
+            Walk W;
+            walk_start(a, f0, W);
+            cnt = walk_block<(1 << 30), false>(a, W, f0, f1, nullptr, 0);
+        }
+        if (lane == 0) lookback_publish(a.status, r, cnt);
+    };
+    for (;;) {
+        // ---- choose: a count task while the counts are less than LA ranges ahead
+        long long task = 0;
+        int kind = 1;
+        if (lane == 0) {
+            const unsigned long long c = ld_relaxed_u64(cticket), e = ld_relaxed_u64(eticket);
+            if ((long long)c < R && c < e + a.lookahead) {
+                const unsigned long long t = atomicAdd(cticket, 1ull);
+                if ((long long)t < R) {
+                    kind = 0;
+                    task = (long long)t;
+                }
+            }
+            if (kind) task = (long long)atomicAdd(eticket, 1ull);
+        }
+        kind = __shfl_sync(0xffffffffu, kind, 0);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (kind == 0) {
+            count_range(task);
+            continue;
+        }
+        const long long r = task;
+        if (r >= R) break;
+        // ---- make sure range r's count is owned by someone (claim counts up to r ourselves)
+        while (true) {
+            unsigned long long c = 0;
+            if (lane == 0) c = ld_relaxed_u64(cticket);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            if ((long long)c > r) break;
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(cticket, 1ull);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if ((long long)t < R) count_range((long long)t);
+        }
+        // ---- own count (flag A or P set by its count task), then the prefix by look-back
+        unsigned long long sw = 0;
+        if (lane == 0) {
+            unsigned spins = 0;
+            while (((sw = ld_relaxed_u64(&a.status[r])) >> 62) == 0) {
+                __nanosleep(64);
+                if (++spins > (1u << 24)) {  // watchdog: report instead of hanging the GPU
+                    atomicExch(&a.ctl->abort, 1);
+                    break;
+                }
+            }
+        }
+        sw = __shfl_sync(0xffffffffu, sw, 0);
+        const long long cnt = (long long)(sw & kValMask);
+        const long long pre = lookback_resolve(a.status, r, cnt, a.ctl);
+        if (r == R - 1 && lane == 0) {  // the last range knows the total
+            a.chain_off[a.nseg] = pre + cnt;
+            a.ctl->total = pre + cnt;
+        }
+        if (pre + cnt > a.out_cap) {  // caller's buffer too small: write nothing
+            if (lane == 0) record_error(a.ctl, 0, 4);
+            continue;
+        }
+        // ---- emit range r from its known output position (as list_emit_kernel)
+        const long long f0 = r * a.range_len, f1 = min(f0 + a.range_len, a.total_samples);
+        long long pos = pre;
+        Walk W;
+        if (f0 < f1) walk_start(a, f0, W);
+        for (long long b = f0; b < f1; b += CH) {
+            const uintptr_t g0 = reinterpret_cast<uintptr_t>(a.out) + 12ull * (unsigned long long)pos;
+            const int skew = (int)((g0 & 15u) >> 2);
+            uint32_t* stage = region + skew;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+            const int cn = walk_block<IPT, true>(a, W, b, min(b + CH, f1), stage, pos);
+            const uintptr_t g1 = g0 + 12ull * (unsigned)cn;
+            const uintptr_t a0 = (g0 + 15) & ~(uintptr_t)15;
+            const uintptr_t a1 = g1 & ~(uintptr_t)15;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (a1 > a0) {
+                const int hw = (int)((a0 - g0) >> 2), tw = (int)((g1 - a1) >> 2);
+                if (lane == 0) bulk_store(reinterpret_cast<void*>(a0), stage + hw, (unsigned)(a1 - a0));
+                if (lane < hw) reinterpret_cast<uint32_t*>(g0)[lane] = stage[lane];
+                else if (lane >= 4 && lane - 4 < tw)
+                    reinterpret_cast<uint32_t*>(a1)[lane - 4] =
+                        stage[hw + (int)((a1 - a0) >> 2) + (lane - 4)];
+            } else {
+                const int nw = (int)((g1 - g0) >> 2);
+                if (lane < nw) reinterpret_cast<uint32_t*>(g0)[lane] = stage[lane];
+            }
+            pos += cn;
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // =============================================================================== emit: bitmap
 // Same row walker over a flat sample space of entries (segments, or clipped in-slab k-ranges);
 // every sample voxel inside [0,V)^2 x [z_lo,z_hi) sets its bit.
@@ -600,10 +720,27 @@ long long list_ranges(int num_sms) {
     return n;
 }
 
+int list_resident_warps(int num_sms) { return (int)list_ranges(num_sms); }
+
 cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s) {
     const unsigned grid = (unsigned)((a.nranges * kCountSplit + kListNW - 1) / kListNW);
     list_count_kernel<kListNW><<<grid, kListNW * 32, 0, s>>>(a);
     range_scan_kernel<<<1, 1024, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// Fused launch: persistent CTAs (as many as fit), ranges = a.nranges (finer than one per warp).
+cudaError_t launch_list_fused(const ListArgs& a, int num_sms, cudaStream_t s) {
+    const size_t smem = (size_t)kListNW * (3 * 32 * kListIPT + 4) * 4;
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaFuncSetAttribute(list_fused_kernel<kListNW, kListIPT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, list_fused_kernel<kListNW, kListIPT>,
+                                                      kListNW * 32, smem);
+        if (per_sm < 1) per_sm = 1;
+    }
+    list_fused_kernel<kListNW, kListIPT><<<(unsigned)(per_sm * num_sms), kListNW * 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -37,6 +37,8 @@ struct ListArgs {
     long long out_cap;
     long long* chain_off;       // nseg + 1
     Control* ctl;
+    unsigned long long* status; // fused kernel: nranges look-back words (zeroed)
+    long long lookahead;        // fused kernel: max count tasks ahead of the emit tasks
 };
 
 struct BitmapArgs {
@@ -99,6 +101,8 @@ void launch_tile_index(const long long* off, long long n_entries, int ts_log2, l
                        cudaStream_t s);
 cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s);  // count pass + range scan
 cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s);   // emit pass
+cudaError_t launch_list_fused(const ListArgs& a, int num_sms, cudaStream_t s);  // both, overlapped
+int list_resident_warps(int num_sms);
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
 void launch_clip(const ClipArgs& a, cudaStream_t s);
 int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz);  // -> smem bytes
