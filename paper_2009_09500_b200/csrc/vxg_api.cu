@@ -414,10 +414,11 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     g.ntz = ceil_div(z_hi - z_lo, g.tz);
     g.ntiles = g.ntx * g.nty * g.ntz;
     const long long nbins = g.ntiles * vxg::tile_len_classes();
-    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)(2 * nbins + 1)))
+    if (!b->tile_seg.ensure(ctx, sizeof(long long) * (size_t)(2 * nbins + 1) + 4 * (size_t)nbins))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
     g.tile_cnt = b->tile_seg.as<long long>();
     g.tile_off = g.tile_cnt + nbins;
+    g.tile_cur = reinterpret_cast<unsigned*>(g.tile_off + nbins + 1);
     g.words = d_words;
     g.ctl = ctl_slot(b, 3);
     cudaEventRecord(ctx->ev[2], ctx->stream);
@@ -425,11 +426,12 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     cudaMemsetAsync(g.tile_cnt, 0, sizeof(long long) * (size_t)nbins, ctx->stream);
     // walk order grouped by segment length (pays off when lengths vary: long batches only)
     if (b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256) {
-        if (!b->ent_off.ensure(ctx, sizeof(int) * (size_t)b->n + 64 * sizeof(long long)))
+        const size_t keys = (size_t)vxg::tile_perm_keys();
+        if (!b->ent_off.ensure(ctx, sizeof(int) * (size_t)b->n + keys * sizeof(long long)))
             return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
         g.perm_cur = b->ent_off.as<long long>();
-        g.perm = reinterpret_cast<int*>(g.perm_cur + 64);
-        cudaMemsetAsync(g.perm_cur, 0, 64 * sizeof(long long), ctx->stream);
+        g.perm = reinterpret_cast<int*>(g.perm_cur + keys);
+        cudaMemsetAsync(g.perm_cur, 0, keys * sizeof(long long), ctx->stream);
         vxg::launch_tiles_perm(g, ctx->stream);
         ctx->launches += 3;
     }
@@ -440,6 +442,9 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     vxg_status s = read_ctl(ctx, g.ctl, c, "bitmap");
     if (s) return s;
     const long long npieces = c.n_entries;
+    if (npieces >= (1ll << 32))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: %lld pieces exceed the 32-bit bin cursors; "
+                         "split the batch", npieces);
     const long long in_box = (long long)c.outside;  // samples inside the slab box
     if (outside) *outside = b->capacity - c.total;
     if (npieces == 0) {

@@ -243,56 +243,89 @@ __device__ __forceinline__ long long seg_steps(const TileArgs& g, long long i) {
 // Walk order: segments grouped by length (32 buckets of N / 64), so the 32 segments a warp walks
 // in lock step have similar piece counts (the warp runs as long as its longest walk).
 constexpr int kLenBuckets = 32;
+constexpr int kCellsPerAxis = 16;  // coarse spatial cells (16^3) of the box
+constexpr int kPermKeys = kLenBuckets * kCellsPerAxis * kCellsPerAxis * kCellsPerAxis;
 __device__ __forceinline__ int len_bucket(long long N) { return (int)min(N >> 6, (long long)kLenBuckets - 1); }
 
+// Walk-order key: length bucket (major) then the coarse cell of round(S) (minor). Lanes of a
+// warp then walk equally long segments (the warp runs as long as its longest walk) that start
+// near each other, so their pieces land in neighbouring bins (the scatter's writes and atomics
+// stay L2-local).
+__device__ __forceinline__ int perm_key(const TileArgs& g, long long i) {
+    const SegRec r = load_rec(g.rec + i);
+    const long long V = g.V, D = g.z_hi - g.z_lo;
+    auto cell = [](long long v, long long ext) {
+        const long long c = v < 0 ? 0 : (v >= ext ? ext - 1 : v);
+        return (int)(c * kCellsPerAxis / ext);
+    };
+    const long long sx = axis_round(r.sx, r.wx, 0), sy = axis_round(r.sy, r.wy, 0),
+                    sz = axis_round(r.sz, r.wz, 0) - g.z_lo;
+    const int c = (cell(sz, D) * kCellsPerAxis + cell(sy, V)) * kCellsPerAxis + cell(sx, V);
+    return len_bucket(seg_steps(g, i)) * (kCellsPerAxis * kCellsPerAxis * kCellsPerAxis) + c;
+}
+
 __global__ void __launch_bounds__(256) perm_hist_kernel(TileArgs g) {
-    __shared__ unsigned s_h[kLenBuckets];
-    if (threadIdx.x < kLenBuckets) s_h[threadIdx.x] = 0;
-    __syncthreads();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < g.n) atomicAdd(&s_h[len_bucket(seg_steps(g, i))], 1u);
-    __syncthreads();
-    if (threadIdx.x < kLenBuckets && s_h[threadIdx.x])
-        atomicAdd(reinterpret_cast<unsigned long long*>(g.perm_cur) + threadIdx.x,
-                  (unsigned long long)s_h[threadIdx.x]);
+    if (i >= g.n) return;
+    const int k = perm_key(g, i);
+    // warp-aggregated: lanes with the same key add once
+    const unsigned peers = __match_any_sync(__activemask(), k);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1)
+        atomicAdd(reinterpret_cast<unsigned long long*>(g.perm_cur) + k,
+                  (unsigned long long)__popc(peers));
 }
 
-// perm_cur holds the bucket counts on entry; every CTA reserves its range per bucket.
+// perm_cur[key] holds the bucket start on entry (perm_scan_kernel): positions by atomics.
 __global__ void __launch_bounds__(256) perm_scatter_kernel(TileArgs g) {
-    __shared__ unsigned s_h[kLenBuckets];
-    __shared__ unsigned long long s_base[kLenBuckets];
-    if (threadIdx.x < kLenBuckets) s_h[threadIdx.x] = 0;
-    __syncthreads();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    int b = 0;
-    unsigned rank = 0;
-    if (i < g.n) {
-        b = len_bucket(seg_steps(g, i));
-        rank = atomicAdd(&s_h[b], 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x < kLenBuckets && s_h[threadIdx.x]) {
-        // bucket start = sum of the counts of the smaller buckets (kept in perm_cur[32..63])
-        s_base[threadIdx.x] = g.perm_cur[kLenBuckets + threadIdx.x] +
-            atomicAdd(reinterpret_cast<unsigned long long*>(g.perm_cur) + threadIdx.x,
-                      (unsigned long long)s_h[threadIdx.x]);
-    }
-    __syncthreads();
-    if (i < g.n) g.perm[s_base[b] + rank] = (int)i;
+    if (i >= g.n) return;
+    const int k = perm_key(g, i);
+    const unsigned peers = __match_any_sync(__activemask(), k);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long base = 0;
+    if ((threadIdx.x & 31) == leader)
+        base = atomicAdd(reinterpret_cast<unsigned long long*>(g.perm_cur) + k,
+                         (unsigned long long)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    const unsigned below = peers & ((1u << (threadIdx.x & 31)) - 1u);
+    g.perm[base + __popc(below)] = (int)i;
 }
 
-// Bucket starts from the counts (one warp): perm_cur[32 + b] = exclusive prefix, counts reset.
-__global__ void perm_scan_kernel(TileArgs g) {
-    const int lane = threadIdx.x;
-    const long long v = g.perm_cur[lane];
-    long long incl = v;
+// Exclusive prefix of the kPermKeys bucket counts, in place (one CTA).
+__global__ void __launch_bounds__(1024) perm_scan_kernel(TileArgs g) {
+    __shared__ long long s_warp[33];
+    __shared__ long long s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int base = 0; base < kPermKeys; base += 1024) {
+        const int i = base + tid;
+        const long long v = g.perm_cur[i];
+        long long incl = v;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const long long x = s_warp[lane];
+            long long xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long t = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += t;
+            }
+            s_warp[lane] = xi - x;
+            if (lane == 31) s_warp[32] = xi;
+        }
+        __syncthreads();
+        g.perm_cur[i] = s_carry + s_warp[warp] + incl - v;
+        __syncthreads();
+        if (tid == 0) s_carry += s_warp[32];
+        __syncthreads();
     }
-    g.perm_cur[kLenBuckets + lane] = incl - v;
-    g.perm_cur[lane] = 0;
 }
 
 __device__ __forceinline__ long long walk_segment(const TileArgs& g, long long t) {
@@ -354,7 +387,7 @@ __global__ void __launch_bounds__(1024) tiles_scan_kernel(TileArgs g) {
         __syncthreads();
         if (i < nbins) {
             g.tile_off[i] = s_carry + s_warp[warp] + incl - v;
-            g.tile_cnt[i] = s_carry + s_warp[warp] + incl - v;  // the scatter's cursor
+            g.tile_cur[i] = (unsigned)(s_carry + s_warp[warp] + incl - v);  // scatter cursor
         }
         __syncthreads();
         if (tid == 0) s_carry += s_warp[32];
@@ -366,7 +399,7 @@ __global__ void __launch_bounds__(1024) tiles_scan_kernel(TileArgs g) {
     }
 }
 
-// Pass B: write the pieces into their tiles' bins. tile_cnt holds every bin's start on entry (the
+// Pass B: write the pieces into their tiles' bins. tile_cur holds every bin's start on entry (the
 // scan wrote it), so the slot is one atomicAdd; the store of a piece is deferred to the next
 // piece so the atomic's round trip overlaps the walk instead of stalling it.
 __global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
@@ -375,15 +408,15 @@ __global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
     const long long i = walk_segment(g, tix);
     const SegRec r = load_rec(g.rec + i);
     bool pending = false;
-    unsigned long long pslot = 0;
+    unsigned pslot = 0;
     uint4 pp = make_uint4(0, 0, 0, 0);
     walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long ka, long long len, bool hasE) {
-        const unsigned long long slot =
-            atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + bin_of(t, len), 1ull);
+        // store the previous piece first: its slot arrived while this piece was being walked;
+        // the new atomic's result lands directly in pslot and is not read until the next piece
         if (pending) g.pieces[pslot] = pp;
-        pending = true;
-        pslot = slot;
+        pslot = atomicAdd(g.tile_cur + bin_of(t, len), 1u);  // 32-bit: one register
         pp = make_uint4((uint32_t)i, (uint32_t)ka, (uint32_t)len | (hasE ? 0x80000000u : 0u), 0u);
+        pending = true;
     });
     if (pending) g.pieces[pslot] = pp;
 }
@@ -544,6 +577,7 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
 
 // =============================================================================== launchers
 int tile_len_classes() { return kLenClasses; }
+int tile_perm_keys() { return kPermKeys; }
 
 int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz) {
     tx = kTX;
@@ -557,7 +591,7 @@ int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz) {
 void launch_tiles_perm(const TileArgs& g, cudaStream_t s) {
     const unsigned grid = (unsigned)((g.n + 255) / 256);
     perm_hist_kernel<<<grid, 256, 0, s>>>(g);
-    perm_scan_kernel<<<1, 32, 0, s>>>(g);
+    perm_scan_kernel<<<1, 1024, 0, s>>>(g);
     perm_scatter_kernel<<<grid, 256, 0, s>>>(g);
 }
 

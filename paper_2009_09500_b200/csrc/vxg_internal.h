@@ -61,11 +61,12 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     long long ntx, nty, ntz, ntiles;  // tiles per axis of the box [0,V)^2 x [z_lo,z_hi)
     long long* tile_cnt;              // ntiles * classes (zeroed): pieces per bin, then cursor
     long long* tile_off;              // ntiles * classes + 1: exclusive prefix
+    unsigned* tile_cur;               // ntiles * classes: scatter cursors (pieces < 2^32)
     uint4* pieces;                    // {segment, ka, len | hasE << 31, 0} binned by tile
     unsigned long long* words;        // the slab's bitmap (OR-ed into)
     Control* ctl;                     // total: in-volume samples, n_entries: pieces
     int* perm;                        // walk order (segments grouped by length) or null
-    long long* perm_cur;              // 64: bucket counts / cursors, bucket starts (zeroed)
+    long long* perm_cur;              // tile_perm_keys(): bucket counts, then cursors (zeroed)
 };
 
 struct ClipArgs {
@@ -107,6 +108,7 @@ cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
 void launch_clip(const ClipArgs& a, cudaStream_t s);
 int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz);  // -> smem bytes
 int tile_len_classes();  // piece bins per tile (length classes)
+int tile_perm_keys();    // walk-order buckets (length x coarse cell)
 void launch_tiles_perm(const TileArgs& g, cudaStream_t s);  // length-grouped walk order
 void launch_tiles_count(const TileArgs& g, cudaStream_t s);
 void launch_tiles_scan(const TileArgs& g, cudaStream_t s);
