@@ -323,6 +323,10 @@ def main():
         alg_bytes = 8 * ((V * V * (z_hi - z_lo) + 63) // 64) + 48 * n
         dominant = "tiles_fill_kernel"
     achieved = alg_bytes / (emit_avg / 1e3) / 1e9
+    # FP64-pipe view: every sample costs 10 FP64 operations (3 DMUL + 3 DADD for S + W*k, 3 DADD
+    # for llround, 1 DADD for k); peak = DADD/DMUL issue measured on this pool's B200s
+    # (tools/microbench_fp64.cu: 63.4 op/clk/SM, 18.42 TOP/s at 1965 MHz; profiles/)
+    samples = float(units) if kind in ("bitmap", "slab") else None
     traffic, traffic_src = load_traffic(args.workload)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
@@ -330,6 +334,10 @@ def main():
                 "aux_kernels_ms": statistics.mean(aux_ms),
                 "algorithmic_bytes": alg_bytes, "peak_source": peak_src,
                 "step_share": emit_avg / ms}
+    if samples is not None:  # bitmaps: the FP64 evaluation, not HBM, bounds the fill kernel
+        fp64 = 10.0 * samples / (emit_avg / 1e3) / 1e12
+        roofline["fp64"] = {"achieved": fp64, "peak": 18.42, "unit": "TOP/s", "frac": fp64 / 18.42,
+                            "source": "profiles/r1_microbench_fp64.txt (measured DADD/DMUL rate)"}
 
     # ---- end to end through the public host API (pinned host buffers, copies inside the timer)
     e2e = None
