@@ -136,9 +136,11 @@ VXG_API vxg_status vxg_batch_item_count(const vxg_batch* b, int64_t* live, int64
  * OUT_OF_RANGE outside [0,N_P) x [0,N_max]. Evaluated on the GPU. */
 VXG_API vxg_status vxg_batch_work_item(vxg_batch* b, int64_t i, int64_t k, int32_t out[3],
                                        int* live);
-/* Kernel + assemble phases of batch_voxelize (src/batch.cpp:107-150) as ONE GPU pass:
- * thread-per-sample emit, in-kernel consecutive-duplicate removal, single-pass look-back
- * compaction. Chain i is out[chain_off[i] .. chain_off[i+1]); *total = BatchResult.total_voxels.
+/* Kernel + assemble phases of batch_voxelize (src/batch.cpp:107-150) on the GPU: every sample of
+ * the flat (segment, k) space is evaluated by a warp row of 32, consecutive duplicates are dropped
+ * in registers, and the kept voxels are compacted into the list (a count task per range, a prefix,
+ * an emit task per range; fused into one kernel for large batches). Chain i is
+ * out[chain_off[i] .. chain_off[i+1]); *total = BatchResult.total_voxels.
  * `out` needs room for `total` voxels (capacity always suffices); chain_off has n+1 entries.
  * where == VXG_MEM_HOST: out/chain_off are host pointers (D2H included, synchronous).
  * where == VXG_MEM_DEVICE: device pointers; *total still returned (one 8-byte readback). */
@@ -147,8 +149,11 @@ VXG_API vxg_status vxg_batch_emit_list(vxg_batch* b, vxg_voxel* out, int64_t out
 /* Occupancy bitmap of the batch's samples restricted to planes [z_lo, z_hi) of a V^3 volume.
  * Samples outside [0,V)^3 are skipped and counted in *outside (may be NULL). `words` holds
  * V*V*(z_hi-z_lo)/64 uint64 (rounded up) and is OR-ed into (caller zeroes it).
- * clip != 0 clips every segment's k-range to the slab first (the z-slab partitioner), so the
- * work is proportional to the slab's samples; clip == 0 scans every sample. */
+ * V % 128 == 0 (and every N_i < 2^31): the tile-binned path -- segments are walked through
+ * 256x80x80-voxel tiles (clipped to the slab on the device, the z-slab partitioner), their
+ * in-tile k-ranges binned, every tile filled in shared memory and OR-ed into `words` once.
+ * Other volumes: one global atomic per sample; clip != 0 then clips every segment's k-range to
+ * the slab first (work proportional to the slab's samples), clip == 0 scans every sample. */
 VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t V, int64_t z_lo,
                                          int64_t z_hi, int clip, int64_t* outside, vxg_mem where);
 /* Samples of the batch whose rounded z lies in [z_lo, z_hi) (the slab's work). */
