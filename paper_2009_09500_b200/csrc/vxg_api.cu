@@ -286,8 +286,9 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
     const bool fused = mode_env ? std::strcmp(mode_env, "fused") == 0
                                 : b->capacity >= (int64_t)warps * 4 * 4 * blk;
     int64_t nranges = fused ? 4 * warps : warps;
-    const int64_t blocks = ceil_div(b->capacity, blk);
-    int64_t range_len = ceil_div(blocks, nranges) * blk;
+    const int64_t rblk = fused ? vxg::list_fused_block_samples() : blk;
+    const int64_t blocks = ceil_div(b->capacity, rblk);
+    int64_t range_len = ceil_div(blocks, nranges) * rblk;
     nranges = ceil_div(b->capacity, range_len);
     if (!b->ranges.ensure(ctx, sizeof(long long) * (size_t)(4 * nranges + 1)))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");

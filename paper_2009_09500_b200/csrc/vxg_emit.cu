@@ -730,17 +730,20 @@ cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s) {
 }
 
 // Fused launch: persistent CTAs (as many as fit), ranges = a.nranges (finer than one per warp).
+constexpr int kFusedIPT = 24;  // 768-sample blocks (16 lost to spills and block overhead: measured)
+int list_fused_block_samples() { return 32 * kFusedIPT; }
+
 cudaError_t launch_list_fused(const ListArgs& a, int num_sms, cudaStream_t s) {
-    const size_t smem = (size_t)kListNW * (3 * 32 * kListIPT + 4) * 4;
+    const size_t smem = (size_t)kListNW * (3 * 32 * kFusedIPT + 4) * 4;
     static int per_sm = 0;
     if (!per_sm) {
-        cudaFuncSetAttribute(list_fused_kernel<kListNW, kListIPT>,
+        cudaFuncSetAttribute(list_fused_kernel<kListNW, kFusedIPT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, list_fused_kernel<kListNW, kListIPT>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, list_fused_kernel<kListNW, kFusedIPT>,
                                                       kListNW * 32, smem);
         if (per_sm < 1) per_sm = 1;
     }
-    list_fused_kernel<kListNW, kListIPT><<<(unsigned)(per_sm * num_sms), kListNW * 32, smem, s>>>(a);
+    list_fused_kernel<kListNW, kFusedIPT><<<(unsigned)(per_sm * num_sms), kListNW * 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 

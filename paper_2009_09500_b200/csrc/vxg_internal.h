@@ -104,6 +104,7 @@ cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s);  // count pass
 cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s);   // emit pass
 cudaError_t launch_list_fused(const ListArgs& a, int num_sms, cudaStream_t s);  // both, overlapped
 int list_resident_warps(int num_sms);
+int list_fused_block_samples();  // fused kernel's staged block
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);
 void launch_clip(const ClipArgs& a, cudaStream_t s);
 int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz);  // -> smem bytes
