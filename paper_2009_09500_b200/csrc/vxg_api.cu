@@ -280,12 +280,14 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
     vxg_context* ctx = b->ctx;
     const int64_t blk = vxg::list_block_samples();
     const int64_t warps = vxg::list_resident_warps(ctx->num_sms);
-    // Large batches: the fused kernel over 4 ranges per resident warp (count and emit tasks
+    // Large batches: the fused kernel over 32 ranges per resident warp (count and emit tasks
     // overlap); small ones: one range per warp, count pass + scan + emit pass.
     static const char* mode_env = std::getenv("VXG_LIST_MODE");
     const bool fused = mode_env ? std::strcmp(mode_env, "fused") == 0
                                 : b->capacity >= (int64_t)warps * 4 * 4 * blk;
-    int64_t nranges = fused ? 4 * warps : warps;
+    static const int rpw_env = std::getenv("VXG_FUSED_RPW") ? std::atoi(std::getenv("VXG_FUSED_RPW")) : 32;
+    static const double la_env = std::getenv("VXG_FUSED_LA") ? std::atof(std::getenv("VXG_FUSED_LA")) : 1.0;
+    int64_t nranges = fused ? rpw_env * warps : warps;
     const int64_t rblk = fused ? vxg::list_fused_block_samples() : blk;
     const int64_t blocks = ceil_div(b->capacity, rblk);
     int64_t range_len = ceil_div(blocks, nranges) * rblk;
@@ -301,7 +303,8 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
     long long* rc = b->ranges.as<long long>();
     vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->n, b->capacity, nranges,
                     range_len, rc, rc + 3 * nranges, d_out, out_cap, d_chain, ctl_slot(b, 1),
-                    fused ? b->status.as<unsigned long long>() : nullptr, warps};
+                    fused ? b->status.as<unsigned long long>() : nullptr,
+                    std::max<int64_t>(1, (int64_t)(la_env * (double)warps))};
     cudaError_t e;
     if (fused) {
         cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)nranges, ctx->stream);
