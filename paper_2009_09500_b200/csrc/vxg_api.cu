@@ -429,7 +429,8 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     cudaMemsetAsync(g.ctl, 0, sizeof(Control), ctx->stream);
     cudaMemsetAsync(g.tile_cnt, 0, sizeof(long long) * (size_t)nbins, ctx->stream);
     // walk order grouped by segment length (pays off when lengths vary: long batches only)
-    if (b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256) {
+    // (a thin z-slab -- one rank of many -- walks little of each segment: not worth the sort)
+    if (b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256 && 2 * (z_hi - z_lo) >= V) {
         const size_t keys = (size_t)vxg::tile_perm_keys();
         if (!b->ent_off.ensure(ctx, sizeof(int) * (size_t)b->n + keys * sizeof(long long)))
             return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
