@@ -282,7 +282,7 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
     const int64_t warps = vxg::list_resident_warps(ctx->num_sms);
     // Large batches: the fused kernel over 32 ranges per resident warp (count and emit tasks
     // overlap); small ones: one range per warp, count pass + scan + emit pass.
-    static const char* mode_env = std::getenv("VXG_LIST_MODE");
+    const char* mode_env = std::getenv("VXG_LIST_MODE");  // (read per call: tests toggle it)
     const bool fused = mode_env ? std::strcmp(mode_env, "fused") == 0
                                 : b->capacity >= (int64_t)warps * 4 * 4 * blk;
     static const int rpw_env = std::getenv("VXG_FUSED_RPW") ? std::atoi(std::getenv("VXG_FUSED_RPW")) : 32;

@@ -302,6 +302,27 @@ def test_bitmap_tiles_accumulate_and_match_atomic_path(vx, oracle, monkeypatch):
     assert np.array_equal(w_atomic, w_tiles)
 
 
+@pytest.mark.parametrize("mode", ["fused", "twopass"])
+def test_list_modes_match_oracle(vx, oracle, monkeypatch, mode):
+    """Both list implementations -- the fused count/emit-task kernel (default for large batches)
+    and the count pass + scan + emit pass -- on the same corpora, bit-exact against the oracle:
+    arbitrary lengths (ranges cut segments everywhere), 1-sample segments, negative coordinates."""
+    monkeypatch.setenv("VXG_LIST_MODE", mode)
+    rng = np.random.default_rng(99)
+    corpora = [
+        vx.gen_segments(30000, 0, 2048, 4096, 123),
+        np.concatenate([rng.uniform(-30, 30, size=(20000, 6)),
+                        np.repeat(rng.uniform(0, 9, size=(5000, 3)), 2, axis=1).reshape(-1, 6)]),
+        vx.gen_segments(50000, 37, 0, 0, 5),
+    ]
+    for segs in corpora:
+        vox, off, total = vx.run_batch_flat(segs)
+        ovox, ooff, ototal = oracle.run_batch(segs)
+        assert total == ototal
+        assert np.array_equal(off, ooff)
+        assert np.array_equal(vox, ovox)
+
+
 # ------------------------------------------------------------------ device-resident (torch)
 def test_torch_device_buffers(vx, oracle):
     import torch
