@@ -315,38 +315,6 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
     return running;
 }
 
-// Copy a warp's staged records (words [0, 3*cnt) of `stage`) to global bytes [g0, g0 + 12*cnt):
-// 16-B vector stores for the aligned middle, single words for head and tail.
-__device__ __forceinline__ void store_records(const uint32_t* stage, int cnt, char* g0p) {
-    const int lane = threadIdx.x & 31;
-    const uintptr_t g0 = reinterpret_cast<uintptr_t>(g0p);
-    const uintptr_t g1 = g0 + 12ull * (unsigned)cnt;
-    const uintptr_t a0 = (g0 + 15) & ~(uintptr_t)15;
-    const uintptr_t a1 = g1 & ~(uintptr_t)15;
-    if (a1 > a0) {
-        const int hw = (int)((a0 - g0) >> 2);  // head words (0..3); stage word of a0 == hw
-        const int nv = (int)((a1 - a0) >> 4);
-        uint4* dst = reinterpret_cast<uint4*>(a0);
-        for (int v = lane; v < nv; v += 32) {
-            const uint32_t* src = stage + hw + 4 * v;
-            uint4 q;
-            q.x = src[0];
-            q.y = src[1];
-            q.z = src[2];
-            q.w = src[3];
-            st_stream_v4(dst + v, q);
-        }
-        const int tw = (int)((g1 - a1) >> 2);
-        if (lane < hw)
-            reinterpret_cast<uint32_t*>(g0)[lane] = stage[lane];
-        else if (lane >= 4 && lane - 4 < tw)
-            reinterpret_cast<uint32_t*>(a1)[lane - 4] = stage[hw + 4 * nv + (lane - 4)];
-    } else {
-        const int nw = (int)((g1 - g0) >> 2);  // fewer than 8 words
-        if (lane < nw) reinterpret_cast<uint32_t*>(g0)[lane] = stage[lane];
-    }
-}
-
 // Pass 1: kept voxels of every warp range, counted by kCountSplit warps per range (the count
 // pass needs no shared memory, so it can run more warps than the emit pass has ranges).
 constexpr int kCountSplit = 2;
