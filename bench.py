@@ -406,8 +406,6 @@ def run_e2e(vx, ctx, torch, d_segs, cfg, kind, n, capacity, units, z_lo, z_hi, w
     torch.cuda.empty_cache()
     times = []
     for it in range(steps + 1):
-        if kind not in ("list", "single"):
-            words_h[:] = 0
         barrier(world)
         t0 = time.perf_counter()
         b = vx.Batch(segs_h, ctx=ctx)
@@ -415,7 +413,7 @@ def run_e2e(vx, ctx, torch, d_segs, cfg, kind, n, capacity, units, z_lo, z_hi, w
             _, _, total = b.emit_list(out=out_h, chain_off=chain_h)
             assert total == units
         else:
-            b.emit_bitmap(V, z_lo, z_hi, clip=(kind == "slab"), words=words_h)
+            b.emit_bitmap(V, z_lo, z_hi, clip=(kind == "slab"), words=words_h, overwrite=True)
         b.close()
         dt = time.perf_counter() - t0
         if it > 0:

@@ -152,10 +152,15 @@ VXG_API vxg_status vxg_batch_emit_list(vxg_batch* b, vxg_voxel* out, int64_t out
  * V % 128 == 0 (and every N_i < 2^31): the tile-binned path -- segments are walked through
  * 256x80x80-voxel tiles (clipped to the slab on the device, the z-slab partitioner), their
  * in-tile k-ranges binned, every tile filled in shared memory and OR-ed into `words` once.
- * Other volumes: one global atomic per sample; clip != 0 then clips every segment's k-range to
- * the slab first (work proportional to the slab's samples), clip == 0 scans every sample. */
+ * Other volumes: one global atomic per sample; VXG_BITMAP_CLIP then clips every segment's
+ * k-range to the slab first (work proportional to the slab's samples), without it every sample
+ * is scanned. `flags` is a bit set of VXG_BITMAP_*; VXG_BITMAP_OVERWRITE zeroes `words` on the
+ * device first instead of OR-ing into them (with VXG_MEM_HOST it also skips uploading the
+ * caller's words: the host->device traffic is the segments only). */
+#define VXG_BITMAP_CLIP 1
+#define VXG_BITMAP_OVERWRITE 2
 VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t V, int64_t z_lo,
-                                         int64_t z_hi, int clip, int64_t* outside, vxg_mem where);
+                                         int64_t z_hi, int flags, int64_t* outside, vxg_mem where);
 /* Samples of the batch whose rounded z lies in [z_lo, z_hi) (the slab's work). */
 VXG_API vxg_status vxg_batch_slab_samples(vxg_batch* b, int64_t z_lo, int64_t z_hi,
                                           int64_t* samples);

@@ -141,6 +141,13 @@ def chain_length_bounds(start, end):
 
 
 # ----------------------------------------------------------------------------- batch engine
+BITMAP_CLIP, BITMAP_OVERWRITE = 1, 2  # include/voxgpu.h VXG_BITMAP_*
+
+
+def _bitmap_flags(clip: bool, overwrite: bool) -> int:
+    return (BITMAP_CLIP if clip else 0) | (BITMAP_OVERWRITE if overwrite else 0)
+
+
 class Batch:
     """A device-resident batch (vxg_batch): segments + plan kept in HBM between calls."""
 
@@ -188,22 +195,28 @@ class Batch:
         return total.value
 
     def emit_bitmap(self, V: int, z_lo: int = 0, z_hi: int | None = None, clip: bool = False,
-                    words: np.ndarray | None = None):
+                    words: np.ndarray | None = None, overwrite: bool | None = None):
+        """Bitmap of planes [z_lo, z_hi) into `words` (host). The words are OR-ed into unless
+        `overwrite` (default: True when `words` is None, so a fresh bitmap is zeroed on the
+        device and nothing but the segments crosses PCIe host->device)."""
         z_hi = V if z_hi is None else z_hi
         nwords = (V * V * (z_hi - z_lo) + 63) // 64
+        if overwrite is None:
+            overwrite = words is None
         if words is None:
-            words = np.zeros(max(nwords, 1), np.uint64)
+            words = np.empty(max(nwords, 1), np.uint64)
         outside = C.c_int64()
         self.ctx.check(self.ctx.lib.vxg_batch_emit_bitmap(self.h, _ptr(words), V, z_lo, z_hi,
-                                                          int(clip), C.byref(outside), MEM_HOST))
+                                                          _bitmap_flags(clip, overwrite),
+                                                          C.byref(outside), MEM_HOST))
         return words[:nwords], outside.value
 
     def emit_bitmap_device(self, words_ptr: int, V: int, z_lo: int, z_hi: int,
-                           clip: bool) -> int:
+                           clip: bool, overwrite: bool = False) -> int:
         outside = C.c_int64()
         self.ctx.check(self.ctx.lib.vxg_batch_emit_bitmap(self.h, words_ptr, V, z_lo, z_hi,
-                                                          int(clip), C.byref(outside),
-                                                          MEM_DEVICE))
+                                                          _bitmap_flags(clip, overwrite),
+                                                          C.byref(outside), MEM_DEVICE))
         return outside.value
 
     def slab_samples(self, z_lo: int, z_hi: int) -> int:

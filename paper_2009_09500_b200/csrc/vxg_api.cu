@@ -849,8 +849,10 @@ VXG_API vxg_status vxg_batch_emit_list(vxg_batch* b, vxg_voxel* out, int64_t out
 }
 
 VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t V, int64_t z_lo,
-                                         int64_t z_hi, int clip, int64_t* outside, vxg_mem where) {
-    if (!b || !words) return VXG_INVALID_ARGUMENT;
+                                         int64_t z_hi, int flags, int64_t* outside, vxg_mem where) {
+    if (!b || !words || (flags & ~(VXG_BITMAP_CLIP | VXG_BITMAP_OVERWRITE))) return VXG_INVALID_ARGUMENT;
+    const int clip = flags & VXG_BITMAP_CLIP;
+    const bool overwrite = (flags & VXG_BITMAP_OVERWRITE) != 0;
     vxg_context* ctx = b->ctx;
     ctx->ok();
     if (V <= 0 || V > (1ll << 21) || z_lo < 0 || z_hi > V || z_lo > z_hi)
@@ -861,6 +863,7 @@ VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t 
     const size_t nwords = (size_t)((V * V * (z_hi - z_lo) + 63) / 64);
     const auto t0 = Clock::now();
     if (where == VXG_MEM_DEVICE) {
+        if (overwrite) cudaMemsetAsync(words, 0, 8 * nwords, ctx->stream);
         const vxg_status s = emit_bitmap_device(b, reinterpret_cast<unsigned long long*>(words), V,
                                                 z_lo, z_hi, clip, outside);
         b->timing.kernel_ns = ns_since(t0);
@@ -869,7 +872,10 @@ VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t 
     DBuf d;
     if (!d.ensure(ctx, 8 * std::max<size_t>(nwords, 1)))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
-    cudaMemcpyAsync(d.p, words, 8 * nwords, cudaMemcpyHostToDevice, ctx->stream);
+    if (overwrite)
+        cudaMemsetAsync(d.p, 0, 8 * nwords, ctx->stream);
+    else
+        cudaMemcpyAsync(d.p, words, 8 * nwords, cudaMemcpyHostToDevice, ctx->stream);
     vxg_status s = emit_bitmap_device(b, d.as<unsigned long long>(), V, z_lo, z_hi, clip, outside);
     b->timing.kernel_ns = ns_since(t0);
     if (s) return s;

@@ -302,6 +302,27 @@ def test_bitmap_tiles_accumulate_and_match_atomic_path(vx, oracle, monkeypatch):
     assert np.array_equal(w_atomic, w_tiles)
 
 
+def test_bitmap_overwrite_discards_prior_words(vx, oracle):
+    """VXG_BITMAP_OVERWRITE zeroes the words on the device: garbage in the caller's buffer
+    (host or device) does not survive, on the tile path and on a slab."""
+    import torch
+    segs = vx.gen_segments(2000, 0, 300, 512, 23)
+    b = vx.Batch(segs)
+    junk = np.full(512 ** 3 // 64, np.uint64(0xFFFF0000FFFF0000), np.uint64)
+    w_host, _ = b.emit_bitmap(512, 0, 512, words=junk, overwrite=True)
+    ow, _ = oracle.bitmap(segs, 512)
+    assert np.array_equal(w_host, ow)
+    w_fresh, _ = b.emit_bitmap(512, 128, 384, clip=True)  # words=None: overwrite by default
+    ow, _ = oracle.bitmap(segs, 512, 128, 384)
+    assert np.array_equal(w_fresh, ow)
+    d = torch.full((512 ** 3 // 64,), -1, dtype=torch.int64, device="cuda")
+    b.emit_bitmap_device(d.data_ptr(), 512, 0, 512, clip=False, overwrite=True)
+    torch.cuda.synchronize()
+    ow, _ = oracle.bitmap(segs, 512)
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), ow)
+    b.close()
+
+
 @pytest.mark.parametrize("mode", ["fused", "twopass"])
 def test_list_modes_match_oracle(vx, oracle, monkeypatch, mode):
     """Both list implementations -- the fused count/emit-task kernel (default for large batches)
