@@ -113,6 +113,13 @@ def test_cli_usage_and_input_errors(tmp_path):
     empty = _write(tmp_path, "empty.csv", "# nothing\n\n")
     r = run("batch", "--input", empty, "--out", str(tmp_path / "o"))
     assert r.returncode == 2 and "no segments" in r.stderr
+    # bench (tools/voxline_cli.cpp:143-156, tests/test_cli.cpp:227-233): bad scenario -> 2
+    r = run("bench", "--scenario", "nope")
+    assert r.returncode == 2 and "unknown scenario" in r.stderr
+    assert run("bench").returncode == 2                                    # --scenario required
+    assert run("bench", "--scenario", "single", "--reps", "0").returncode == 2
+    assert run("bench", "--scenario", "single", "--scale", "-1").returncode == 2
+    assert run("bench", "--scenario", "single", "--warmup", "-1").returncode == 2
 
 
 def test_cli_no_gpu_fails_loudly(tmp_path):
@@ -161,3 +168,71 @@ def test_cli_voxelize(tmp_path, oracle):
     chain = np.frombuffer(data[16:], dtype=np.int32).reshape(n, 3)
     assert np.array_equal(chain, oracle.voxelize_parametric([0.1, 0.3, 0.7, 12.45, 4.9, 0.2]))
     assert n == 14 and tuple(chain[12]) == (11, 5, 0)
+
+
+def _expected_bench(oracle, kind, scale, seed):
+    """Parameter points and total voxels of the reference's run_scenario (src/bench.cpp:148-203,
+    288-313) from the oracle: same sub-seeds, same generators, chain lengths from the oracle."""
+    sc = lambda v: max(1, int(np.floor(v * scale + 0.5)))  # noqa: E731  (llround, v*scale > 0)
+    sub = oracle.splitmix(seed, 4)
+    if kind == "single":
+        pts = [sc(1000), sc(10000), sc(100000), sc(1000000)]
+        sets = [oracle.gen_segment_of_length(p, sub[i])[None] for i, p in enumerate(pts)]
+    elif kind == "fixed-batch":
+        pts = [sc(20), sc(200), sc(2000), sc(20000)]
+        sets = [np.stack([oracle.gen_segment_of_length(p, s2) for s2 in oracle.splitmix(sub[i], 1024)])
+                for i, p in enumerate(pts)]
+    else:
+        pts = [max(1024, sc(10000000))]
+        sets = [oracle.gen_arbitrary_batch(pts[0], 1024, sub[0])]
+    return pts, [int(oracle.chain_lengths(s).sum()) for s in sets]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,scale", [("single", 0.01), ("fixed-batch", 0.05), ("arbitrary", 0.01)])
+def test_cli_bench_reports(tmp_path, oracle, kind, scale):
+    """`voxgpu bench`: the reference harness's scenarios (tests/test_cli.cpp:201-225 pins the
+    table, the CSV header and the JSON sections), same parameter points and workloads -- every
+    method's total_voxels equals the oracle's chain-length sum on the same generated segments."""
+    import json
+    csv, js = tmp_path / "r.csv", tmp_path / "r.json"
+    r = subprocess.run([CLI, "bench", "--scenario", kind, "--scale", str(scale), "--reps", "2",
+                        "--warmup", "1", "--seed", "7", "--workers", "3", "--report", str(csv),
+                        "--report-json", str(js)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.splitlines()[0].split() == ["scenario", "parameter", "method", "workers",
+                                                "group", "median_ms", "total_voxels", "MVps"]
+    rows = csv.read_text().splitlines()
+    assert rows[0] == "scenario,parameter,method,workers,group_size,median_ms,total_voxels,mvps"
+    recs = [x.split(",") for x in rows[1:]]
+    pts, totals = _expected_bench(oracle, kind, scale, 7)
+    assert len(recs) == 3 * len(pts)
+    for i, (p, t) in enumerate(zip(pts, totals)):
+        trio = recs[3 * i: 3 * i + 3]
+        assert [x[2] for x in trio] == ["sequential", "batch", "batch-device"]
+        for x in trio:
+            assert x[0] == kind and int(x[1]) == p and int(x[6]) == t, (x, p, t)
+            assert float(x[5]) > 0 and abs(float(x[7]) - t / float(x[5]) / 1e3) <= 1e-6 * float(x[7])
+        assert trio[0][3] == "1" and trio[1][3] == "3" and trio[1][4] == "64"
+    ref_bench = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    if os.path.exists(ref_bench):  # the reference's own harness (src/bench.cpp) on the host
+        rr = tmp_path / "ref.csv"
+        q = subprocess.run([ref_bench, kind, "--scale", str(scale), "--reps", "1", "--warmup", "0",
+                            "--seed", "7", "--workers", "3", "--report", str(rr)],
+                           capture_output=True, text=True, timeout=600)
+        assert q.returncode == 0, q.stderr
+        theirs = [x.split(",") for x in rr.read_text().splitlines()[1:]]
+        assert [(x[0], x[1], x[6]) for x in theirs] == \
+            [(x[0], x[1], x[6]) for x in recs if x[2] != "batch-device"]
+    doc = json.loads(js.read_text())
+    assert doc["metadata"]["scenario"] == kind and doc["metadata"]["seed"] == 7
+    assert ("length_distribution" in doc["metadata"]) == (kind == "arbitrary")
+    assert [d["total_voxels"] for d in doc["records"]] == [int(x[6]) for x in recs]
+
+
+@pytest.mark.gpu
+def test_cli_bench_bad_report_path():
+    r = subprocess.run([CLI, "bench", "--scenario", "single", "--scale", "0.001", "--reps", "1",
+                        "--warmup", "0", "--report", "/nonexistent-dir/r.csv"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 3 and "cannot open report file" in r.stderr
