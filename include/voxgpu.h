@@ -116,7 +116,11 @@ VXG_API vxg_status vxg_chain_length_bounds(vxg_context* ctx, const vxg_segment* 
 /* ---------------------------------------------------------------- batch engine */
 /* batch_preprocess (src/batch.cpp:57-73): upload n segments (host or device pointer) and build
  * the plan on the GPU (plan kernel + decoupled look-back offset scan). Empty -> INVALID_ARGUMENT;
- * bad endpoint -> RANGE_ERROR (lowest segment index reported). */
+ * bad endpoint -> RANGE_ERROR (lowest segment index reported).
+ * VXG_MEM_HOST: synchronous; plan errors are returned here. VXG_MEM_DEVICE: only enqueued -- the
+ * plan's N_max / capacity and any plan error are read back by the first call that needs them
+ * (vxg_batch_info, or the single readback of a device-pointer vxg_batch_emit_list on a batch of
+ * fewer than 2^18 segments), which then returns the plan's error; every later call repeats it. */
 VXG_API vxg_status vxg_batch_create(vxg_context* ctx, const vxg_segment* segs, int64_t n,
                                     vxg_mem where, vxg_batch** out);
 /* A batch from a caller-supplied plan (batch_voxelize takes `const BatchPlan&`,

@@ -164,10 +164,27 @@ class Batch:
                                                a.shape[0], MEM_HOST, C.byref(h))
         self.ctx.check(st)
         self.h = h
-        n_, mx, cap = C.c_int64(), C.c_int64(), C.c_int64()
-        self.ctx.check(self.ctx.lib.vxg_batch_info(h, C.byref(n_), C.byref(mx), C.byref(cap)))
-        self.n, self.max_steps, self.capacity = n_.value, mx.value, cap.value
+        self.n = int(n) if device_ptr is not None else int(self._keep.shape[0])
+        self._info = None  # (max_steps, capacity): read back on first use (vxg_batch_info)
         self._plans = None
+
+    def resolve(self):
+        """Read the plan's N_max / capacity back (raises the plan's error, if any). A device-
+        resident batch defers this; emit_list_device resolves it in its own readback."""
+        if self._info is None:
+            n_, mx, cap = C.c_int64(), C.c_int64(), C.c_int64()
+            self.ctx.check(self.ctx.lib.vxg_batch_info(self.h, C.byref(n_), C.byref(mx),
+                                                       C.byref(cap)))
+            self._info = (mx.value, cap.value)
+        return self._info
+
+    @property
+    def max_steps(self) -> int:
+        return self.resolve()[0]
+
+    @property
+    def capacity(self) -> int:
+        return self.resolve()[1]
 
     def plans(self) -> np.ndarray:
         if self._plans is None:
@@ -288,6 +305,7 @@ def batch_preprocess(segments) -> BatchPlan:
     import time
     t0 = time.perf_counter_ns()
     b = Batch(segments)
+    b.resolve()
     return BatchPlan(b, time.perf_counter_ns() - t0)
 
 

@@ -100,7 +100,7 @@ struct vxg_context {
     int64_t launches = 0;
     int num_sms = 148;
     DeviceCache cache;
-    Control* h_ctl = nullptr;  // pinned readback slot
+    Control* h_ctl = nullptr;  // pinned readback slots (2)
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
     vxg_status fail(vxg_status s, int64_t seg, const char* fmt, ...) {
@@ -155,8 +155,20 @@ struct vxg_batch {
     const double* d_segs = nullptr;  // owned (segs) or borrowed device pointer
     DBuf segs, rec, steps, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl, ranges;
     int64_t max_steps = 0, capacity = 0;
+    // The plan's scalars (N_max, capacity) and errors are read back lazily: batch_create only
+    // enqueues the plan kernel; the first call that needs them (or the emit's own readback for a
+    // small list batch) resolves the plan, so a small batch costs one host round trip, not two.
+    bool plan_pending = false;
+    vxg_status plan_status = VXG_OK;  // a resolved plan's error, re-reported by every later call
+    std::string plan_err;
+    int64_t plan_err_seg = -1;
+    cudaEvent_t pev[2] = {nullptr, nullptr};  // plan kernel start / end (this batch's own)
     float plan_ms = 0.f, emit_ms = 0.f, aux_ms = 0.f;  // plan kernel / emit kernel / tile index + clip
     vxg_timing timing{0, 0, 0};
+    ~vxg_batch() {
+        for (cudaEvent_t e : pev)
+            if (e) cudaEventDestroy(e);
+    }
 };
 
 namespace {
@@ -169,6 +181,8 @@ vxg_status check_launch(vxg_context* ctx, const char* where) {
     return VXG_OK;
 }
 
+vxg_status ctl_status(vxg_context* ctx, const Control& out, const char* phase);
+
 // Read back a Control block (synchronises the stream) and convert a recorded error.
 vxg_status read_ctl(vxg_context* ctx, Control* d_ctl, Control& out, const char* phase) {
     cudaError_t e = cudaMemcpyAsync(ctx->h_ctl, d_ctl, sizeof(Control), cudaMemcpyDeviceToHost,
@@ -176,6 +190,10 @@ vxg_status read_ctl(vxg_context* ctx, Control* d_ctl, Control& out, const char* 
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, phase);
     out = *ctx->h_ctl;
+    return ctl_status(ctx, out, phase);
+}
+
+vxg_status ctl_status(vxg_context* ctx, const Control& out, const char* phase) {
     if (out.abort)
         return ctx->fail(VXG_LOGIC_ERROR, -1, "%s: look-back watchdog fired (internal error)", phase);
     if (out.err_seg != 0) {
@@ -244,26 +262,56 @@ vxg_status run_plan(vxg_batch* b) {
     cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)tiles, ctx->stream);
     vxg::PlanArgs a{b->d_segs, n, b->rec.as<SegRec>(), b->steps.as<long long>(),
                     b->off.as<long long>(), b->status.as<unsigned long long>(), ctl_slot(b, 0)};
-    cudaEventRecord(ctx->ev[0], ctx->stream);
+    cudaEventRecord(b->pev[0], ctx->stream);
     vxg::launch_plan(a, ctx->stream);
     ctx->launches++;
-    cudaEventRecord(ctx->ev[1], ctx->stream);
-    vxg_status s = check_launch(ctx, "plan_kernel");
-    if (s) return s;
-    Control c;
-    s = read_ctl(ctx, ctl_slot(b, 0), c, "batch_preprocess");
-    cudaEventElapsedTime(&b->plan_ms, ctx->ev[0], ctx->ev[1]);
-    if (s) return s;
+    cudaEventRecord(b->pev[1], ctx->stream);
+    b->plan_pending = true;
+    return check_launch(ctx, "plan_kernel");
+}
+
+// The plan's readback (slot 0) once it is on the host: N_max, capacity, plan errors.
+vxg_status plan_resolved(vxg_batch* b, const Control& c) {
+    b->plan_pending = false;
+    cudaEventElapsedTime(&b->plan_ms, b->pev[0], b->pev[1]);
+    const vxg_status s = ctl_status(b->ctx, c, "batch_preprocess");
+    if (s) {
+        b->plan_status = s;
+        b->plan_err = b->ctx->err;
+        b->plan_err_seg = b->ctx->err_seg;
+        return s;
+    }
     b->max_steps = (int64_t)c.max_steps;
     b->capacity = c.total;
     return VXG_OK;
+}
+
+// Resolve a pending plan (one readback). Every entry point that needs N_max / capacity calls it.
+vxg_status plan_ready(vxg_batch* b) {
+    vxg_context* ctx = b->ctx;
+    if (!b->plan_pending) {
+        if (b->plan_status) {
+            ctx->err = b->plan_err;
+            ctx->err_seg = b->plan_err_seg;
+        }
+        return b->plan_status;
+    }
+    cudaError_t e = cudaMemcpyAsync(ctx->h_ctl, ctl_slot(b, 0), sizeof(Control),
+                                    cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        b->plan_pending = false;
+        return ctx->cuda_fail(e, "batch_preprocess");
+    }
+    return plan_resolved(b, ctx->h_ctl[0]);
 }
 
 vxg_status new_batch(vxg_context* ctx, vxg_batch** out) {
     vxg_batch* b = new (std::nothrow) vxg_batch();
     if (!b) return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch: out of host memory");
     b->ctx = ctx;
-    if (!b->ctl.ensure(ctx, sizeof(Control) * kMaxCtlSlots)) {
+    if (!b->ctl.ensure(ctx, sizeof(Control) * kMaxCtlSlots) ||
+        cudaEventCreate(&b->pev[0]) != cudaSuccess || cudaEventCreate(&b->pev[1]) != cudaSuccess) {
         delete b;
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch: out of device memory");
     }
@@ -273,6 +321,9 @@ vxg_status new_batch(vxg_context* ctx, vxg_batch** out) {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Batches below this many segments may emit a list before their plan is read back.
+constexpr int64_t kDeferredMaxSegments = 1 << 18;
+
 // Emit the voxel list into device buffers (out: >= out_cap voxels, chain: n+1): count pass, range
 // scan, emit pass.
 vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long long* d_chain,
@@ -280,18 +331,30 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
     vxg_context* ctx = b->ctx;
     const int64_t blk = vxg::list_block_samples();
     const int64_t warps = vxg::list_resident_warps(ctx->num_sms);
+    const char* mode_env = std::getenv("VXG_LIST_MODE");  // (read per call: tests toggle it)
+    // A small batch whose plan is still pending goes straight to the count pass: the kernels
+    // derive the range geometry from the capacity the plan kernel left in off[n], and the plan's
+    // and the emit's control blocks come back in ONE readback.
+    const bool deferred = b->plan_pending && b->n < kDeferredMaxSegments &&
+                          !(mode_env && std::strcmp(mode_env, "fused") == 0);
+    if (!deferred) {
+        const vxg_status s = plan_ready(b);
+        if (s) return s;
+    }
     // Large batches: the fused kernel over 32 ranges per resident warp (count and emit tasks
     // overlap); small ones: one range per warp, count pass + scan + emit pass.
-    const char* mode_env = std::getenv("VXG_LIST_MODE");  // (read per call: tests toggle it)
-    const bool fused = mode_env ? std::strcmp(mode_env, "fused") == 0
-                                : b->capacity >= (int64_t)warps * 4 * 4 * blk;
+    const bool fused = !deferred && (mode_env ? std::strcmp(mode_env, "fused") == 0
+                                              : b->capacity >= (int64_t)warps * 4 * 4 * blk);
     static const int rpw_env = std::getenv("VXG_FUSED_RPW") ? std::atoi(std::getenv("VXG_FUSED_RPW")) : 32;
     static const double la_env = std::getenv("VXG_FUSED_LA") ? std::atof(std::getenv("VXG_FUSED_LA")) : 1.0;
     int64_t nranges = fused ? rpw_env * warps : warps;
     const int64_t rblk = fused ? vxg::list_fused_block_samples() : blk;
-    const int64_t blocks = ceil_div(b->capacity, rblk);
-    int64_t range_len = ceil_div(blocks, nranges) * rblk;
-    nranges = ceil_div(b->capacity, range_len);
+    int64_t range_len = rblk;  // deferred: the kernels scale it by the capacity they read
+    if (!deferred) {
+        const int64_t blocks = ceil_div(b->capacity, rblk);
+        range_len = ceil_div(blocks, nranges) * rblk;
+        nranges = ceil_div(b->capacity, range_len);
+    }
     if (!b->ranges.ensure(ctx, sizeof(long long) * (size_t)(4 * nranges + 1)))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
     if (fused && !b->status.ensure(ctx, sizeof(unsigned long long) *
@@ -301,10 +364,12 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
         return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_voxelize: output must be 4-byte aligned");
     cudaMemsetAsync(ctl_slot(b, 1), 0, sizeof(Control), ctx->stream);
     long long* rc = b->ranges.as<long long>();
-    vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->n, b->capacity, nranges,
+    vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->n,
+                    deferred ? -1 : b->capacity, nranges,
                     range_len, rc, rc + 3 * nranges, d_out, out_cap, d_chain, ctl_slot(b, 1),
                     fused ? b->status.as<unsigned long long>() : nullptr,
-                    std::max<int64_t>(1, (int64_t)(la_env * (double)warps))};
+                    std::max<int64_t>(1, (int64_t)(la_env * (double)warps)),
+                    deferred ? ctl_slot(b, 0) : nullptr};
     cudaError_t e;
     if (fused) {
         cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)nranges, ctx->stream);
@@ -322,7 +387,21 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
     cudaEventRecord(ctx->ev[4], ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "list emit");
     Control c;
-    vxg_status s = read_ctl(ctx, ctl_slot(b, 1), c, "batch_voxelize");
+    vxg_status s;
+    if (deferred) {  // slots 0 (plan) and 1 (emit) in one readback
+        e = cudaMemcpyAsync(ctx->h_ctl, ctl_slot(b, 0), 2 * sizeof(Control), cudaMemcpyDeviceToHost,
+                            ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) {
+            b->plan_pending = false;
+            return ctx->cuda_fail(e, "batch_voxelize");
+        }
+        c = ctx->h_ctl[1];
+        s = plan_resolved(b, ctx->h_ctl[0]);
+        if (!s) s = ctl_status(ctx, c, "batch_voxelize");
+    } else {
+        s = read_ctl(ctx, ctl_slot(b, 1), c, "batch_voxelize");
+    }
     cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);   // count pass + range scan
     cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);  // emit pass (fused: both)
     if (s) return s;
@@ -501,7 +580,7 @@ VXG_API vxg_status vxg_create(int device, vxg_context** out) {
     if (!ctx) return VXG_OUT_OF_MEMORY;
     ctx->device = device;
     if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ctl), sizeof(Control), cudaHostAllocDefault) !=
+        cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_ctl), 2 * sizeof(Control), cudaHostAllocDefault) !=
             cudaSuccess ||
         cudaEventCreate(&ctx->ev[0]) != cudaSuccess || cudaEventCreate(&ctx->ev[1]) != cudaSuccess ||
         cudaEventCreate(&ctx->ev[2]) != cudaSuccess || cudaEventCreate(&ctx->ev[3]) != cudaSuccess ||
@@ -627,7 +706,11 @@ VXG_API vxg_status vxg_voxelize_parametric(vxg_context* ctx, const vxg_segment* 
     if (!ctx || !seg || !count || cap < 0 || (cap > 0 && !out)) return VXG_INVALID_ARGUMENT;
     vxg_batch* b = nullptr;
     vxg_status s = vxg_batch_create(ctx, seg, 1, VXG_MEM_HOST, &b);
-    if (s) return s;
+    if (!s) s = plan_ready(b);
+    if (s) {
+        vxg_batch_destroy(b);
+        return s;
+    }
     if (!b->out.ensure(ctx, 12 * (size_t)b->capacity) || !b->chain.ensure(ctx, 16)) {
         vxg_batch_destroy(b);
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "voxelize_parametric: out of device memory");
@@ -685,6 +768,9 @@ VXG_API vxg_status vxg_batch_create(vxg_context* ctx, const vxg_segment* segs, i
     const auto t0 = Clock::now();
     s = upload_segments(b, segs, n, where);
     if (!s) s = run_plan(b);
+    // host segments: resolve now (the call is synchronous for host pointers, and plan errors
+    // surface here as batch_preprocess's do); device segments: lazily (see vxg_batch)
+    if (!s && where == VXG_MEM_HOST) s = plan_ready(b);
     b->timing.preprocess_ns = ns_since(t0);
     if (s) {
         delete b;
@@ -743,15 +829,19 @@ VXG_API vxg_status vxg_batch_from_plan(vxg_context* ctx, const vxg_segment* segs
     return VXG_OK;
 }
 
+// No synchronisation: the batch's buffers go back to the context cache, whose next user works
+// on the same stream (stream order keeps the reuse safe; vxg_set_stream synchronises).
 VXG_API void vxg_batch_destroy(vxg_batch* b) {
     if (!b) return;
-    cudaStreamSynchronize(b->ctx->stream);
     delete b;
 }
 
 VXG_API vxg_status vxg_batch_info(const vxg_batch* b, int64_t* n, int64_t* max_steps,
                                   int64_t* capacity) {
     if (!b) return VXG_INVALID_ARGUMENT;
+    b->ctx->ok();
+    const vxg_status s = plan_ready(const_cast<vxg_batch*>(b));
+    if (s) return s;
     if (n) *n = b->n;
     if (max_steps) *max_steps = b->max_steps;
     if (capacity) *capacity = b->capacity;
@@ -761,7 +851,9 @@ VXG_API vxg_status vxg_batch_info(const vxg_batch* b, int64_t* n, int64_t* max_s
 VXG_API vxg_status vxg_batch_plans(vxg_batch* b, vxg_segment_plan* out) {
     if (!b || !out) return VXG_INVALID_ARGUMENT;
     vxg_context* ctx = b->ctx;
+    ctx->ok();
     cudaSetDevice(ctx->device);
+    if (const vxg_status s = plan_ready(b)) return s;
     DBuf d;
     if (!d.ensure(ctx, sizeof(vxg_segment_plan) * (size_t)b->n))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "plans: out of device memory");
@@ -776,6 +868,8 @@ VXG_API vxg_status vxg_batch_plans(vxg_batch* b, vxg_segment_plan* out) {
 
 VXG_API vxg_status vxg_batch_item_count(const vxg_batch* b, int64_t* live, int64_t* redundant) {
     if (!b) return VXG_INVALID_ARGUMENT;
+    b->ctx->ok();
+    if (const vxg_status s = plan_ready(const_cast<vxg_batch*>(b))) return s;
     if (live) *live = b->capacity;
     if (redundant) *redundant = b->n * (b->max_steps + 1) - b->capacity;
     return VXG_OK;
@@ -786,6 +880,7 @@ VXG_API vxg_status vxg_batch_work_item(vxg_batch* b, int64_t i, int64_t k, int32
     if (!b || !out || !live) return VXG_INVALID_ARGUMENT;
     vxg_context* ctx = b->ctx;
     ctx->ok();
+    if (const vxg_status s = plan_ready(b)) return s;
     if (i < 0 || i >= b->n || k < 0 || k > b->max_steps)
         return ctx->fail(VXG_OUT_OF_RANGE, -1,
                          "kernel_work_item: item index outside the %lld x %lld grid",
@@ -822,13 +917,14 @@ VXG_API vxg_status vxg_batch_emit_list(vxg_batch* b, vxg_voxel* out, int64_t out
     cudaSetDevice(ctx->device);
     const auto t0 = Clock::now();
     vxg_status s;
-    if (where == VXG_MEM_DEVICE) {
+    if (where == VXG_MEM_DEVICE) {  // (a small batch's pending plan resolves in the emit's readback)
         s = emit_list_device(b, reinterpret_cast<int32_t*>(out), out_cap,
                              reinterpret_cast<long long*>(chain_off), total);
         b->timing.kernel_ns = ns_since(t0);
         b->timing.assemble_ns = 0;
         return s;
     }
+    if ((s = plan_ready(b))) return s;
     if (!b->out.ensure(ctx, 12 * (size_t)std::max<int64_t>(b->capacity, 1)) ||
         !b->chain.ensure(ctx, 8 * (size_t)(b->n + 1)))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
@@ -855,6 +951,7 @@ VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t 
     const bool overwrite = (flags & VXG_BITMAP_OVERWRITE) != 0;
     vxg_context* ctx = b->ctx;
     ctx->ok();
+    if (const vxg_status s = plan_ready(b)) return s;
     if (V <= 0 || V > (1ll << 21) || z_lo < 0 || z_hi > V || z_lo > z_hi)
         return ctx->fail(VXG_INVALID_ARGUMENT, -1, "bitmap: invalid volume / slab");
     if ((V * V * (z_hi - z_lo) + 63) / 64 >= 0xffffffffll)  // word indices are 32-bit keys in-kernel
@@ -891,12 +988,15 @@ VXG_API vxg_status vxg_batch_slab_samples(vxg_batch* b, int64_t z_lo, int64_t z_
     if (!b || !samples) return VXG_INVALID_ARGUMENT;
     b->ctx->ok();
     cudaSetDevice(b->ctx->device);
+    if (const vxg_status s = plan_ready(b)) return s;
     int64_t ne = 0;
     return run_clip(b, z_lo, z_hi, &ne, samples);
 }
 
 VXG_API vxg_status vxg_batch_timing(const vxg_batch* b, vxg_timing* t) {
     if (!b || !t) return VXG_INVALID_ARGUMENT;
+    b->ctx->ok();
+    if (const vxg_status s = plan_ready(const_cast<vxg_batch*>(b))) return s;
     t->preprocess_ns = (int64_t)((double)b->plan_ms * 1e6);
     t->kernel_ns = (int64_t)((double)b->emit_ms * 1e6);
     t->assemble_ns = (int64_t)((double)b->aux_ms * 1e6);

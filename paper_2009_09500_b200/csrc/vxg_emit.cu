@@ -319,14 +319,38 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
 // pass needs no shared memory, so it can run more warps than the emit pass has ranges).
 constexpr int kCountSplit = 2;
 
+// Two-pass geometry: host-given, or ("deferred", total_samples < 0) derived from the capacity the
+// plan kernel left in off[nseg] -- the same arithmetic the host uses (vxg_api.cu
+// emit_list_device). Returns false (nothing to do) if the plan recorded an error.
+__device__ __forceinline__ bool list_geometry(const ListArgs& a, long long& total,
+                                              long long& range_len) {
+    if (a.total_samples >= 0) {
+        total = a.total_samples;
+        range_len = a.range_len;
+        return true;
+    }
+    if (*reinterpret_cast<const volatile long long*>(&a.plan_ctl->err_seg) != 0 ||
+        *reinterpret_cast<const volatile int*>(&a.plan_ctl->abort) != 0)
+        return false;
+    total = __ldg(a.off + a.nseg);
+    const long long blocks = (total + a.range_len - 1) / a.range_len;
+    range_len = (blocks + a.nranges - 1) / a.nranges * a.range_len;
+    return range_len > 0;
+}
+
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 4) list_count_kernel(ListArgs a) {
     const int lane = threadIdx.x & 31;
     const long long q = (long long)blockIdx.x * NW + (threadIdx.x >> 5);
     const long long r = q / kCountSplit;
     if (r >= a.nranges) return;
-    const long long r0 = r * a.range_len, r1 = min(r0 + a.range_len, a.total_samples);
-    const long long part = ((a.range_len / kCountSplit) + 31) & ~31ll;  // whole rows
+    long long total, range_len;
+    if (!list_geometry(a, total, range_len)) {
+        if (lane == 0) a.range_cnt[q] = 0;
+        return;
+    }
+    const long long r0 = r * range_len, r1 = min(r0 + range_len, total);
+    const long long part = ((range_len / kCountSplit) + 31) & ~31ll;  // whole rows
     const long long f0 = min(r0 + (q % kCountSplit) * part, r1);
     const long long f1 = (q % kCountSplit) == kCountSplit - 1 ? r1 : min(f0 + part, r1);
     long long cnt = 0;
@@ -402,7 +426,9 @@ __global__ void __launch_bounds__(NW * 32, 3) list_emit_kernel(ListArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long r = (long long)blockIdx.x * NW + warp;
     if (r >= a.nranges) return;
-    const long long f0 = r * a.range_len, f1 = min(f0 + a.range_len, a.total_samples);
+    long long total, range_len;
+    if (!list_geometry(a, total, range_len)) return;
+    const long long f0 = r * range_len, f1 = min(f0 + range_len, total);
     if (f0 >= f1) return;
     uint32_t* region = smem + warp * REGION;
     long long pos = __ldg(a.range_pre + r);

@@ -39,6 +39,10 @@ struct ListArgs {
     Control* ctl;
     unsigned long long* status; // fused kernel: nranges look-back words (zeroed)
     long long lookahead;        // fused kernel: max count tasks ahead of the emit tasks
+    // two-pass kernels with total_samples < 0 ("deferred"): the capacity is off[nseg], written by
+    // the plan kernel earlier on the stream, range_len holds the block granularity and the
+    // kernels do nothing if plan_ctl records a plan error
+    const Control* plan_ctl;
 };
 
 struct BitmapArgs {

@@ -363,6 +363,44 @@ def test_torch_device_buffers(vx, oracle):
     assert np.array_equal(words.cpu().numpy().view(np.uint64), ow)
 
 
+@pytest.mark.parametrize("n,lmax", [(1, 1000000), (1, 1), (3000, 2048), (65536, 128)])
+def test_device_batch_deferred_plan(vx, oracle, n, lmax):
+    """A device-resident batch below 2^18 segments emits before its plan is read back: the
+    count / scan / emit kernels take the range geometry from off[n] on the device, and the plan's
+    and the emit's control blocks come back in one readback. Bit-exact against the oracle,
+    capacity/N_max resolved afterwards, too-small buffers and plan errors still reported."""
+    import torch
+    segs = oracle.gen_batch(n, 0, lmax, 0, 40 + n)
+    d = torch.from_numpy(segs).cuda()
+    vox, off, ototal = oracle.run_batch(segs)
+    cap = int(sum(oracle.make_plan(s)[0] + 1 for s in segs)) if n <= 3000 else None
+    out = torch.empty((ototal + 4096, 3), dtype=torch.int32, device="cuda")
+    chain = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    b = vx.Batch(None, device_ptr=d.data_ptr(), n=n)
+    assert b._info is None                      # nothing read back yet
+    total = b.emit_list_device(out.data_ptr(), out.shape[0], chain.data_ptr())
+    assert total == ototal
+    assert np.array_equal(out[:total].cpu().numpy(), vox)
+    assert np.array_equal(chain.cpu().numpy(), off)
+    if cap is not None:
+        assert b.capacity == cap
+    b.close()
+    b = vx.Batch(None, device_ptr=d.data_ptr(), n=n)
+    with pytest.raises(vx.VoxGpuError):          # buffer smaller than the list: nothing written
+        b.emit_list_device(out.data_ptr(), ototal - 1, chain.data_ptr())
+    b.close()
+    bad = segs.copy()
+    bad[n // 2, 4] = np.inf
+    db = torch.from_numpy(bad).cuda()
+    b = vx.Batch(None, device_ptr=db.data_ptr(), n=n)   # enqueued: no error yet
+    for _ in range(2):                                   # reported, and again on the next call
+        with pytest.raises(vx.RangeError):
+            b.emit_list_device(out.data_ptr(), out.shape[0], chain.data_ptr())
+    with pytest.raises(vx.RangeError):
+        b.capacity
+    b.close()
+
+
 # ------------------------------------------------------------------ full BASELINE sizes
 @pytest.mark.slow
 def test_full_config4_list_hashes(vx, oracle):
