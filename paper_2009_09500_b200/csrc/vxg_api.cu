@@ -101,6 +101,9 @@ struct vxg_context {
     int num_sms = 148;
     DeviceCache cache;
     Control* h_ctl = nullptr;  // pinned readback slots (2)
+    // single-chain path: mapped pinned chain buffer + control block (allocated on first use)
+    int32_t* h_single = nullptr;
+    Control* h_single_ctl = nullptr;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
     vxg_status fail(vxg_status s, int64_t seg, const char* fmt, ...) {
@@ -601,6 +604,7 @@ VXG_API void vxg_destroy(vxg_context* ctx) {
     ctx->cache.release();
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
+    if (ctx->h_single) cudaFreeHost(ctx->h_single);
     for (cudaEvent_t e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;
@@ -701,9 +705,63 @@ VXG_API vxg_status vxg_make_plans(vxg_context* ctx, const vxg_segment* segs, int
     return VXG_OK;
 }
 
+// Chains up to this many samples take the one-launch single_chain_kernel (one CTA: ~2.5 us per
+// 1024 samples on top of a ~12 us launch + synchronisation; longer chains are faster through the
+// batch path's full-GPU passes).
+constexpr int64_t kSingleMaxSamples = 1 << 14;
+
+// voxelize_parametric in one launch + one synchronisation (see single_chain_kernel). Returns
+// false when the segment is too long (or non-finite) for it: the caller takes the batch path.
+bool single_chain(vxg_context* ctx, const vxg_segment* seg, vxg_voxel* out, int64_t cap,
+                  int64_t* count, vxg_status* st) {
+    // dispatch bound on N + 1 from the endpoints (the kernel recomputes N exactly and refuses,
+    // writing nothing, if the bound was wrong)
+    const double dx = seg->ex - seg->sx, dy = seg->ey - seg->sy, dz = seg->ez - seg->sz;
+    const double ext = std::max(std::fabs(dx), std::max(std::fabs(dy), std::fabs(dz)));
+    const double bound = std::sqrt(dx * dx + dy * dy + dz * dz) + ext + 4.0;
+    if (!(bound < (double)kSingleMaxSamples)) return false;  // long, or non-finite: batch path
+    if (!ctx->h_single) {
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, 12 * (size_t)kSingleMaxSamples + sizeof(Control), cudaHostAllocMapped) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        ctx->h_single = static_cast<int32_t*>(p);
+        ctx->h_single_ctl = reinterpret_cast<Control*>(ctx->h_single + 3 * kSingleMaxSamples);
+    }
+    std::memset(ctx->h_single_ctl, 0, sizeof(Control));
+    vxg::SingleArgs a{{seg->sx, seg->sy, seg->sz, seg->ex, seg->ey, seg->ez},
+                      kSingleMaxSamples, kSingleMaxSamples, ctx->h_single, ctx->h_single_ctl};
+    cudaError_t e = vxg::launch_single_chain(a, ctx->stream);
+    ctx->launches++;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        *st = ctx->cuda_fail(e, "voxelize_parametric");
+        return true;
+    }
+    const Control c = *ctx->h_single_ctl;
+    if (c.n_entries != 0) return false;  // longer than the bound: batch path
+    *st = ctl_status(ctx, c, "voxelize_parametric");
+    if (*st) return true;
+    *count = c.total;
+    const int64_t ncopy = std::min<int64_t>(c.total, cap);
+    if (ncopy > 0) std::memcpy(out, ctx->h_single, 12 * (size_t)ncopy);
+    if (c.total > cap)
+        *st = ctx->fail(VXG_LOGIC_ERROR, 0, "voxelize_parametric: chain of %lld voxels exceeds cap %lld",
+                        (long long)c.total, (long long)cap);
+    return true;
+}
+
 VXG_API vxg_status vxg_voxelize_parametric(vxg_context* ctx, const vxg_segment* seg,
                                            vxg_voxel* out, int64_t cap, int64_t* count) {
     if (!ctx || !seg || !count || cap < 0 || (cap > 0 && !out)) return VXG_INVALID_ARGUMENT;
+    ctx->ok();
+    cudaSetDevice(ctx->device);
+    if (!std::getenv("VXG_NO_SINGLE")) {
+        vxg_status st = VXG_OK;
+        if (single_chain(ctx, seg, out, cap, count, &st)) return st;
+    }
     vxg_batch* b = nullptr;
     vxg_status s = vxg_batch_create(ctx, seg, 1, VXG_MEM_HOST, &b);
     if (!s) s = plan_ready(b);

@@ -748,6 +748,89 @@ cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ======================================================================== single chain
+// voxelize_parametric (src/parametric.cpp:28-40) of ONE segment in ONE launch: plan, samples,
+// dedup and compaction in a single CTA, the chain written straight into mapped pinned host
+// memory -- the latency regime of config 2 and of the reference harness's per-segment
+// "sequential" method, where the batch path's plan readback + count/scan/emit launches would
+// dominate. Each thread evaluates its sample and its predecessor (no cross-thread dependency);
+// chunks of 1024 samples are compacted with a block-wide ballot scan.
+__global__ void __launch_bounds__(1024) single_chain_kernel(SingleArgs a) {
+    __shared__ int s_warp[33];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    Plan pl;
+    if (!make_plan(a.seg[0], a.seg[1], a.seg[2], a.seg[3], a.seg[4], a.seg[5], pl)) {
+        if (tid == 0) record_error(a.ctl, 0, 2);
+        return;
+    }
+    SegRec r;
+    r.sx = a.seg[0];
+    r.sy = a.seg[1];
+    r.sz = a.seg[2];
+    r.wx = pl.wx;
+    r.wy = pl.wy;
+    r.wz = pl.wz;
+    r.ex = pl.ex;
+    r.ey = pl.ey;
+    r.ez = pl.ez;
+    r.flags = rec_flags(a.seg[0], a.seg[1], a.seg[2], a.seg[3], a.seg[4], a.seg[5]);
+    const long long N = pl.n, samples = N + 1;
+    if (samples > a.max_samples) {  // the host's bound was wrong: nothing written, host reroutes
+        if (tid == 0) a.ctl->n_entries = samples;
+        return;
+    }
+    bool bad = false;
+    long long running = 0;
+    for (long long base = 0; base < samples; base += 1024) {
+        const long long k = base + tid;
+        bool keep = false;
+        int32_t x = 0, y = 0, z = 0;
+        if (k < samples) {
+            eval_sample(r, k, N, x, y, z, bad);
+            keep = true;
+            if (k > 0) {
+                int32_t px, py, pz;
+                eval_sample(r, k - 1, N, px, py, pz, bad);
+                keep = x != px || y != py || z != pz;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_warp[warp] = __popc(m);
+        __syncthreads();
+        if (warp == 0) {
+            const int v = s_warp[lane];
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            s_warp[lane] = incl - v;
+            if (lane == 31) s_warp[32] = incl;
+        }
+        __syncthreads();
+        const long long rank = running + s_warp[warp] + __popc(m & ((1u << lane) - 1u));
+        if (keep && rank < a.cap) {
+            int32_t* d = a.out + 3 * rank;
+            d[0] = x;
+            d[1] = y;
+            d[2] = z;
+        }
+        running += s_warp[32];
+        __syncthreads();
+    }
+    if (bad) record_error(a.ctl, 0, 2);
+    if (tid == 0) {
+        a.ctl->total = running;
+        a.ctl->max_steps = (unsigned long long)N;
+    }
+}
+
+cudaError_t launch_single_chain(const SingleArgs& a, cudaStream_t s) {
+    single_chain_kernel<<<1, 1024, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
 int bitmap_tile_log2() { return 12; }
 
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s) {

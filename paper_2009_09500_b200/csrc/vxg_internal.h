@@ -45,6 +45,14 @@ struct ListArgs {
     const Control* plan_ctl;
 };
 
+struct SingleArgs {          // one segment, one CTA (single_chain_kernel)
+    double seg[6];
+    long long cap;              // voxels `out` can hold (more are counted, not written)
+    long long max_samples;      // the launch's bound on N + 1 (larger: nothing done, host reroutes)
+    int32_t* out;               // 3 int32 per voxel (mapped pinned host memory)
+    Control* ctl;               // mapped: total, max_steps (= N), err_seg, n_entries (reroute)
+};
+
 struct BitmapArgs {
     const SegRec* rec;
     const ClipEntry* entries;   // CLIP mode only
@@ -107,6 +115,7 @@ void launch_tile_index(const long long* off, long long n_entries, int ts_log2, l
 cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s);  // count pass + range scan
 cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s);   // emit pass
 cudaError_t launch_list_fused(const ListArgs& a, int num_sms, cudaStream_t s);  // both, overlapped
+cudaError_t launch_single_chain(const SingleArgs& a, cudaStream_t s);
 int list_resident_warps(int num_sms);
 int list_fused_block_samples();  // fused kernel's staged block
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);

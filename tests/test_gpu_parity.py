@@ -168,6 +168,45 @@ def test_single_long_segments(vx, oracle):
         assert np.array_equal(got, oracle.voxelize_parametric(s)), L
 
 
+def test_single_chain_kernel_matches_batch_path(vx, oracle, monkeypatch):
+    """voxelize_parametric's one-launch path (single_chain_kernel: plan + samples + dedup in one
+    CTA, chain into mapped pinned memory) == the batch path (VXG_NO_SINGLE) == the oracle, on the
+    edge cases of both routes: lengths straddling the 2^14-sample dispatch bound, ties, negative
+    coordinates, zero-length segments, the int32 edge (checked rounding), and the error / cap
+    contract (range error for non-finite endpoints, LOGIC_ERROR + the true count when cap is
+    short)."""
+    import ctypes as C
+    cases = [oracle.gen_segment_of_length(L, 77 + L) for L in (1, 2, 31, 32, 33, 1023, 1024, 1025,
+                                                               16370, 16378, 16383, 16384, 16390)]
+    cases += [np.array(c, dtype=np.float64) for c in (
+        [0.5, 0.5, 0.5, -0.5, -0.5, -0.5], [0.1, 0.3, 0.7, 12.45, 4.9, 0.2],
+        [3.2, 3.2, 3.2, 3.4, 3.1, 2.9], [-7.5, 2.5, -0.5, 9.5, -3.5, 0.5],
+        [2147483640.0, 0.0, 0.0, 2147483647.4, 0.0, 0.0],
+        [-2147483647.4, -5.0, 1.0, -2147483600.2, 6.0, -1.0])]
+    rng = np.random.default_rng(5)
+    cases += list(rng.uniform(-300, 300, size=(40, 6)))
+    for s in cases:
+        want = oracle.voxelize_parametric(s)
+        monkeypatch.delenv("VXG_NO_SINGLE", raising=False)
+        got = np.asarray(vx.voxelize_parametric(s[:3], s[3:]), dtype=np.int32).reshape(-1, 3)
+        monkeypatch.setenv("VXG_NO_SINGLE", "1")
+        got_b = np.asarray(vx.voxelize_parametric(s[:3], s[3:]), dtype=np.int32).reshape(-1, 3)
+        assert np.array_equal(got, want), s
+        assert np.array_equal(got_b, want), s
+    monkeypatch.delenv("VXG_NO_SINGLE", raising=False)
+    with pytest.raises(vx.RangeError):
+        vx.voxelize_parametric((0.0, np.nan, 0.0), (1.0, 2.0, 3.0))
+    with pytest.raises(vx.RangeError):
+        vx.voxelize_parametric((0.0, 0.0, 0.0), (3e9, 2.0, 3.0))
+    ctx = vx.default_context()
+    seg = np.array([0.0, 0.0, 0.0, 100.0, 3.0, 1.0])
+    out = np.zeros((10, 3), np.int32)
+    cnt = C.c_int64()
+    st = ctx.lib.vxg_voxelize_parametric(ctx.h, seg.ctypes.data, out.ctypes.data, 10, C.byref(cnt))
+    assert st == vx._lib.VXG_LOGIC_ERROR and cnt.value == 101
+    assert np.array_equal(out, oracle.voxelize_parametric(seg)[:10])
+
+
 def test_config_scaled_lists(vx, oracle):
     for kw in [dict(n=65536, len_fixed=128, V=512, seed=0x5EED0101),
                dict(n=20000, len_max=2048, V=4096, seed=0x5EED0104)]:
