@@ -21,3 +21,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"lis
   -o $out/prof_cfg4 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof4.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tiles_(count|scatter|fill)" -s 3 -c 3 \
   -o $out/prof_cfg5 python bench.py --workload cfg5 --segments 8388608 --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof5.log 2>&1
+# the reference harness's scenarios: voxgpu bench beside the reference's own harness
+bash tools/gpu_paper_tables.sh $tag/pt
+[ -x tools/latency_probe ] || g++ -std=c++17 -O2 -I/usr/local/cuda/include -o tools/latency_probe tools/latency_probe.cpp \
+  -Lpaper_2009_09500_b200/lib -lvoxgpu -L/usr/local/cuda/lib64 -lcudart_static -ldl -lrt -lpthread -Wl,-rpath,'$ORIGIN/../paper_2009_09500_b200/lib'
+( for a in "1 1000" "1 100000" "65536 128"; do echo "== $a"; ./tools/latency_probe $a; done ) > $out/latency_probe.txt 2>&1
