@@ -1,6 +1,5 @@
 // Host-side latency of the small-batch API path (device-resident inputs): where does a small
 // create + emit spend its time? Build: see tools/gpu_session.sh. Prints mean us per call sequence.
-// one-segment create + emit go? Build: see tools/gpu_latency.sh. Prints mean us per call sequence.
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
