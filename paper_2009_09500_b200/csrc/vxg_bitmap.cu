@@ -442,9 +442,10 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-struct PieceRef {  // a decoded piece and its segment's record
-    SegRec r;
+struct PieceRef {  // a decoded piece and its segment's S and W (E is loaded when needed)
+    double sx, sy, sz, wx, wy, wz;
     long long ka;
+    unsigned seg;
     int len;    // samples S + W*k (the E sample, if any, is extra)
     bool hasE;
 };
@@ -454,9 +455,19 @@ __device__ __forceinline__ void load_piece(const TileArgs& g, long long p, long 
     q.len = 0;
     q.hasE = false;
     q.ka = 0;
+    q.seg = 0;
+    q.sx = q.sy = q.sz = q.wx = q.wy = q.wz = 0.0;
     if (p < p1) {
         const uint4 pc = g.pieces[p];
-        q.r = load_rec(g.rec + pc.x);
+        const double2* r = reinterpret_cast<const double2*>(g.rec + pc.x);
+        const double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2);
+        q.sx = a.x;
+        q.sy = a.y;
+        q.sz = b.x;
+        q.wx = b.y;
+        q.wy = c.x;
+        q.wz = c.y;
+        q.seg = pc.x;
         q.ka = pc.y;
         q.hasE = (pc.z >> 31) != 0;
         q.len = (int)(pc.z & 0x7fffffffu) - (q.hasE ? 1 : 0);
@@ -475,7 +486,8 @@ __device__ __forceinline__ void red_or_shared(uint32_t saddr, uint32_t bit, bool
 // Set the bits of one piece group (G lanes per piece, 32/G pieces per warp). sbase: the shared
 // byte address of the tile's word 0 minus 4 * (the tile's global word base).
 template <int G>
-__device__ __forceinline__ void fill_piece(uint32_t sbase, const PieceRef& q, int gl) {
+__device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, const PieceRef& q,
+                                           int gl) {
     int mx = q.len;
 #pragma unroll
     for (int o = G; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -484,17 +496,19 @@ __device__ __forceinline__ void fill_piece(uint32_t sbase, const PieceRef& q, in
     int j = gl;
 #pragma unroll 4
     for (int st = 0; st < steps; ++st) {
-        const int32_t x = round_pos(sample_axis(q.r.sx, q.r.wx, t));
-        const int32_t y = round_pos(sample_axis(q.r.sy, q.r.wy, t));
-        const int32_t z = round_pos(sample_axis(q.r.sz, q.r.wz, t));
+        const int32_t x = round_pos(sample_axis(q.sx, q.wx, t));
+        const int32_t y = round_pos(sample_axis(q.sy, q.wy, t));
+        const int32_t z = round_pos(sample_axis(q.sz, q.wz, t));
         const uint32_t w = (uint32_t)(z * kSS + y * kRW + (x >> 5));
         red_or_shared(sbase + 4u * w, 1u << (x & 31), j < q.len);
         t = __dadd_rn(t, (double)G);
         j += G;
     }
-    if (q.hasE && gl == 0)
-        red_or_shared(sbase + 4u * (uint32_t)(q.r.ez * kSS + q.r.ey * kRW + (q.r.ex >> 5)),
-                      1u << (q.r.ex & 31), true);
+    if (q.hasE && gl == 0) {
+        const SegRec* r = g.rec + q.seg;
+        const int32_t ex = __ldg(&r->ex), ey = __ldg(&r->ey), ez = __ldg(&r->ez);
+        red_or_shared(sbase + 4u * (uint32_t)(ez * kSS + ey * kRW + (ex >> 5)), 1u << (ex & 31), true);
+    }
 }
 
 // Persistent CTAs: claim a tile, set its samples' bits in shared memory, OR it into the bitmap.
@@ -533,7 +547,7 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         for (long long pb = p0 + (long long)warp * PPW; pb < p1; pb += step) {
             PieceRef q;
             load_piece(g, pb + grp, p1, q);
-            fill_piece<G>(sbase, q, gl);
+            fill_piece<G>(g, sbase, q, gl);
         }
         __syncthreads();
         // OR the tile into the bitmap: a row of kTX bits is 4 words = 2 x 16 B; each thread
