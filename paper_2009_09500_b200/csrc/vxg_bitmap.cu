@@ -450,15 +450,14 @@ struct PieceRef {  // a decoded piece and its segment's S and W (E is loaded whe
     bool hasE;
 };
 
-__device__ __forceinline__ void load_piece(const TileArgs& g, long long p, long long p1,
-                                           PieceRef& q) {
-    q.len = 0;
-    q.hasE = false;
-    q.ka = 0;
-    q.seg = 0;
+// Decode a piece entry and issue the loads of its segment's S and W.
+__device__ __forceinline__ void decode_piece(const TileArgs& g, const uint4 pc, PieceRef& q) {
+    q.hasE = (pc.z >> 31) != 0;
+    q.len = (int)(pc.z & 0x7fffffffu) - (q.hasE ? 1 : 0);
+    q.ka = pc.y;
+    q.seg = pc.x;
     q.sx = q.sy = q.sz = q.wx = q.wy = q.wz = 0.0;
-    if (p < p1) {
-        const uint4 pc = g.pieces[p];
+    if (pc.z != 0u) {
         const double2* r = reinterpret_cast<const double2*>(g.rec + pc.x);
         const double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2);
         q.sx = a.x;
@@ -467,10 +466,6 @@ __device__ __forceinline__ void load_piece(const TileArgs& g, long long p, long 
         q.wx = b.y;
         q.wy = c.x;
         q.wz = c.y;
-        q.seg = pc.x;
-        q.ka = pc.y;
-        q.hasE = (pc.z >> 31) != 0;
-        q.len = (int)(pc.z & 0x7fffffffu) - (q.hasE ? 1 : 0);
     }
 }
 
@@ -544,9 +539,19 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bits) - 4u * (uint32_t)base;
         // warp steps of 32/G pieces (G lanes per piece); a step's pieces load together
         constexpr long long step = (long long)NW * PPW;
-        for (long long pb = p0 + (long long)warp * PPW; pb < p1; pb += step) {
+        // the piece entries run two steps ahead and their records are prefetched into L1 one
+        // step ahead (a random 48-B gather per piece; registers are at the 64 limit, so no
+        // second PieceRef: the prefetch costs one instruction and no register)
+        long long pb = p0 + (long long)warp * PPW;
+        const uint4* pcs = g.pieces;
+        uint4 r1 = pb + grp < p1 ? pcs[pb + grp] : make_uint4(0u, 0u, 0u, 0u);
+        uint4 r2 = pb + step + grp < p1 ? pcs[pb + step + grp] : make_uint4(0u, 0u, 0u, 0u);
+        for (; pb < p1; pb += step) {
+            if (r2.z) prefetch_l1(g.rec + r2.x);
             PieceRef q;
-            load_piece(g, pb + grp, p1, q);
+            decode_piece(g, r1, q);
+            r1 = r2;
+            r2 = pb + 2 * step + grp < p1 ? pcs[pb + 2 * step + grp] : make_uint4(0u, 0u, 0u, 0u);
             fill_piece<G>(g, sbase, q, gl);
         }
         __syncthreads();
@@ -591,6 +596,7 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
 
 // =============================================================================== launchers
 int tile_len_classes() { return kLenClasses; }
+
 int tile_perm_keys() { return kPermKeys; }
 
 int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz) {

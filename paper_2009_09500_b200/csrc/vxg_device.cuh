@@ -87,6 +87,11 @@ __device__ __forceinline__ bool round_checked(double c, int32_t& out) {
     return true;
 }
 
+// L1 prefetch (no register); callers keep p in bounds.
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // S + W*t with separate multiply and add (include/voxline/parametric.hpp:44-47).
 __device__ __forceinline__ double sample_axis(double s, double w, double t) {
     return __dadd_rn(s, __dmul_rn(w, t));
