@@ -469,20 +469,19 @@ __device__ __forceinline__ void decode_piece(const TileArgs& g, const uint4 pc, 
     }
 }
 
-// Set the bits of one piece group (G lanes per piece, 32/G pieces per warp).
-// OR a bit into the tile through a 32-bit shared address; the predicate keeps the row loop
-// branch-free (lanes past their piece's end compute but do not store).
-__device__ __forceinline__ void red_or_shared(uint32_t saddr, uint32_t bit, bool on) {
-    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p red.shared.or.b32 [%0], %1;\n\t}"
-                 ::"r"(saddr), "r"(bit), "r"((uint32_t)on)
-                 : "memory");
+// OR a bit into the tile through a 32-bit shared address.
+__device__ __forceinline__ void red_or_shared(uint32_t saddr, uint32_t bit) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(saddr), "r"(bit) : "memory");
 }
 
 // Set the bits of one piece group (G lanes per piece, 32/G pieces per warp). sbase: the shared
 // byte address of the tile's word 0 minus 4 * (the tile's global word base).
+// Lanes past their piece's end still compute a sample but OR it into their own scratch word
+// (`spare`, after the tile) instead of branching around the reduction: the row loop stays
+// straight-line (a select instead of a branch pair per sample).
 template <int G>
-__device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, const PieceRef& q,
-                                           int gl) {
+__device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, uint32_t spare,
+                                           const PieceRef& q, int gl) {
     int mx = q.len;
 #pragma unroll
     for (int o = G; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -495,14 +494,14 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, co
         const int32_t y = round_pos(sample_axis(q.sy, q.wy, t));
         const int32_t z = round_pos(sample_axis(q.sz, q.wz, t));
         const uint32_t w = (uint32_t)(z * kSS + y * kRW + (x >> 5));
-        red_or_shared(sbase + 4u * w, 1u << (x & 31), j < q.len);
+        red_or_shared(j < q.len ? sbase + 4u * w : spare, 1u << (x & 31));
         t = __dadd_rn(t, (double)G);
         j += G;
     }
     if (q.hasE && gl == 0) {
         const SegRec* r = g.rec + q.seg;
         const int32_t ex = __ldg(&r->ex), ey = __ldg(&r->ey), ez = __ldg(&r->ez);
-        red_or_shared(sbase + 4u * (uint32_t)(ez * kSS + ey * kRW + (ex >> 5)), 1u << (ex & 31), true);
+        red_or_shared(sbase + 4u * (uint32_t)(ez * kSS + ey * kRW + (ex >> 5)), 1u << (ex & 31));
     }
 }
 
@@ -512,8 +511,7 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, co
 // a step in z moves to the next bank (without the pad, samples of a segment running along z hit
 // the same bank with different words: up to 32-way conflicts on the shared atomics).
 // Work split: a warp takes 32/G pieces at a time, G lanes per piece (G from the mean piece
-// length), with the next pieces and their segments' records in flight while the current ones
-// are evaluated (two register sets, no copies).
+// length); piece entries run two steps ahead, their records are prefetched one step ahead.
 template <int NW, int G>
 __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
     extern __shared__ __align__(16) uint32_t bits[];
@@ -537,6 +535,7 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         const int x0 = (int)(txi * kTX), y0 = (int)(tyi * kTY), z0 = (int)(g.z_lo + tzi * kTZ);
         const int base = z0 * kSS + y0 * kRW + (x0 >> 5);  // (x0 is a multiple of 32)
         const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bits) - 4u * (uint32_t)base;
+        const uint32_t spare = (uint32_t)__cvta_generic_to_shared(bits + kTileWords + lane);
         // warp steps of 32/G pieces (G lanes per piece); a step's pieces load together
         constexpr long long step = (long long)NW * PPW;
         // the piece entries run two steps ahead and their records are prefetched into L1 one
@@ -552,7 +551,7 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
             decode_piece(g, r1, q);
             r1 = r2;
             r2 = pb + 2 * step + grp < p1 ? pcs[pb + 2 * step + grp] : make_uint4(0u, 0u, 0u, 0u);
-            fill_piece<G>(g, sbase, q, gl);
+            fill_piece<G>(g, sbase, spare, q, gl);
         }
         __syncthreads();
         // OR the tile into the bitmap: a row of kTX bits is 4 words = 2 x 16 B; each thread
@@ -605,7 +604,7 @@ int tile_dims(long long V, long long depth, int& tx, int& ty, int& tz) {
     tz = kTZ;
     (void)V;
     (void)depth;
-    return kTileWords * 4;  // shared-memory bytes (padded z-slices)
+    return kTileWords * 4;  // shared-memory bytes of the tile (padded z-slices)
 }
 
 void launch_tiles_perm(const TileArgs& g, cudaStream_t s) {
@@ -625,7 +624,7 @@ void launch_tiles_scatter(const TileArgs& g, cudaStream_t s) {
 template <int G>
 static cudaError_t launch_fill_g(const TileArgs& g, int num_sms, cudaStream_t s) {
     constexpr int NW = 32;
-    const size_t smem = (size_t)kTileWords * 4;
+    const size_t smem = (size_t)(kTileWords + 32) * 4;  // the tile + 32 per-lane spare words
     cudaFuncSetAttribute(tiles_fill_kernel<NW, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     int per_sm = 0;
