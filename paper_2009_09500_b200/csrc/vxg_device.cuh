@@ -40,8 +40,12 @@ __device__ __forceinline__ int32_t voxel_key(int32_t x, int32_t y, int32_t z) {
 // RM(c + K) = 2^51 + floor(2c + 1) / 2 exactly and the 52-bit mantissa field is F = floor(2c + 1);
 // llround(c) = floor(c + 0.5) = F >> 1 (one funnel shift on the ALU pipe). One FP64 op instead of
 // the two of an RZ add + magic-number extraction, and no F2I (quarter-rate conversion pipe).
+// (K lives in the constant bank: DADD takes it as a c[][] operand, so hot loops neither hold it
+// in two registers nor rematerialise it with two moves per iteration)
+static __constant__ double kRoundPosK = 0x1.0000000000001p51;
+
 __device__ __forceinline__ int32_t round_pos(double c) {
-    const double d = __dadd_rd(c, 0x1.0000000000001p51);
+    const double d = __dadd_rd(c, kRoundPosK);
     return (int32_t)__funnelshift_r((unsigned)__double2loint(d), (unsigned)__double2hiint(d), 1);
 }
 
