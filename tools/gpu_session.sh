@@ -19,8 +19,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --cs
   --log-file $out/launches_cfg5.csv python bench.py --workload cfg5 --steps 1 --warmup 3 --no-e2e --no-cpu > $out/ncu_bench5.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"list_(fused|count|emit)_kernel" -s 1 -c 1 \
   -o $out/prof_cfg4 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof4.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tiles_(count|scatter|fill)" -s 3 -c 3 \
-  -o $out/prof_cfg5 python bench.py --workload cfg5 --segments 8388608 --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof5.log 2>&1
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"tiles_(count|scatter|fill)" -s 3 -c 3 \
+  -o $out/prof_cfg5 python bench.py --workload cfg5 --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof5.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tiles_fill" -s 1 -c 1 \
+  -o $out/prof_cfg3 python bench.py --workload cfg3 --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof3.log 2>&1
 # the reference harness's scenarios: voxgpu bench beside the reference's own harness
 bash tools/gpu_paper_tables.sh $tag/pt
 [ -x tools/latency_probe ] || g++ -std=c++17 -O2 -I/usr/local/cuda/include -o tools/latency_probe tools/latency_probe.cpp \
