@@ -106,7 +106,10 @@ VXG_API vxg_status vxg_segment_lengths(vxg_context* ctx, const vxg_segment* segs
 VXG_API vxg_status vxg_make_plans(vxg_context* ctx, const vxg_segment* segs, int64_t n,
                                   int64_t* steps, double* w3);
 /* voxelize_parametric (src/parametric.cpp:28-40) of one host segment: the chain goes to host
- * `out` (capacity `cap` voxels; N+1 always suffices), its length to *count. */
+ * `out` (capacity `cap` voxels; N+1 always suffices), its length to *count. A chain longer than
+ * `cap` -> LOGIC_ERROR with the true length in *count and the first `cap` voxels written.
+ * Chains up to 2^14 samples take one launch and one synchronisation (single_chain_kernel, the
+ * latency regime); longer ones the batch passes. */
 VXG_API vxg_status vxg_voxelize_parametric(vxg_context* ctx, const vxg_segment* seg,
                                            vxg_voxel* out, int64_t cap, int64_t* count);
 /* chain_length_bounds (src/parametric.cpp:42-50). */
