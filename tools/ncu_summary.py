@@ -1,6 +1,6 @@
 """Summarise an ncu --set full report of one kernel (run here, no GPU needed).
 
-    python tools/ncu_summary.py gpurun_out/x.ncu-rep [--json out.json] [--top 25]
+    python tools/ncu_summary.py gpurun_out/x.ncu-rep [-k kernel_regex] [--json out.json] [--top 25]
 
 Prints duration, DRAM bytes/throughput, occupancy, issue utilisation, the stall-reason mix and
 the hottest SASS instructions (stall samples + execution counts).
@@ -34,8 +34,10 @@ def main():
     ap.add_argument("rep")
     ap.add_argument("--json")
     ap.add_argument("--top", type=int, default=25)
+    ap.add_argument("-k", default=None, help="kernel name regex (reports holding several kernels)")
     args = ap.parse_args()
-    rows = ncu_csv(args.rep, "raw")
+    filt = ["-k", "regex:" + args.k] if args.k else []
+    rows = ncu_csv(args.rep, "raw", filt)
     hdr, units, vals = rows[0], rows[1], rows[2]
     d = dict(zip(hdr, vals))
     u = dict(zip(hdr, units))
@@ -50,11 +52,13 @@ def main():
     summary["stalls_pct"] = {k: round(100 * v / tot, 1) for k, v in stalls[:10]}
     for k, v in summary.items():
         print(f"{k:70s} {v}")
-    src = ncu_csv(args.rep, "source", ["--print-source", "sass"])
+    src = ncu_csv(args.rep, "source", ["--print-source", "sass", *filt])
     hdr2 = src[1]
     ix = {h: i for i, h in enumerate(hdr2)}
     top, tot_s, tot_e = [], 0, 0
     for r in src[2:]:
+        if r and r[0] in ("Kernel Name", "Address"):
+            break  # a second kernel's block: keep the first
         if len(r) < len(hdr2):
             continue
         s = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
