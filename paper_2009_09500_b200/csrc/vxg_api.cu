@@ -17,6 +17,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "vxg_device.cuh"
@@ -94,6 +95,9 @@ constexpr long long kSegMax = (1ll << 59) - 1;
 struct vxg_context {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // streamed bitmap readback (created on first use)
+    unsigned* h_layers = nullptr;        // mapped: finished tiles per z-layer (streamed readback)
+    int64_t h_layers_cap = 0;
     bool own_stream = false;
     std::string err;
     int64_t err_seg = -1;
@@ -484,8 +488,39 @@ vxg_status emit_bitmap_atomic(vxg_batch* b, unsigned long long* d_words, int64_t
 
 
 // Tile-binned path (vxg_bitmap.cu): V a multiple of 128, every N_i < 2^31.
+// Streamed readback of a host bitmap: while the fill kernel runs, every z-layer of tiles it has
+// finished (counted in mapped memory by the kernel) is copied to the host on the copy stream, so
+// the PCIe transfer overlaps the fill instead of following it.
+struct LayerStream {
+    uint64_t* host_words;
+    unsigned* counts;  // mapped, one per z-layer
+};
+
+bool layer_stream_setup(vxg_context* ctx, int64_t ntz, LayerStream& ls) {
+    if (!ctx->copy_stream &&
+        cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (ctx->h_layers_cap < ntz) {
+        if (ctx->h_layers) cudaFreeHost(ctx->h_layers);
+        ctx->h_layers = nullptr;
+        ctx->h_layers_cap = 0;
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, sizeof(unsigned) * (size_t)ntz, cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        ctx->h_layers = static_cast<unsigned*>(p);
+        ctx->h_layers_cap = ntz;
+    }
+    std::memset(ctx->h_layers, 0, sizeof(unsigned) * (size_t)ntz);
+    ls.counts = ctx->h_layers;
+    return true;
+}
+
 vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t V, int64_t z_lo,
-                             int64_t z_hi, int64_t* outside) {
+                             int64_t z_hi, int64_t* outside, uint64_t* host_words = nullptr) {
     vxg_context* ctx = b->ctx;
     vxg::TileArgs g{};
     g.rec = b->rec.as<SegRec>();
@@ -507,6 +542,9 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     g.tile_cur = reinterpret_cast<unsigned*>(g.tile_off + nbins + 1);
     g.words = d_words;
     g.ctl = ctl_slot(b, 3);
+    LayerStream ls{host_words, nullptr};
+    if (host_words && !layer_stream_setup(ctx, g.ntz, ls)) ls.host_words = nullptr;
+    g.layer_done = ls.host_words ? ls.counts : nullptr;
     cudaEventRecord(ctx->ev[2], ctx->stream);
     cudaMemsetAsync(g.ctl, 0, sizeof(Control), ctx->stream);
     cudaMemsetAsync(g.tile_cnt, 0, sizeof(long long) * (size_t)nbins, ctx->stream);
@@ -536,6 +574,13 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     if (outside) *outside = b->capacity - c.total;
     if (npieces == 0) {
         b->emit_ms = b->aux_ms = 0.f;
+        if (ls.host_words) {  // nothing to fill: the device words (zeroed or uploaded) go back as they are
+            const size_t bytes = 8 * (size_t)(((V * V * (z_hi - z_lo)) + 63) / 64);
+            cudaError_t ce = cudaMemcpyAsync(ls.host_words, d_words, bytes, cudaMemcpyDeviceToHost,
+                                             ctx->stream);
+            if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
+            if (ce != cudaSuccess) return ctx->cuda_fail(ce, "bitmap readback");
+        }
         return VXG_OK;
     }
     if (!b->entries.ensure(ctx, sizeof(uint4) * (size_t)npieces))
@@ -549,16 +594,58 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     ctx->launches += 2;
     cudaEventRecord(ctx->ev[4], ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "tiles_fill_kernel");
+    cudaError_t qe = cudaSuccess;
+    if (ls.host_words) {  // copy each finished layer while the fill goes on
+        const unsigned per_layer = (unsigned)(g.ntx * g.nty);
+        const int64_t plane_words = V * V / 64;
+        std::vector<char> copied((size_t)g.ntz, 0);
+        int64_t left = g.ntz;
+        bool done = false;
+        while (left > 0) {
+            bool any = false;
+            for (int64_t l = 0; l < g.ntz; ++l) {
+                if (copied[(size_t)l]) continue;
+                if (!done && reinterpret_cast<volatile unsigned*>(ls.counts)[l] < per_layer) continue;
+                const int64_t za = z_lo + l * g.tz, zb = std::min<int64_t>(za + g.tz, z_hi);
+                const int64_t w0 = (za - z_lo) * plane_words;
+                cudaMemcpyAsync(ls.host_words + w0, d_words + w0, 8 * (size_t)((zb - za) * plane_words),
+                                cudaMemcpyDeviceToHost, ctx->copy_stream);
+                copied[(size_t)l] = 1;
+                --left;
+                any = true;
+            }
+            if (left == 0) break;
+            if (!done) {
+                qe = cudaStreamQuery(ctx->stream);
+                if (qe == cudaSuccess) {
+                    done = true;  // the fill is over: copy whatever is left
+                    continue;
+                }
+                if (qe != cudaErrorNotReady) break;
+                qe = cudaSuccess;
+            }
+            if (!any) std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+    }
     s = read_ctl(ctx, g.ctl, c, "bitmap");
+    if (ls.host_words) {
+        const cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+        if (!s && qe != cudaSuccess) s = ctx->cuda_fail(qe, "tiles_fill_kernel");
+        if (!s && ce != cudaSuccess) s = ctx->cuda_fail(ce, "bitmap readback");
+    }
     cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);
     cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);
     return s;
 }
 
+bool use_tiles(const vxg_batch* b, int64_t V, int64_t z_lo, int64_t z_hi) {
+    return V % 128 == 0 && b->max_steps < (1ll << 31) && z_hi > z_lo &&
+           !std::getenv("VXG_BITMAP_ATOMIC");
+}
+
 vxg_status emit_bitmap_device(vxg_batch* b, unsigned long long* d_words, int64_t V, int64_t z_lo,
                               int64_t z_hi, int clip, int64_t* outside) {
-    if (V % 128 == 0 && b->max_steps < (1ll << 31) && z_hi > z_lo && !std::getenv("VXG_BITMAP_ATOMIC"))
-        return emit_bitmap_tiles(b, d_words, V, z_lo, z_hi, outside);
+    if (use_tiles(b, V, z_lo, z_hi)) return emit_bitmap_tiles(b, d_words, V, z_lo, z_hi, outside);
     return emit_bitmap_atomic(b, d_words, V, z_lo, z_hi, clip, outside);
 }
 
@@ -601,6 +688,11 @@ VXG_API void vxg_destroy(vxg_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+    }
+    if (ctx->h_layers) cudaFreeHost(ctx->h_layers);
     ctx->cache.release();
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -1031,6 +1123,17 @@ VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t 
         cudaMemsetAsync(d.p, 0, 8 * nwords, ctx->stream);
     else
         cudaMemcpyAsync(d.p, words, 8 * nwords, cudaMemcpyHostToDevice, ctx->stream);
+    // large slabs through the tile path: streamed readback (each finished z-layer of tiles goes
+    // over PCIe while the fill continues)
+    const char* smin = std::getenv("VXG_BITMAP_STREAM_MIN");  // bytes (tests lower it)
+    if (use_tiles(b, V, z_lo, z_hi) && 8 * nwords >= (smin ? std::strtoull(smin, nullptr, 10) : (64ull << 20)) &&
+        !std::getenv("VXG_BITMAP_NO_STREAM")) {
+        const vxg_status s = emit_bitmap_tiles(b, d.as<unsigned long long>(), V, z_lo, z_hi,
+                                               outside, words);
+        b->timing.kernel_ns = ns_since(t0);
+        b->timing.assemble_ns = 0;
+        return s;
+    }
     vxg_status s = emit_bitmap_device(b, d.as<unsigned long long>(), V, z_lo, z_hi, clip, outside);
     b->timing.kernel_ns = ns_since(t0);
     if (s) return s;

@@ -530,8 +530,11 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         if (tile >= g.ntiles) break;
         const long long p0 = __ldg(g.tile_off + tile * kLenClasses),
                         p1 = __ldg(g.tile_off + (tile + 1) * kLenClasses);
-        if (p0 == p1) continue;  // no samples: the bitmap keeps its words
         const long long txi = tile % g.ntx, tyi = (tile / g.ntx) % g.nty, tzi = tile / (g.ntx * g.nty);
+        if (p0 == p1) {  // no samples: the bitmap keeps its words
+            if (g.layer_done && tid == 0) atomicAdd_system(g.layer_done + tzi, 1u);
+            continue;
+        }
         const int x0 = (int)(txi * kTX), y0 = (int)(tyi * kTY), z0 = (int)(g.z_lo + tzi * kTZ);
         const int base = z0 * kSS + y0 * kRW + (x0 >> 5);  // (x0 is a multiple of 32)
         const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bits) - 4u * (uint32_t)base;
@@ -590,6 +593,11 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
             }
         }
         // (the next iteration's __syncthreads orders these clears before new atomics)
+        if (g.layer_done) {  // streamed readback: this tile's words are final
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) atomicAdd_system(g.layer_done + tzi, 1u);
+        }
     }
 }
 

@@ -341,6 +341,34 @@ def test_bitmap_tiles_accumulate_and_match_atomic_path(vx, oracle, monkeypatch):
     assert np.array_equal(w_atomic, w_tiles)
 
 
+@pytest.mark.parametrize("V,slab", [(512, (0, 512)), (1024, (100, 700)), (1024, (900, 1000))])
+def test_bitmap_streamed_readback(vx, oracle, monkeypatch, V, slab):
+    """Host bitmaps (>= 64 MiB by default) through the tile path are read back layer by layer while the
+    fill runs (mapped per-layer tile counters, copy stream): same words and outside count as the
+    plain readback (VXG_BITMAP_NO_STREAM), overwriting or OR-ing into the caller's words, and an
+    empty slab still returns the caller's words."""
+    z0, z1 = slab
+    monkeypatch.setenv("VXG_BITMAP_STREAM_MIN", "0")  # stream every size here
+    segs = np.concatenate([vx.gen_segments(4000, 0, 500, V, 71), oracle.gen_batch(300, 0, 200, 0, 72)])
+    b = vx.Batch(segs)
+    want, _ = oracle.bitmap(segs, V, z0, z1)
+    monkeypatch.setenv("VXG_BITMAP_NO_STREAM", "1")
+    plain, out_p = b.emit_bitmap(V, z0, z1)
+    monkeypatch.delenv("VXG_BITMAP_NO_STREAM")
+    streamed, out_s = b.emit_bitmap(V, z0, z1)
+    assert np.array_equal(plain, want) and np.array_equal(streamed, want)
+    assert out_s == out_p
+    prior = np.zeros_like(want)
+    prior[::11] = np.uint64(3)
+    got, _ = b.emit_bitmap(V, z0, z1, words=prior.copy(), overwrite=False)
+    assert np.array_equal(got, want | prior)
+    b.close()
+    far = vx.Batch(np.array([[5000.0, 5000, 5000, 5010, 5003, 5001]]))  # no sample in the volume
+    got, outside = far.emit_bitmap(V, z0, z1, words=prior.copy(), overwrite=False)
+    assert np.array_equal(got, prior) and outside == 11
+    far.close()
+
+
 def test_bitmap_overwrite_discards_prior_words(vx, oracle):
     """VXG_BITMAP_OVERWRITE zeroes the words on the device: garbage in the caller's buffer
     (host or device) does not survive, on the tile path and on a slab."""
