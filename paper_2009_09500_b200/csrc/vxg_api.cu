@@ -160,7 +160,7 @@ struct vxg_batch {
     vxg_context* ctx = nullptr;
     int64_t n = 0;
     const double* d_segs = nullptr;  // owned (segs) or borrowed device pointer
-    DBuf segs, rec, steps, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl, ranges;
+    DBuf segs, rec, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl, ranges;
     int64_t max_steps = 0, capacity = 0;
     // The plan's scalars (N_max, capacity) and errors are read back lazily: batch_create only
     // enqueues the plan kernel; the first call that needs them (or the emit's own readback for a
@@ -261,14 +261,13 @@ vxg_status run_plan(vxg_batch* b) {
     const int64_t n = b->n;
     const int tiles = vxg::plan_tile_count(n);
     if (!b->rec.ensure(ctx, sizeof(SegRec) * (size_t)n) ||
-        !b->steps.ensure(ctx, sizeof(long long) * (size_t)n) ||
         !b->off.ensure(ctx, sizeof(long long) * (size_t)(n + 1)) ||
         !b->status.ensure(ctx, sizeof(unsigned long long) * (size_t)tiles))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_preprocess: out of device memory");
     cudaMemsetAsync(ctl_slot(b, 0), 0, sizeof(Control), ctx->stream);
     cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)tiles, ctx->stream);
-    vxg::PlanArgs a{b->d_segs, n, b->rec.as<SegRec>(), b->steps.as<long long>(),
-                    b->off.as<long long>(), b->status.as<unsigned long long>(), ctl_slot(b, 0)};
+    vxg::PlanArgs a{b->d_segs, n, b->rec.as<SegRec>(), b->off.as<long long>(),
+                    b->status.as<unsigned long long>(), ctl_slot(b, 0)};
     cudaEventRecord(b->pev[0], ctx->stream);
     vxg::launch_plan(a, ctx->stream);
     ctx->launches++;
@@ -953,7 +952,7 @@ VXG_API vxg_status vxg_batch_from_plan(vxg_context* ctx, const vxg_segment* segs
     DBuf dplans;
     s = upload_segments(b, segs, n, VXG_MEM_HOST);
     if (!s && (!b->rec.ensure(ctx, sizeof(SegRec) * (size_t)n) ||
-               !b->steps.ensure(ctx, 8 * (size_t)n) || !b->off.ensure(ctx, 8 * (size_t)(n + 1)) ||
+               !b->off.ensure(ctx, 8 * (size_t)(n + 1)) ||
                !dplans.ensure(ctx, sizeof(vxg_segment_plan) * (size_t)n)))
         s = ctx->fail(VXG_OUT_OF_MEMORY, -1, "batch_voxelize: out of device memory");
     if (!s) {
@@ -962,7 +961,7 @@ VXG_API vxg_status vxg_batch_from_plan(vxg_context* ctx, const vxg_segment* segs
         cudaMemcpyAsync(b->off.as<long long>() + n, &capacity, 8, cudaMemcpyHostToDevice, ctx->stream);
         cudaMemsetAsync(ctl_slot(b, 0), 0, sizeof(Control), ctx->stream);
         vxg::launch_pack_plan(b->d_segs, dplans.as<vxg_segment_plan>(), n, b->rec.as<SegRec>(),
-                              b->steps.as<long long>(), b->off.as<long long>(), ctl_slot(b, 0),
+                              b->off.as<long long>(), ctl_slot(b, 0),
                               ctx->stream);
         ctx->launches++;
         Control c;

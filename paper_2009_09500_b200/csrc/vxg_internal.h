@@ -19,7 +19,6 @@ struct PlanArgs {
     const double* segs;  // AoS, 6 doubles per segment, 16-B aligned
     long long n;
     SegRec* rec;
-    long long* steps;
     long long* offsets;  // n + 1
     unsigned long long* status;
     Control* ctl;
@@ -134,7 +133,7 @@ void launch_segment_lengths(const double* segs, long long n, double* out, cudaSt
 void launch_export_plans(const SegRec* rec, const long long* off, long long n,
                          vxg_segment_plan* out, cudaStream_t s);
 void launch_pack_plan(const double* segs, const vxg_segment_plan* plans, long long n, SegRec* rec,
-                      long long* steps, long long* off, Control* ctl, cudaStream_t s);
+                      long long* off, Control* ctl, cudaStream_t s);
 void launch_work_item(const SegRec* rec, const long long* off, long long i, long long k,
                       int32_t* out, Control* ctl, cudaStream_t s);
 void launch_gen(const GenArgs& a, cudaStream_t s);

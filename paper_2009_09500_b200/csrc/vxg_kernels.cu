@@ -90,7 +90,6 @@ __global__ void __launch_bounds__(BLOCK) plan_kernel(PlanArgs a) {
             r.ez = pl.ez;
             r.flags = rec_flags(sx, sy, sz, ex, ey, ez);
             a.rec[i] = r;
-            a.steps[i] = pl.n;
             cnt = pl.n + 1;
             mx = (unsigned long long)pl.n > mx ? (unsigned long long)pl.n : mx;
         }
@@ -337,8 +336,8 @@ __global__ void export_plans_kernel(const SegRec* __restrict__ rec, const long l
 // are the exclusive prefix of N_i + 1 (src/batch.cpp:98-105 checks only the last one).
 __global__ void pack_plan_kernel(const double* __restrict__ segs,
                                  const vxg_segment_plan* __restrict__ plans, long long n,
-                                 SegRec* __restrict__ rec, long long* __restrict__ steps,
-                                 long long* __restrict__ off, Control* ctl) {
+                                 SegRec* __restrict__ rec, long long* __restrict__ off,
+                                 Control* ctl) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double* s = segs + 6 * i;
@@ -362,7 +361,6 @@ __global__ void pack_plan_kernel(const double* __restrict__ segs,
               (rec_flags(s[0], s[1], s[2], s[3], s[4], s[5]) & REC_CHECK) |
               ((fabs(p.wx) > 1.0 || fabs(p.wy) > 1.0 || fabs(p.wz) > 1.0) ? REC_WIDE : 0u);
     rec[i] = r;
-    steps[i] = p.step_count;
     off[i] = p.output_offset;
     if (p.step_count < 0) record_error(ctl, i, 4);
     if (i > 0 && plans[i - 1].output_offset + plans[i - 1].step_count + 1 != p.output_offset)
@@ -498,8 +496,8 @@ void launch_export_plans(const SegRec* rec, const long long* off, long long n,
     export_plans_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(rec, off, n, out);
 }
 void launch_pack_plan(const double* segs, const vxg_segment_plan* plans, long long n, SegRec* rec,
-                      long long* steps, long long* off, Control* ctl, cudaStream_t s) {
-    pack_plan_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(segs, plans, n, rec, steps, off, ctl);
+                      long long* off, Control* ctl, cudaStream_t s) {
+    pack_plan_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(segs, plans, n, rec, off, ctl);
 }
 void launch_work_item(const SegRec* rec, const long long* off, long long i, long long k,
                       int32_t* out, Control* ctl, cudaStream_t s) {
