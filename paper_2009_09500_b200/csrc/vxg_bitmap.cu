@@ -512,7 +512,7 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, ui
 // the same bank with different words: up to 32-way conflicts on the shared atomics).
 // Work split: a warp takes 32/G pieces at a time, G lanes per piece (G from the mean piece
 // length); piece entries run two steps ahead, their records are prefetched one step ahead.
-template <int NW, int G>
+template <int NW, int G, bool STREAM>
 __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
     extern __shared__ __align__(16) uint32_t bits[];
     __shared__ long long s_tile[2];
@@ -530,11 +530,11 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         if (tile >= g.ntiles) break;
         const long long p0 = __ldg(g.tile_off + tile * kLenClasses),
                         p1 = __ldg(g.tile_off + (tile + 1) * kLenClasses);
-        const long long txi = tile % g.ntx, tyi = (tile / g.ntx) % g.nty, tzi = tile / (g.ntx * g.nty);
         if (p0 == p1) {  // no samples: the bitmap keeps its words
-            if (g.layer_done && tid == 0) atomicAdd_system(g.layer_done + tzi, 1u);
+            if (STREAM && tid == 0) atomicAdd_system(g.layer_done + tile / (g.ntx * g.nty), 1u);
             continue;
         }
+        const long long txi = tile % g.ntx, tyi = (tile / g.ntx) % g.nty, tzi = tile / (g.ntx * g.nty);
         const int x0 = (int)(txi * kTX), y0 = (int)(tyi * kTY), z0 = (int)(g.z_lo + tzi * kTZ);
         const int base = z0 * kSS + y0 * kRW + (x0 >> 5);  // (x0 is a multiple of 32)
         const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bits) - 4u * (uint32_t)base;
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
             }
         }
         // (the next iteration's __syncthreads orders these clears before new atomics)
-        if (g.layer_done) {  // streamed readback: this tile's words are final
+        if (STREAM) {  // streamed readback: this tile's words are final
             __threadfence();
             __syncthreads();
             if (tid == 0) atomicAdd_system(g.layer_done + tzi, 1u);
@@ -629,19 +629,26 @@ void launch_tiles_scan(const TileArgs& g, cudaStream_t s) { tiles_scan_kernel<<<
 void launch_tiles_scatter(const TileArgs& g, cudaStream_t s) {
     tiles_scatter_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(g);
 }
-template <int G>
-static cudaError_t launch_fill_g(const TileArgs& g, int num_sms, cudaStream_t s) {
+template <int G, bool STREAM>
+static cudaError_t launch_fill_gs(const TileArgs& g, int num_sms, cudaStream_t s) {
     constexpr int NW = 32;
     const size_t smem = (size_t)(kTileWords + 32) * 4;  // the tile + 32 per-lane spare words
-    cudaFuncSetAttribute(tiles_fill_kernel<NW, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(tiles_fill_kernel<NW, G, STREAM>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiles_fill_kernel<NW, G>, NW * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiles_fill_kernel<NW, G, STREAM>, NW * 32,
+                                                  smem);
     if (per_sm < 1) per_sm = 1;
     long long grid = (long long)per_sm * num_sms;
     if (grid > g.ntiles) grid = g.ntiles;
-    tiles_fill_kernel<NW, G><<<(unsigned)grid, NW * 32, smem, s>>>(g);
+    tiles_fill_kernel<NW, G, STREAM><<<(unsigned)grid, NW * 32, smem, s>>>(g);
     return cudaGetLastError();
+}
+
+// (the streamed-readback signalling is a separate instantiation: the plain kernel stays as lean)
+template <int G>
+static cudaError_t launch_fill_g(const TileArgs& g, int num_sms, cudaStream_t s) {
+    return g.layer_done ? launch_fill_gs<G, true>(g, num_sms, s) : launch_fill_gs<G, false>(g, num_sms, s);
 }
 
 // mean_len: mean samples per piece -> lanes per piece (VXG_FILL_G overrides: 4, 8, 16 or 32)
