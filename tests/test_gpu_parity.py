@@ -497,6 +497,27 @@ def test_full_config4_list_hashes(vx, oracle):
 
 
 @pytest.mark.slow
+def test_full_config3_bitmap(vx, oracle):
+    """Config 3 at full size (16M segments, N = 64, 1024^3, the bench's seed): the device
+    bitmap, the streamed host bitmap and the oracle's bitmap over all 1.09 G samples agree bit
+    for bit, and so do the outside counts."""
+    import torch
+    V, n = 1024, 16 * 1024 * 1024
+    d = torch.empty((n, 6), dtype=torch.float64, device="cuda")
+    ctx = vx.default_context()
+    ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, 64, 0, V, 0x5EED0103, d.data_ptr(), 1))
+    b = vx.Batch(None, device_ptr=d.data_ptr(), n=n)
+    w = torch.zeros(V ** 3 // 64, dtype=torch.int64, device="cuda")
+    out_d = b.emit_bitmap_device(w.data_ptr(), V, 0, V, False)
+    host, out_h = b.emit_bitmap(V)  # 128 MiB: the streamed readback
+    segs = d.cpu().numpy()
+    ow, oo = oracle.bitmap(segs, V)
+    assert np.array_equal(w.cpu().numpy().view(np.uint64), ow)
+    assert np.array_equal(host, ow)
+    assert out_d == out_h == oo
+
+
+@pytest.mark.slow
 def test_full_config5_slabs_consistent(vx, oracle):
     """Config 5 geometry (4096^3 bitmap, N ~ U{1..2048}) on 8M segments: the 8 device-clipped
     z-slabs reassemble the unclipped full bitmap bit for bit, and a 1/512 subsample of the
