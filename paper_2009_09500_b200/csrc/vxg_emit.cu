@@ -90,12 +90,16 @@ __device__ __forceinline__ void walker_row(RowWalker& w, const long long* __rest
 //   list_count_kernel : every warp walks its range and counts the kept (deduplicated) voxels
 //   range_scan_kernel : exclusive prefix of the R range counts (one CTA)
 //   list_emit_kernel  : every warp walks the same range again from its known output position,
-//                       staging kept voxels in shared memory (12-B records at their rank) and
-//                       streaming each block of 32*IPT samples out with 16-B vector stores; chain
-//                       offsets are written as the k = 0 samples go by
+//                       staging kept voxels in shared memory (12-B records at their rank, at the
+//                       output's 16-B phase) and writing each block of 32*IPT samples out with one
+//                       TMA bulk store (cp.async.bulk); chain offsets are written as the k = 0
+//                       samples go by
 // No inter-warp waiting anywhere (a single pass would need a look-back whose waits couple every
 // warp to its predecessors). Each warp walks one long contiguous range, so the per-block start-up
 // (entry search, record load, dedup carry) happens once per range, not once per block.
+// Large batches use list_fused_kernel instead: the same count and emit walks as tasks over 32x
+// finer ranges in one persistent kernel, so the FP64-bound counting and the store-bound emitting
+// share the SMs (see its comment).
 //
 // A warp walks rows of 32 consecutive samples (lane L holds sample row_start + L). Rows without an
 // entry boundary (most rows: config-4 segments are ~1000 samples long) take the fast path: one
