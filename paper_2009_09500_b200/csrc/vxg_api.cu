@@ -96,7 +96,7 @@ struct vxg_context {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // streamed bitmap readback (created on first use)
-    unsigned* h_layers = nullptr;        // mapped: finished tiles per z-layer (streamed readback)
+    unsigned* h_layers = nullptr;        // mapped: per-z-layer done flags (streamed readback)
     int64_t h_layers_cap = 0;
     bool own_stream = false;
     std::string err;
@@ -492,7 +492,7 @@ vxg_status emit_bitmap_atomic(vxg_batch* b, unsigned long long* d_words, int64_t
 // the PCIe transfer overlaps the fill instead of following it.
 struct LayerStream {
     uint64_t* host_words;
-    unsigned* counts;  // mapped, one per z-layer
+    unsigned* flags;  // mapped, one per z-layer: 1 once every tile of the layer is final
 };
 
 bool layer_stream_setup(vxg_context* ctx, int64_t ntz, LayerStream& ls) {
@@ -514,7 +514,7 @@ bool layer_stream_setup(vxg_context* ctx, int64_t ntz, LayerStream& ls) {
         ctx->h_layers_cap = ntz;
     }
     std::memset(ctx->h_layers, 0, sizeof(unsigned) * (size_t)ntz);
-    ls.counts = ctx->h_layers;
+    ls.flags = ctx->h_layers;
     return true;
 }
 
@@ -542,8 +542,15 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     g.words = d_words;
     g.ctl = ctl_slot(b, 3);
     LayerStream ls{host_words, nullptr};
-    if (host_words && !layer_stream_setup(ctx, g.ntz, ls)) ls.host_words = nullptr;
-    g.layer_done = ls.host_words ? ls.counts : nullptr;
+    DBuf layer_cnt;
+    if (host_words && (!layer_stream_setup(ctx, g.ntz, ls) ||
+                       !layer_cnt.ensure(ctx, sizeof(unsigned) * (size_t)g.ntz)))
+        ls.host_words = nullptr;
+    if (ls.host_words) {
+        cudaMemsetAsync(layer_cnt.p, 0, sizeof(unsigned) * (size_t)g.ntz, ctx->stream);
+        g.layer_cnt = layer_cnt.as<unsigned>();
+        g.layer_done = ls.flags;
+    }
     cudaEventRecord(ctx->ev[2], ctx->stream);
     cudaMemsetAsync(g.ctl, 0, sizeof(Control), ctx->stream);
     cudaMemsetAsync(g.tile_cnt, 0, sizeof(long long) * (size_t)nbins, ctx->stream);
@@ -595,7 +602,6 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     if (e != cudaSuccess) return ctx->cuda_fail(e, "tiles_fill_kernel");
     cudaError_t qe = cudaSuccess;
     if (ls.host_words) {  // copy each finished layer while the fill goes on
-        const unsigned per_layer = (unsigned)(g.ntx * g.nty);
         const int64_t plane_words = V * V / 64;
         std::vector<char> copied((size_t)g.ntz, 0);
         int64_t left = g.ntz;
@@ -604,7 +610,7 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
             bool any = false;
             for (int64_t l = 0; l < g.ntz; ++l) {
                 if (copied[(size_t)l]) continue;
-                if (!done && reinterpret_cast<volatile unsigned*>(ls.counts)[l] < per_layer) continue;
+                if (!done && reinterpret_cast<volatile unsigned*>(ls.flags)[l] == 0u) continue;
                 const int64_t za = z_lo + l * g.tz, zb = std::min<int64_t>(za + g.tz, z_hi);
                 const int64_t w0 = (za - z_lo) * plane_words;
                 cudaMemcpyAsync(ls.host_words + w0, d_words + w0, 8 * (size_t)((zb - za) * plane_words),

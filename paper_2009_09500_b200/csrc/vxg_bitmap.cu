@@ -512,6 +512,16 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, ui
 // the same bank with different words: up to 32-way conflicts on the shared atomics).
 // Work split: a warp takes 32/G pieces at a time, G lanes per piece (G from the mean piece
 // length); piece entries run two steps ahead, their records are prefetched one step ahead.
+// Streamed readback: count a finished tile of z-layer tzi on the device; the tile that completes
+// the layer raises the layer's flag in mapped host memory (one plain store per layer, after a
+// system fence: the host then copies the layer while the fill goes on).
+__device__ __forceinline__ void layer_tile_done(const TileArgs& g, long long tzi) {
+    if (atomicAdd(g.layer_cnt + tzi, 1u) + 1u == (unsigned)(g.ntx * g.nty)) {
+        __threadfence_system();
+        *reinterpret_cast<volatile unsigned*>(g.layer_done + tzi) = 1u;
+    }
+}
+
 template <int NW, int G, bool STREAM>
 __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
     extern __shared__ __align__(16) uint32_t bits[];
@@ -531,7 +541,7 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         const long long p0 = __ldg(g.tile_off + tile * kLenClasses),
                         p1 = __ldg(g.tile_off + (tile + 1) * kLenClasses);
         if (p0 == p1) {  // no samples: the bitmap keeps its words
-            if (STREAM && tid == 0) atomicAdd_system(g.layer_done + tile / (g.ntx * g.nty), 1u);
+            if (STREAM && tid == 0) layer_tile_done(g, tile / (g.ntx * g.nty));
             continue;
         }
         const long long txi = tile % g.ntx, tyi = (tile / g.ntx) % g.nty, tzi = tile / (g.ntx * g.nty);
@@ -596,7 +606,7 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         if (STREAM) {  // streamed readback: this tile's words are final
             __threadfence();
             __syncthreads();
-            if (tid == 0) atomicAdd_system(g.layer_done + tzi, 1u);
+            if (tid == 0) layer_tile_done(g, tzi);
         }
     }
 }

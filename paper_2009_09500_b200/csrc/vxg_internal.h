@@ -78,7 +78,8 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     Control* ctl;                     // total: in-volume samples, n_entries: pieces
     int* perm;                        // walk order (segments grouped by length) or null
     long long* perm_cur;              // tile_perm_keys(): bucket counts, then cursors (zeroed)
-    unsigned* layer_done;             // fill: finished tiles per z-layer (mapped host memory) or null
+    unsigned* layer_cnt;              // fill (streamed readback): finished tiles per z-layer
+    unsigned* layer_done;             // ... and per-layer done flags in mapped host memory, or null
 };
 
 struct ClipArgs {
