@@ -814,8 +814,10 @@ bool single_chain(vxg_context* ctx, const vxg_segment* seg, vxg_voxel* out, int6
     // dispatch bound on N + 1 from the endpoints (the kernel recomputes N exactly and refuses,
     // writing nothing, if the bound was wrong)
     const double dx = seg->ex - seg->sx, dy = seg->ey - seg->sy, dz = seg->ez - seg->sz;
+    // N = max(floor(len), ceil(max|d|), 1) and max|d| <= len, so N + 1 <= len + 2 (+ slack for
+    // this host-side len differing from the kernel's in the last place)
     const double ext = std::max(std::fabs(dx), std::max(std::fabs(dy), std::fabs(dz)));
-    const double bound = std::sqrt(dx * dx + dy * dy + dz * dz) + ext + 4.0;
+    const double bound = std::max(std::sqrt(dx * dx + dy * dy + dz * dz), ext) + 4.0;
     if (!(bound < (double)kSingleMaxSamples)) return false;  // long, or non-finite: batch path
     if (!ctx->h_single) {
         void* p = nullptr;
