@@ -157,7 +157,7 @@ VXG_API vxg_status vxg_batch_emit_list(vxg_batch* b, vxg_voxel* out, int64_t out
  * Samples outside [0,V)^3 are skipped and counted in *outside (may be NULL). `words` holds
  * V*V*(z_hi-z_lo)/64 uint64 (rounded up) and is OR-ed into (caller zeroes it).
  * V % 128 == 0 (and every N_i < 2^31): the tile-binned path -- segments are walked through
- * 256x80x80-voxel tiles (clipped to the slab on the device, the z-slab partitioner), their
+ * 128x120x120-voxel tiles (clipped to the slab on the device, the z-slab partitioner), their
  * in-tile k-ranges binned, every tile filled in shared memory and OR-ed into `words` once.
  * Other volumes: one global atomic per sample; VXG_BITMAP_CLIP then clips every segment's
  * k-range to the slab first (work proportional to the slab's samples), without it every sample

@@ -428,8 +428,11 @@ __global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
 // the same bank with different words: up to 32-way conflicts on the shared atomics).
 // Work split: a warp takes 32/G pieces at a time, G lanes per piece (G from the mean piece
 // length: short pieces would leave most of a full warp idle).
-// Tile shape (voxels): a row of 256 is one 32-B sector of the bitmap; 80 x 80 rows fill ~200 KB.
-constexpr int kTX = 256, kTY = 80, kTZ = 80;
+// 128 x 120 x 120 voxels (225.5 KB with the padding): near-cubic, so a segment crosses ~14
+// tile faces instead of the ~17 of a 256 x 80 x 80 tile -- fewer pieces to bin and to fill
+// (cfg5: binning 38.4 -> 32.6 ms, fill 86.7 -> 83.1 ms; 128 x 112 x 112 and 256 x 88 x 80 were
+// in between). A row is 16 B of the bitmap, each tile's own (x0 is a multiple of 128).
+constexpr int kTX = 128, kTY = 120, kTZ = 120;
 constexpr int kRW = kTX / 32;          // 32-bit words per row
 constexpr int kSS = kRW * kTY + 1;     // words per z-slice (padded by one: bank skew per z step)
 constexpr int kTileWords = kSS * kTZ;
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         const int xw = (int)min((unsigned long long)kTX, V - x0) / 64;  // words inside the volume
         constexpr int kRows = kTY * kTZ;
         constexpr int kBatch = 4;  // rows per thread in flight
-        for (int half = 0; half < 2; ++half) {  // 16-B pairs 0 and 1 of every row
+        for (int half = 0; half < kRW / 4; ++half) {  // the row's 16-B chunks
             for (int r0 = tid; r0 < kRows; r0 += kBatch * NW * 32) {
                 ulonglong2 cur[kBatch];
                 unsigned long long wa[kBatch], wb[kBatch];
