@@ -666,10 +666,12 @@ static cudaError_t launch_fill_g(const TileArgs& g, int num_sms, cudaStream_t s)
 
 // mean_len: mean samples per piece -> lanes per piece (VXG_FILL_G overrides: 4, 8, 16 or 32)
 cudaError_t launch_tiles_fill(const TileArgs& g, int num_sms, double mean_len, cudaStream_t s) {
-    // (measured with length-class bins: G = 4 is best for the config-3 (28) and config-5 (70)
-    // means, profiles/r1_fill_G)
-    int G = mean_len < 160.0 ? 4 : (mean_len < 320.0 ? 16 : 32);
+    // (measured with length-class bins and 128x120x120 tiles: G = 2 is best for the config-3
+    // and config-5 piece lengths -- cfg5 fill 79.7 ms against 83.4 (G = 4), 83.6 (G = 1), 93.5
+    // (G = 8); profiles/r1_fill_G for the earlier 256x80x80 sweep)
+    int G = mean_len < 160.0 ? 2 : (mean_len < 320.0 ? 16 : 32);
     if (const char* e = getenv("VXG_FILL_G")) G = atoi(e);
+    if (G == 2) return launch_fill_g<2>(g, num_sms, s);
     if (G == 4) return launch_fill_g<4>(g, num_sms, s);
     if (G == 8) return launch_fill_g<8>(g, num_sms, s);
     if (G == 16) return launch_fill_g<16>(g, num_sms, s);
