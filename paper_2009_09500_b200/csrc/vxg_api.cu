@@ -554,6 +554,12 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     cudaEventRecord(ctx->ev[2], ctx->stream);
     cudaMemsetAsync(g.ctl, 0, sizeof(Control), ctx->stream);
     cudaMemsetAsync(g.tile_cnt, 0, sizeof(long long) * (size_t)nbins, ctx->stream);
+    DBuf scan_status;  // the bin scan's look-back words
+    const int scan_tiles = vxg::tile_scan_tiles(nbins);
+    if (scan_status.ensure(ctx, sizeof(unsigned long long) * (size_t)scan_tiles)) {
+        cudaMemsetAsync(scan_status.p, 0, sizeof(unsigned long long) * (size_t)scan_tiles, ctx->stream);
+        g.scan_status = scan_status.as<unsigned long long>();
+    }
     // walk order grouped by segment length (pays off when lengths vary: long batches only)
     // (a thin z-slab -- one rank of many -- walks little of each segment: not worth the sort)
     if (b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256 && 2 * (z_hi - z_lo) >= V) {

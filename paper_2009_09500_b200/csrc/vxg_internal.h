@@ -78,6 +78,7 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     Control* ctl;                     // total: in-volume samples, n_entries: pieces
     int* perm;                        // walk order (segments grouped by length) or null
     long long* perm_cur;              // tile_perm_keys(): bucket counts, then cursors (zeroed)
+    unsigned long long* scan_status;  // bin scan: look-back words, one per 4096 bins (zeroed)
     unsigned* layer_cnt;              // fill (streamed readback): finished tiles per z-layer
     unsigned* layer_done;             // ... and per-layer done flags in mapped host memory, or null
 };
@@ -126,7 +127,8 @@ int tile_len_classes();  // piece bins per tile (length classes)
 int tile_perm_keys();    // walk-order buckets (length x coarse cell)
 void launch_tiles_perm(const TileArgs& g, cudaStream_t s);  // length-grouped walk order
 void launch_tiles_count(const TileArgs& g, cudaStream_t s);
-void launch_tiles_scan(const TileArgs& g, cudaStream_t s);
+void launch_tiles_scan(const TileArgs& g, cudaStream_t s);  // (look-back scan if g.scan_status)
+int tile_scan_tiles(long long nbins);
 void launch_tiles_scatter(const TileArgs& g, cudaStream_t s);
 cudaError_t launch_tiles_fill(const TileArgs& g, int num_sms, double mean_len, cudaStream_t s);
 void launch_round_points(const double* p, long long n, int32_t* out, Control* ctl, cudaStream_t s);

@@ -19,38 +19,6 @@
 
 namespace vxg {
 
-// =============================================================================== block scan
-// Exclusive scan of one long long per thread over the block; returns the thread's exclusive
-// prefix and (in every thread, after the call) the block total via `total`.
-template <int BLOCK>
-__device__ __forceinline__ long long block_excl_scan(long long v, long long* s_warp,
-                                                     long long& total) {
-    constexpr int NW = BLOCK / 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    long long incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const long long t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        long long x = lane < NW ? s_warp[lane] : 0;
-        long long xi = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const long long t = __shfl_up_sync(0xffffffffu, xi, o);
-            if (lane >= o) xi += t;
-        }
-        if (lane < NW) s_warp[lane] = xi - x;
-        if (lane == 31) s_warp[NW] = xi;
-    }
-    __syncthreads();
-    total = s_warp[NW];
-    return s_warp[warp] + incl - v;
-}
-
 // =============================================================================== plan kernel
 // One tile = BLOCK*IPT segments. Segments are read striped (coalesced), the (N_i + 1) counts are
 // transposed through shared memory into a blocked arrangement for the in-order scan, and the
