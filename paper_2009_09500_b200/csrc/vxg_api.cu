@@ -562,7 +562,8 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     }
     // walk order grouped by segment length (pays off when lengths vary: long batches only)
     // (a thin z-slab -- one rank of many -- walks little of each segment: not worth the sort)
-    if (b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256 && 2 * (z_hi - z_lo) >= V) {
+    if (b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256 && 2 * (z_hi - z_lo) >= V &&
+        !std::getenv("VXG_BITMAP_NO_PERM")) {
         const size_t keys = (size_t)vxg::tile_perm_keys();
         if (!b->ent_off.ensure(ctx, sizeof(int) * (size_t)b->n + keys * sizeof(long long)))
             return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");

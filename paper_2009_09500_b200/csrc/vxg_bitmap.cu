@@ -243,12 +243,18 @@ __device__ __forceinline__ long long seg_steps(const TileArgs& g, long long i) {
     return __ldg(g.off + i + 1) - __ldg(g.off + i) - 1;
 }
 
-// Walk order: segments grouped by length (32 buckets of N / 64), so the 32 segments a warp walks
-// in lock step have similar piece counts (the warp runs as long as its longest walk).
-constexpr int kLenBuckets = 32;
+// Walk order: segments grouped by length (8 buckets of N / 256), so the 32 segments a warp walks
+// in lock step have similar piece counts (the warp runs as long as its longest walk), and by
+// coarse start cell (16^3). Swept on cfg5 (binning ms): no sort 41.5; 16^3 cells x {1, 2, 4, 8,
+// 16, 32} length buckets 41.8, 35.4, 32.6, 32.2, 32.6, 33.6; {1, 4, 8, 12, 20, 24, 32}^3
+// cells x 32 buckets 57.8, 36.2, 33.4, 33.4, -, -, 35.5.
+constexpr int kLenBucketShift = 8;
+constexpr int kLenBuckets = 2048 >> kLenBucketShift;
 constexpr int kCellsPerAxis = 16;  // coarse spatial cells (16^3) of the box
 constexpr int kPermKeys = kLenBuckets * kCellsPerAxis * kCellsPerAxis * kCellsPerAxis;
-__device__ __forceinline__ int len_bucket(long long N) { return (int)min(N >> 6, (long long)kLenBuckets - 1); }
+__device__ __forceinline__ int len_bucket(long long N) {
+    return (int)min(N >> kLenBucketShift, (long long)kLenBuckets - 1);
+}
 
 // Walk-order key: length bucket (major) then the coarse cell of round(S) (minor). Lanes of a
 // warp then walk equally long segments (the warp runs as long as its longest walk) that start
