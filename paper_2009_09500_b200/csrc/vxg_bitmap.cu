@@ -246,8 +246,8 @@ __device__ __forceinline__ long long seg_steps(const TileArgs& g, long long i) {
 // Walk order: segments grouped by length (8 buckets of N / 256), so the 32 segments a warp walks
 // in lock step have similar piece counts (the warp runs as long as its longest walk), and by
 // coarse start cell (16^3). Swept on cfg5 (binning ms): no sort 41.5; 16^3 cells x {1, 2, 4, 8,
-// 16, 32} length buckets 41.8, 35.4, 32.6, 32.2, 32.6, 33.6; {1, 4, 8, 12, 20, 24, 32}^3
-// cells x 32 buckets 57.8, 36.2, 33.4, 33.4, -, -, 35.5.
+// 16, 32} length buckets 41.8, 35.4, 32.6, 32.2, 32.6, 33.5; {1, 4, 8, 12, 32}^3 cells x 32
+// buckets 57.8, 36.2, 33.4, 33.4, 35.5; {20, 24}^3 cells x 16 buckets 32.8, 33.0.
 constexpr int kLenBucketShift = 8;
 constexpr int kLenBuckets = 2048 >> kLenBucketShift;
 constexpr int kCellsPerAxis = 16;  // coarse spatial cells (16^3) of the box
