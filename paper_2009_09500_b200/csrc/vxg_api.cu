@@ -560,18 +560,42 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
         cudaMemsetAsync(scan_status.p, 0, sizeof(unsigned long long) * (size_t)scan_tiles, ctx->stream);
         g.scan_status = scan_status.as<unsigned long long>();
     }
-    // walk order grouped by segment length (pays off when lengths vary: long batches only)
-    // (a thin z-slab -- one rank of many -- walks little of each segment: not worth the sort)
-    if (b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256 && 2 * (z_hi - z_lo) >= V &&
-        !std::getenv("VXG_BITMAP_NO_PERM")) {
+    // A thin slab (one rank's share): the passes walk only the segments that reach it.
+    const bool select = b->n >= (1 << 16) && b->n < (1ll << 31) && z_hi - z_lo < V &&
+                        !std::getenv("VXG_BITMAP_NO_SELECT");
+    // Walk order grouped by segment length and start cell (pays off when lengths vary).
+    const bool perm = b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256 &&
+                      !std::getenv("VXG_BITMAP_NO_PERM");
+    if (select || perm) {
         const size_t keys = (size_t)vxg::tile_perm_keys();
-        if (!b->ent_off.ensure(ctx, sizeof(int) * (size_t)b->n + keys * sizeof(long long)))
+        if (!b->ent_off.ensure(ctx, keys * sizeof(long long) + sizeof(unsigned long long) +
+                                        2 * sizeof(int) * (size_t)b->n))
             return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
-        g.perm_cur = b->ent_off.as<long long>();
-        g.perm = reinterpret_cast<int*>(g.perm_cur + keys);
-        cudaMemsetAsync(g.perm_cur, 0, keys * sizeof(long long), ctx->stream);
-        vxg::launch_tiles_perm(g, ctx->stream);
-        ctx->launches += 3;
+        long long* perm_cur = b->ent_off.as<long long>();
+        auto* nsel = reinterpret_cast<unsigned long long*>(perm_cur + keys);
+        int* sel = reinterpret_cast<int*>(nsel + 1);
+        int* order = sel + b->n;
+        if (select) {
+            cudaMemsetAsync(nsel, 0, sizeof(unsigned long long), ctx->stream);
+            vxg::launch_slab_select(g, sel, nsel, ctx->stream);
+            ctx->launches++;
+            unsigned long long ns = 0;
+            cudaError_t e = cudaMemcpyAsync(ctx->h_ctl, nsel, sizeof(ns), cudaMemcpyDeviceToHost,
+                                            ctx->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+            if (e != cudaSuccess) return ctx->cuda_fail(e, "bitmap: slab selection");
+            std::memcpy(&ns, ctx->h_ctl, sizeof(ns));
+            g.sel = sel;
+            g.n = (long long)ns;
+            g.perm = sel;  // (walk order = the selection's, unless sorted below)
+        }
+        if (perm && g.n > 0) {
+            g.perm_cur = perm_cur;
+            g.perm = order;
+            cudaMemsetAsync(perm_cur, 0, keys * sizeof(long long), ctx->stream);
+            vxg::launch_tiles_perm(g, ctx->stream);
+            ctx->launches += 3;
+        }
     }
     vxg::launch_tiles_count(g, ctx->stream);
     vxg::launch_tiles_scan(g, ctx->stream);

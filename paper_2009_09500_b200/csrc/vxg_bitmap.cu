@@ -274,8 +274,9 @@ __device__ __forceinline__ int perm_key(const TileArgs& g, long long i) {
 }
 
 __global__ void __launch_bounds__(256) perm_hist_kernel(TileArgs g) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= g.n) return;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.n) return;
+    const long long i = g.sel ? (long long)g.sel[t] : t;  // (over a thin slab's selection)
     const int k = perm_key(g, i);
     // warp-aggregated: lanes with the same key add once
     const unsigned peers = __match_any_sync(__activemask(), k);
@@ -286,8 +287,9 @@ __global__ void __launch_bounds__(256) perm_hist_kernel(TileArgs g) {
 
 // perm_cur[key] holds the bucket start on entry (perm_scan_kernel): positions by atomics.
 __global__ void __launch_bounds__(256) perm_scatter_kernel(TileArgs g) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= g.n) return;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.n) return;
+    const long long i = g.sel ? (long long)g.sel[t] : t;
     const int k = perm_key(g, i);
     const unsigned peers = __match_any_sync(__activemask(), k);
     const int leader = __ffs(peers) - 1;
@@ -339,6 +341,60 @@ __global__ void __launch_bounds__(1024) perm_scan_kernel(TileArgs g) {
 
 __device__ __forceinline__ long long walk_segment(const TileArgs& g, long long t) {
     return g.perm ? (long long)__ldg(g.perm + t) : t;
+}
+
+// Thin z-slabs (one rank's share): the segments whose samples can reach [z_lo, z_hi), appended
+// to a list the count and scatter passes walk instead of every segment. The k < N samples' z is
+// monotone between samples 0 and N-1, and E is the last sample, so the test is exact. A skipped
+// segment still adds its in-volume samples to the outside count (Control::total), as the count
+// pass would have (the same arithmetic as walk_pieces; the common fully-inside case is cheap).
+__global__ void __launch_bounds__(256) slab_select_kernel(TileArgs g, int* sel,
+                                                          unsigned long long* nsel) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool keep = false;
+    long long inside = 0;
+    if (i < g.n) {
+        const SegRec r = load_rec(g.rec + i);
+        const long long N = seg_steps(g, i), nl = N > 0 ? N - 1 : 0;
+        const long long z0 = axis_round(r.sz, r.wz, 0), zl = axis_round(r.sz, r.wz, nl);
+        const long long lo = min(z0, zl), hi = max(z0, zl);
+        keep = (hi >= g.z_lo && lo < g.z_hi) || (r.ez >= g.z_lo && r.ez < g.z_hi) ||
+               (r.flags & (REC_CHECK | REC_WIDE));  // (caller plans: keep, the walk decides)
+        if (!keep) {
+            const bool e_vol = r.ex >= 0 && r.ex < g.V && r.ey >= 0 && r.ey < g.V && r.ez >= 0 &&
+                               r.ez < g.V;
+            const long long s0x = axis_round(r.sx, r.wx, 0), s0y = axis_round(r.sy, r.wy, 0);
+            const long long slx = axis_round(r.sx, r.wx, nl), sly = axis_round(r.sy, r.wy, nl);
+            const bool s_vol = s0x >= 0 && s0x < g.V && s0y >= 0 && s0y < g.V && z0 >= 0 && z0 < g.V;
+            const bool l_vol = slx >= 0 && slx < g.V && sly >= 0 && sly < g.V && zl >= 0 && zl < g.V;
+            if (s_vol && l_vol && e_vol) {
+                inside = N + 1;
+            } else {
+                const double invx = r.wx != 0.0 ? 1.0 / r.wx : 0.0;
+                const double invy = r.wy != 0.0 ? 1.0 / r.wy : 0.0;
+                const double invz = r.wz != 0.0 ? 1.0 / r.wz : 0.0;
+                long long ax0, ax1, ay0, ay1, v0, v1;
+                axis_range(r.sx, r.wx, invx, N, 0, g.V, ax0, ax1);
+                axis_range(r.sy, r.wy, invy, N, 0, g.V, ay0, ay1);
+                const long long klo = max(ax0, ay0), khi = min(ax1, ay1);
+                if (klo < khi) {
+                    axis_range(r.sz, r.wz, invz, N, 0, g.V, v0, v1);
+                    inside = max(0ll, min(khi, v1) - max(klo, v0));
+                }
+                if (e_vol) ++inside;
+            }
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const int lane = threadIdx.x & 31;
+    unsigned base = 0;
+    if (lane == 0 && m) base = (unsigned)atomicAdd(nsel, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) sel[base + __popc(m & ((1u << lane) - 1u))] = (int)i;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) inside += __shfl_xor_sync(0xffffffffu, inside, o);
+    if (lane == 0 && inside)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g.ctl->total), (unsigned long long)inside);
 }
 
 // Pass A: pieces per tile, in-volume samples.
@@ -685,7 +741,12 @@ void launch_tiles_perm(const TileArgs& g, cudaStream_t s) {
     perm_scatter_kernel<<<grid, 256, 0, s>>>(g);
 }
 
+void launch_slab_select(const TileArgs& g, int* sel, unsigned long long* nsel, cudaStream_t s) {
+    slab_select_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(g, sel, nsel);
+}
+
 void launch_tiles_count(const TileArgs& g, cudaStream_t s) {
+    if (g.n <= 0) return;  // (a slab no segment reaches)
     tiles_count_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(g);
 }
 int tile_scan_tiles(long long nbins) { return (int)((nbins + kScanTile - 1) / kScanTile); }
@@ -696,6 +757,7 @@ void launch_tiles_scan(const TileArgs& g, cudaStream_t s) {
         tiles_scan_kernel<<<1, 1024, 0, s>>>(g);
 }
 void launch_tiles_scatter(const TileArgs& g, cudaStream_t s) {
+    if (g.n <= 0) return;
     tiles_scatter_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(g);
 }
 template <int G, bool STREAM>

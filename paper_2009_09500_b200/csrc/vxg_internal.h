@@ -77,6 +77,7 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     unsigned long long* words;        // the slab's bitmap (OR-ed into)
     Control* ctl;                     // total: in-volume samples, n_entries: pieces
     int* perm;                        // walk order (segments grouped by length) or null
+    const int* sel;                   // thin slab: the segments reaching it (g.n of them) or null
     long long* perm_cur;              // tile_perm_keys(): bucket counts, then cursors (zeroed)
     unsigned long long* scan_status;  // bin scan: look-back words, one per 4096 bins (zeroed)
     unsigned* layer_cnt;              // fill (streamed readback): finished tiles per z-layer
@@ -127,6 +128,7 @@ int tile_len_classes();  // piece bins per tile (length classes)
 int tile_perm_keys();    // walk-order buckets (length x coarse cell)
 void launch_tiles_perm(const TileArgs& g, cudaStream_t s);  // length-grouped walk order
 void launch_tiles_count(const TileArgs& g, cudaStream_t s);
+void launch_slab_select(const TileArgs& g, int* sel, unsigned long long* nsel, cudaStream_t s);
 void launch_tiles_scan(const TileArgs& g, cudaStream_t s);  // (look-back scan if g.scan_status)
 int tile_scan_tiles(long long nbins);
 void launch_tiles_scatter(const TileArgs& g, cudaStream_t s);
