@@ -217,6 +217,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--segments", type=int, default=0, help="override the segment count")
+    ap.add_argument("--equal-slabs", action="store_true",
+                    help="bitmap slabs of equal depth instead of equal sample counts")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: ranks may share one GPU (functional test of the N > 1 path)")
     args = ap.parse_args()
@@ -253,9 +255,19 @@ def main():
     ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, cfg["len_fixed"], cfg["len_max"],
                                        cfg["V"], seed, d_segs.data_ptr(), 1))
     V = cfg["V"]
+    slab_cuts = None
     if kind == "slab":  # the z-slab partitioner: rank r owns one slab
-        from paper_2009_09500_b200.shard import slab_bounds
-        z_lo, z_hi = slab_bounds(V, world, rank)
+        from paper_2009_09500_b200.shard import sample_balanced_slabs, slab_bounds
+        if world > 1 and not args.equal_slabs:
+            # equal sample counts (the work), from the batch itself: decided once, before timing
+            bb = vx.Batch(None, ctx=ctx, device_ptr=d_segs.data_ptr(), n=n)
+            slabs = sample_balanced_slabs(bb.slab_samples, V, world)
+            bb.close()
+            z_lo, z_hi = slabs[rank]
+            slab_cuts = "sample-balanced (64 coarse bins)"
+        else:
+            z_lo, z_hi = slab_bounds(V, world, rank)
+            slab_cuts = "equal depth"
     else:
         z_lo, z_hi = 0, V
 
@@ -365,6 +377,7 @@ def main():
             "larger than L2)" if n * 48 > L2_BYTES else "synthetic (SplitMix64 volume generator)",
             "config": {"workload": args.workload, "desc": cfg["desc"], "segments_per_rank": n,
                        "volume": V, "z_slab": [z_lo, z_hi] if kind == "slab" else None,
+                       "slab_cuts": slab_cuts,
                        "l2": "inputs+outputs larger than L2 (no flush needed)"
                        if alg_bytes > 2 * L2_BYTES else "L2-resident working set",
                        "parallelism": f"{cfg['scaling']}-sharded x{world}"},

@@ -6,8 +6,9 @@ The path shards without a data-path collective:
 * voxel lists (configs 1, 4): chains never interact (src/batch.cpp:139-142), so each rank owns a
   contiguous segment range; `sample_balanced_cuts` cuts the offsets scan at k * total / world so
   ranks get equal sample counts (the work), not equal segment counts;
-* bitmaps (configs 3, 5): each rank owns the z-slab `slab_bounds(V, world, rank)`; the device
-  walk clips every segment to its slab (vxg_bitmap.cu), slabs are disjoint, no reduction.
+* bitmaps (configs 3, 5): each rank owns one z-slab -- `sample_balanced_slabs` (equal sample
+  counts; bench.py's default) or `slab_bounds(V, world, rank)` (equal depths); the device walk
+  clips every segment to its slab (vxg_bitmap.cu), slabs are disjoint, no reduction.
 
 The collectives here are for verification and reporting only: `gather_bitmap` / `gather_list`
 reassemble the full result on every rank, `max_over_ranks` / `sum_over_ranks` reduce scalars
@@ -24,6 +25,29 @@ def slab_bounds(V: int, world: int, rank: int) -> tuple[int, int]:
     if not (0 <= rank < world):
         raise ValueError(f"rank {rank} outside world {world}")
     return rank * V // world, (rank + 1) * V // world
+
+
+def sample_balanced_slabs(samples_in, V: int, world: int, bins: int = 64) -> list[tuple[int, int]]:
+    """z-slabs [z_lo, z_hi) covering [0, V) with (nearly) equal sample counts -- the work of a
+    rank's bitmap passes -- instead of equal depths: segments fitted into a volume are denser in
+    its middle. `samples_in(z0, z1)` counts the samples whose rounded z lies in [z0, z1)
+    (Batch.slab_samples); the cuts interpolate linearly inside `bins` equal-depth bins."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    edges = [i * V // bins for i in range(bins + 1)]
+    counts = np.array([samples_in(edges[i], edges[i + 1]) for i in range(bins)], dtype=np.float64)
+    cum = np.concatenate([[0.0], np.cumsum(counts)])
+    total = cum[-1]
+    cuts = [0]
+    for r in range(1, world):
+        target = total * r / world
+        b = int(np.searchsorted(cum, target, side="right")) - 1
+        b = min(max(b, 0), bins - 1)
+        frac = (target - cum[b]) / counts[b] if counts[b] > 0 else 0.0
+        z = int(round(edges[b] + frac * (edges[b + 1] - edges[b])))
+        cuts.append(min(max(z, cuts[-1] + 1), V - (world - r)))
+    cuts.append(V)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
 def sample_balanced_cuts(offsets: np.ndarray, world: int) -> np.ndarray:

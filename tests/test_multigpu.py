@@ -29,6 +29,28 @@ def test_slab_bounds_partition():
         shard.slab_bounds(64, 2, 2)
 
 
+def test_sample_balanced_slabs():
+    """Equal-sample z-slabs: contiguous, disjoint, covering [0, V), and balanced to within the
+    interpolation error for a density peaked in the middle of the volume (as volume-fitted
+    segments are)."""
+    from paper_2009_09500_b200.shard import sample_balanced_slabs
+    V = 4096
+    z = np.arange(V)
+    dens = np.exp(-((z - V / 2) / (V / 5)) ** 2) + 0.05
+    cum = np.concatenate([[0.0], np.cumsum(dens)])
+    samples_in = lambda a, b: cum[b] - cum[a]  # noqa: E731
+    for world in (1, 2, 3, 4, 8):
+        slabs = sample_balanced_slabs(samples_in, V, world)
+        assert slabs[0][0] == 0 and slabs[-1][1] == V
+        assert all(a < b for a, b in slabs)
+        assert all(slabs[i][1] == slabs[i + 1][0] for i in range(world - 1))
+        work = np.array([samples_in(a, b) for a, b in slabs])
+        assert work.max() / work.mean() < 1.02, (world, work)
+    eq = [(r * V // 8, (r + 1) * V // 8) for r in range(8)]
+    ew = np.array([samples_in(a, b) for a, b in eq])
+    assert ew.max() / ew.mean() > 1.5  # what equal depths would have given
+
+
 def test_sample_balanced_cuts(oracle):
     segs = oracle.gen_batch(5000, 0, 2048, 4096, 0x5EED0004)
     steps, _, off, nmax, cap = _plan(oracle, segs)
