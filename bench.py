@@ -282,8 +282,21 @@ def main():
         words = torch.zeros(nwords, dtype=torch.int64, device="cuda")
     batch.close()
 
+    # a rank's slab of the bitmap: every step filters the (broadcast) segments down to those
+    # that reach the slab on the device, then plans and bins only those
+    local = None
+    if kind == "slab" and (z_lo > 0 or z_hi < V):
+        from paper_2009_09500_b200.shard import select_slab_segments
+        local = torch.empty_like(d_segs)
+
     def step():
-        b = vx.Batch(None, ctx=ctx, device_ptr=d_segs.data_ptr(), n=n)
+        src, cnt = d_segs, n
+        if local is not None:
+            cnt = select_slab_segments(ctx, d_segs.data_ptr(), n, z_lo, z_hi, local.data_ptr())
+            src = local
+            if cnt == 0:  # (no segment reaches this slab: nothing to do)
+                return None, 0, 0, 0
+        b = vx.Batch(None, ctx=ctx, device_ptr=src.data_ptr(), n=cnt)
         if kind in ("list", "single"):
             units = b.emit_list_device(out.data_ptr(), capacity, chain.data_ptr())
         else:

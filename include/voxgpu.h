@@ -169,6 +169,14 @@ VXG_API vxg_status vxg_batch_emit_list(vxg_batch* b, vxg_voxel* out, int64_t out
 VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t V, int64_t z_lo,
                                          int64_t z_hi, int flags, int64_t* outside, vxg_mem where);
 /* Samples of the batch whose rounded z lies in [z_lo, z_hi) (the slab's work). */
+/* The z-slab partitioner's filter (multi-GPU bitmaps): copy to `out` (device)
+ * the segments of `segs` (device, n) whose samples can reach planes [z_lo, z_hi) -- a
+ * conservative test on the endpoints' z (2 planes of slack; non-finite endpoints are kept, so
+ * the plan still reports them) -- in an unspecified order; *n_out gets their count. A rank's
+ * bitmap of its slab from the filtered batch equals the slab of the full batch's bitmap. */
+VXG_API vxg_status vxg_select_slab_segments(vxg_context* ctx, const vxg_segment* segs, int64_t n,
+                                            int64_t z_lo, int64_t z_hi, vxg_segment* out,
+                                            int64_t* n_out);
 VXG_API vxg_status vxg_batch_slab_samples(vxg_batch* b, int64_t z_lo, int64_t z_hi,
                                           int64_t* samples);
 /* GPU time (ns, CUDA events) on this batch of the last plan kernel + offset scan (preprocess_ns),

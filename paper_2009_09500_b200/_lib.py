@@ -120,6 +120,7 @@ SIGNATURES = {
     "vxg_batch_emit_list": (C.c_int, [_vp, _vp, _i64, _vp, _i64p, C.c_int]),
     "vxg_batch_emit_bitmap": (C.c_int, [_vp, _vp, _i64, _i64, _i64, C.c_int, _i64p, C.c_int]),
     "vxg_batch_slab_samples": (C.c_int, [_vp, _i64, _i64, _i64p]),
+    "vxg_select_slab_segments": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64p]),
     "vxg_batch_timing": (C.c_int, [_vp, C.POINTER(vxg_timing)]),
     "vxg_run_batch": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _vp, _i64p, C.POINTER(vxg_timing)]),
     "vxg_gen_segments": (C.c_int, [_vp, _i64, _vp, _vp, _i64, _i64, _i64, C.c_uint64, _vp,

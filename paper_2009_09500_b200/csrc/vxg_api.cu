@@ -564,8 +564,10 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     const bool select = b->n >= (1 << 16) && b->n < (1ll << 31) && z_hi - z_lo < V &&
                         !std::getenv("VXG_BITMAP_NO_SELECT");
     // Walk order grouped by segment length and start cell (pays off when lengths vary).
+    // (not for slabs thinner than a quarter of the volume: there the sort costs more than it
+    // saves -- one rank of 8 on cfg5, measured)
     const bool perm = b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256 &&
-                      !std::getenv("VXG_BITMAP_NO_PERM");
+                      4 * (z_hi - z_lo) >= V && !std::getenv("VXG_BITMAP_NO_PERM");
     if (select || perm) {
         const size_t keys = (size_t)vxg::tile_perm_keys();
         if (!b->ent_off.ensure(ctx, keys * sizeof(long long) + sizeof(unsigned long long) +
@@ -1180,6 +1182,30 @@ VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t 
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     b->timing.assemble_ns = ns_since(t1);
     return e == cudaSuccess ? VXG_OK : ctx->cuda_fail(e, "bitmap readback");
+}
+
+VXG_API vxg_status vxg_select_slab_segments(vxg_context* ctx, const vxg_segment* segs, int64_t n,
+                                            int64_t z_lo, int64_t z_hi, vxg_segment* out,
+                                            int64_t* n_out) {
+    if (!ctx || !segs || !out || !n_out || n < 0) return VXG_INVALID_ARGUMENT;
+    ctx->ok();
+    cudaSetDevice(ctx->device);
+    *n_out = 0;
+    if (n == 0) return VXG_OK;
+    DBuf cnt;
+    if (!cnt.ensure(ctx, sizeof(unsigned long long)))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "select_slab_segments: out of device memory");
+    cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream);
+    vxg::launch_select_slab(reinterpret_cast<const double*>(segs), n, z_lo, z_hi,
+                            reinterpret_cast<double*>(out), cnt.as<unsigned long long>(), ctx->stream);
+    ctx->launches++;
+    unsigned long long c = 0;
+    cudaError_t e = cudaMemcpyAsync(ctx->h_ctl, cnt.p, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "select_slab_segments");
+    std::memcpy(&c, ctx->h_ctl, sizeof(c));
+    *n_out = (int64_t)c;
+    return VXG_OK;
 }
 
 VXG_API vxg_status vxg_batch_slab_samples(vxg_batch* b, int64_t z_lo, int64_t z_hi,

@@ -344,57 +344,93 @@ __device__ __forceinline__ long long walk_segment(const TileArgs& g, long long t
 }
 
 // Thin z-slabs (one rank's share): the segments whose samples can reach [z_lo, z_hi), appended
-// to a list the count and scatter passes walk instead of every segment. The k < N samples' z is
-// monotone between samples 0 and N-1, and E is the last sample, so the test is exact. A skipped
-// segment still adds its in-volume samples to the outside count (Control::total), as the count
-// pass would have (the same arithmetic as walk_pieces; the common fully-inside case is cheap).
+// to a list the count and scatter passes walk instead of every segment (a conservative test:
+// a few segments near the slab are walked for nothing). A skipped segment still adds its
+// in-volume samples to the outside count (Control::total), as the count pass would have: N + 1
+// when S and E are well inside the volume, else the same arithmetic as walk_pieces.
 __global__ void __launch_bounds__(256) slab_select_kernel(TileArgs g, int* sel,
                                                           unsigned long long* nsel) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     bool keep = false;
     long long inside = 0;
     if (i < g.n) {
-        const SegRec r = load_rec(g.rec + i);
-        const long long N = seg_steps(g, i), nl = N > 0 ? N - 1 : 0;
-        const long long z0 = axis_round(r.sz, r.wz, 0), zl = axis_round(r.sz, r.wz, nl);
-        const long long lo = min(z0, zl), hi = max(z0, zl);
-        keep = (hi >= g.z_lo && lo < g.z_hi) || (r.ez >= g.z_lo && r.ez < g.z_hi) ||
-               (r.flags & (REC_CHECK | REC_WIDE));  // (caller plans: keep, the walk decides)
+        // S and E only (no rounding): every sample lies between them (k < N: S + W*k with
+        // |W*k| <= |E - S|, up to a few ulp) or is E itself, so its rounded z is within 1 of
+        // [min(S.z, E.z), max(S.z, E.z)]; 2 planes of slack make the test conservative.
+        const SegRec* p = g.rec + i;
+        const double2 a = __ldg(reinterpret_cast<const double2*>(p));      // sx, sy
+        const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);  // sz, wx
+        const uint4 e = __ldg(reinterpret_cast<const uint4*>(p) + 3);      // ex, ey, ez, flags
+        const double sx = a.x, sy = a.y, sz = b.x;
+        const int ex = (int)e.x, ey = (int)e.y, ez = (int)e.z;
+        const double zmin = fmin(sz, (double)ez), zmax = fmax(sz, (double)ez);
+        keep = (zmax + 2.0 >= (double)g.z_lo && zmin - 2.0 < (double)g.z_hi) ||
+               (e.w & (REC_CHECK | REC_WIDE));  // (caller plans: keep, the walk decides)
         if (!keep) {
-            const bool e_vol = r.ex >= 0 && r.ex < g.V && r.ey >= 0 && r.ey < g.V && r.ez >= 0 &&
-                               r.ez < g.V;
-            const long long s0x = axis_round(r.sx, r.wx, 0), s0y = axis_round(r.sy, r.wy, 0);
-            const long long slx = axis_round(r.sx, r.wx, nl), sly = axis_round(r.sy, r.wy, nl);
-            const bool s_vol = s0x >= 0 && s0x < g.V && s0y >= 0 && s0y < g.V && z0 >= 0 && z0 < g.V;
-            const bool l_vol = slx >= 0 && slx < g.V && sly >= 0 && sly < g.V && zl >= 0 && zl < g.V;
-            if (s_vol && l_vol && e_vol) {
-                inside = N + 1;
-            } else {
-                const double invx = r.wx != 0.0 ? 1.0 / r.wx : 0.0;
-                const double invy = r.wy != 0.0 ? 1.0 / r.wy : 0.0;
-                const double invz = r.wz != 0.0 ? 1.0 / r.wz : 0.0;
-                long long ax0, ax1, ay0, ay1, v0, v1;
-                axis_range(r.sx, r.wx, invx, N, 0, g.V, ax0, ax1);
-                axis_range(r.sy, r.wy, invy, N, 0, g.V, ay0, ay1);
-                const long long klo = max(ax0, ay0), khi = min(ax1, ay1);
-                if (klo < khi) {
-                    axis_range(r.sz, r.wz, invz, N, 0, g.V, v0, v1);
-                    inside = max(0ll, min(khi, v1) - max(klo, v0));
+            const double lo = 1.0, hi = (double)(g.V - 2);
+            const bool s_in = sx >= lo && sx <= hi && sy >= lo && sy <= hi && sz >= lo && sz <= hi;
+            const bool e_in = ex >= 1 && ex <= g.V - 2 && ey >= 1 && ey <= g.V - 2 && ez >= 1 &&
+                              ez <= g.V - 2;
+            const long long N = seg_steps(g, i);
+            if (s_in && e_in) {
+                inside = N + 1;  // every sample rounds into [0, V)^3
+            } else {  // exactly, as walk_pieces does
+                const SegRec r = load_rec(p);
+                const long long nl = N > 0 ? N - 1 : 0;
+                const bool e_vol = r.ex >= 0 && r.ex < g.V && r.ey >= 0 && r.ey < g.V &&
+                                   r.ez >= 0 && r.ez < g.V;
+                const long long s0x = axis_round(r.sx, r.wx, 0), s0y = axis_round(r.sy, r.wy, 0),
+                                s0z = axis_round(r.sz, r.wz, 0);
+                const long long slx = axis_round(r.sx, r.wx, nl), sly = axis_round(r.sy, r.wy, nl),
+                                slz = axis_round(r.sz, r.wz, nl);
+                const bool s_vol = s0x >= 0 && s0x < g.V && s0y >= 0 && s0y < g.V && s0z >= 0 &&
+                                   s0z < g.V;
+                const bool l_vol = slx >= 0 && slx < g.V && sly >= 0 && sly < g.V && slz >= 0 &&
+                                   slz < g.V;
+                if (s_vol && l_vol && e_vol) {
+                    inside = N + 1;
+                } else {
+                    const double invx = r.wx != 0.0 ? 1.0 / r.wx : 0.0;
+                    const double invy = r.wy != 0.0 ? 1.0 / r.wy : 0.0;
+                    const double invz = r.wz != 0.0 ? 1.0 / r.wz : 0.0;
+                    long long ax0, ax1, ay0, ay1, v0, v1;
+                    axis_range(r.sx, r.wx, invx, N, 0, g.V, ax0, ax1);
+                    axis_range(r.sy, r.wy, invy, N, 0, g.V, ay0, ay1);
+                    const long long klo = max(ax0, ay0), khi = min(ax1, ay1);
+                    if (klo < khi) {
+                        axis_range(r.sz, r.wz, invz, N, 0, g.V, v0, v1);
+                        inside = max(0ll, min(khi, v1) - max(klo, v0));
+                    }
+                    if (e_vol) ++inside;
                 }
-                if (e_vol) ++inside;
             }
         }
     }
+    // one list append per block (a per-warp atomic on the single counter serialises: 2M of them)
+    __shared__ unsigned s_cnt[8];
+    __shared__ unsigned s_base;
+    __shared__ unsigned long long s_inside;
     const unsigned m = __ballot_sync(0xffffffffu, keep);
-    const int lane = threadIdx.x & 31;
-    unsigned base = 0;
-    if (lane == 0 && m) base = (unsigned)atomicAdd(nsel, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (keep) sel[base + __popc(m & ((1u << lane) - 1u))] = (int)i;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_inside = 0;
+    if (lane == 0) s_cnt[warp] = __popc(m);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) inside += __shfl_xor_sync(0xffffffffu, inside, o);
-    if (lane == 0 && inside)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&g.ctl->total), (unsigned long long)inside);
+    __syncthreads();
+    if (lane == 0 && inside) atomicAdd(&s_inside, (unsigned long long)inside);
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (int w = 0; w < 8; ++w) {
+            const unsigned c = s_cnt[w];
+            s_cnt[w] = tot;
+            tot += c;
+        }
+        s_base = tot ? (unsigned)atomicAdd(nsel, (unsigned long long)tot) : 0u;
+    }
+    __syncthreads();
+    if (keep) sel[s_base + s_cnt[warp] + __popc(m & ((1u << lane) - 1u))] = (int)i;
+    if (threadIdx.x == 0 && s_inside)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g.ctl->total), s_inside);
 }
 
 // Pass A: pieces per tile, in-volume samples.
@@ -414,9 +450,19 @@ __global__ void __launch_bounds__(256) tiles_count_kernel(TileArgs g) {
         inside += __shfl_xor_sync(0xffffffffu, inside, o);
         inbox += __shfl_xor_sync(0xffffffffu, inbox, o);
     }
-    if ((threadIdx.x & 31) == 0 && inbox) atomicAdd(&g.ctl->outside, (unsigned long long)inbox);
-    if ((threadIdx.x & 31) == 0 && inside)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&g.ctl->total), (unsigned long long)inside);
+    // block totals first: a per-warp atomic on the two single counters serialises in L2
+    __shared__ unsigned long long s_sum[2];
+    if (threadIdx.x == 0) s_sum[0] = s_sum[1] = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        if (inbox) atomicAdd(&s_sum[0], (unsigned long long)inbox);
+        if (inside) atomicAdd(&s_sum[1], (unsigned long long)inside);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_sum[0]) atomicAdd(&g.ctl->outside, s_sum[0]);
+        if (s_sum[1]) atomicAdd(reinterpret_cast<unsigned long long*>(&g.ctl->total), s_sum[1]);
+    }
 }
 
 // Exclusive prefix of the (tile, class) piece counts (one CTA); tile_off[nbins] = total pieces.

@@ -129,6 +129,8 @@ int tile_perm_keys();    // walk-order buckets (length x coarse cell)
 void launch_tiles_perm(const TileArgs& g, cudaStream_t s);  // length-grouped walk order
 void launch_tiles_count(const TileArgs& g, cudaStream_t s);
 void launch_slab_select(const TileArgs& g, int* sel, unsigned long long* nsel, cudaStream_t s);
+void launch_select_slab(const double* segs, long long n, long long z_lo, long long z_hi,
+                        double* out, unsigned long long* count, cudaStream_t s);
 void launch_tiles_scan(const TileArgs& g, cudaStream_t s);  // (look-back scan if g.scan_status)
 int tile_scan_tiles(long long nbins);
 void launch_tiles_scatter(const TileArgs& g, cudaStream_t s);

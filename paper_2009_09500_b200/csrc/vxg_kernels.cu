@@ -63,14 +63,19 @@ __global__ void __launch_bounds__(BLOCK) plan_kernel(PlanArgs a) {
         }
         s_cnt[q * BLOCK + tid] = cnt;
     }
-    // N_max: warp max, one atomic per warp
+    // N_max: warp max, block max in shared memory, one global atomic per tile (a per-warp
+    // atomic on the single counter serialises in L2: 2M of them for 64M segments)
+    __shared__ unsigned long long s_max;
+    if (tid == 0) s_max = 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long t = __shfl_xor_sync(0xffffffffu, mx, o);
         mx = t > mx ? t : mx;
     }
-    if ((tid & 31) == 0 && mx) atomicMax(&a.ctl->max_steps, mx);
     __syncthreads();
+    if ((tid & 31) == 0 && mx) atomicMax(&s_max, mx);
+    __syncthreads();
+    if (tid == 0 && s_max) atomicMax(&a.ctl->max_steps, s_max);
 
     long long local[IPT];
     long long sum = 0;
@@ -298,6 +303,56 @@ __global__ void export_plans_kernel(const SegRec* __restrict__ rec, const long l
     p.wy = r.wy;
     p.wz = r.wz;
     out[i] = p;
+}
+
+// The z-slab filter (vxg_select_slab_segments): segments whose endpoints' z range, widened by 2
+// planes (every sample lies between S and E up to rounding), meets [z_lo, z_hi); one list
+// append per block.
+__global__ void __launch_bounds__(256) select_slab_kernel(const double* __restrict__ segs,
+                                                          long long n, long long z_lo,
+                                                          long long z_hi, double* __restrict__ out,
+                                                          unsigned long long* count) {
+    __shared__ unsigned s_cnt[8];
+    __shared__ unsigned long long s_base;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool keep = false;
+    double2 a0 = make_double2(0, 0), a1 = a0, a2 = a0;
+    if (i < n) {
+        const double2* p = reinterpret_cast<const double2*>(segs + 6 * i);
+        a0 = p[0];
+        a1 = p[1];
+        a2 = p[2];
+        const double sz = a1.x, ez = a2.y;
+        const double lo = fmin(sz, ez), hi = fmax(sz, ez);
+        keep = !(lo == lo && hi == hi && fabs(lo) < 1e18 && fabs(hi) < 1e18) ||  // (non-finite)
+               (hi + 2.0 >= (double)z_lo && lo - 2.0 < (double)z_hi);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s_cnt[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (int w = 0; w < 8; ++w) {
+            const unsigned c = s_cnt[w];
+            s_cnt[w] = tot;
+            tot += c;
+        }
+        s_base = tot ? atomicAdd(count, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    if (keep) {
+        double2* q = reinterpret_cast<double2*>(out + 6 * (s_base + s_cnt[warp] +
+                                                             __popc(m & ((1u << lane) - 1u))));
+        q[0] = a0;
+        q[1] = a1;
+        q[2] = a2;
+    }
+}
+
+void launch_select_slab(const double* segs, long long n, long long z_lo, long long z_hi,
+                        double* out, unsigned long long* count, cudaStream_t s) {
+    select_slab_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(segs, n, z_lo, z_hi, out, count);
 }
 
 // A plan given by the caller (batch_voxelize(const BatchPlan&)): build records, check offsets

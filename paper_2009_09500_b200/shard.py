@@ -50,6 +50,16 @@ def sample_balanced_slabs(samples_in, V: int, world: int, bins: int = 64) -> lis
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
+def select_slab_segments(ctx, segs_ptr: int, n: int, z_lo: int, z_hi: int, out_ptr: int) -> int:
+    """Device-side filter of the z-slab partitioner: copy to `out_ptr` (device, room for n) the
+    segments of `segs_ptr` (device) that can reach planes [z_lo, z_hi); returns their count
+    (vxg_select_slab_segments). A rank then plans and bins only its slab's segments."""
+    import ctypes as C
+    k = C.c_int64()
+    ctx.check(ctx.lib.vxg_select_slab_segments(ctx.h, segs_ptr, n, z_lo, z_hi, out_ptr, C.byref(k)))
+    return k.value
+
+
 def sample_balanced_cuts(offsets: np.ndarray, world: int) -> np.ndarray:
     """Segment cut points c_0 = 0 <= c_1 <= ... <= c_world = n for a plan's sample offsets
     (n + 1 entries, offsets[n] = capacity): rank r owns segments [c_r, c_{r+1}), whose samples

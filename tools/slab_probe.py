@@ -1,14 +1,16 @@
-"""Time every rank's share of config 5 on one GPU: the z-slab bench.py --gpus N would give rank r
-(sample-balanced by default, --equal for equal depths) over the full 64M segments,
-device-resident, CUDA events. The max over ranks is the N-GPU step time (the ranks' slabs are
-independent: no collective on the data path). Usage: python tools/slab_probe.py N [--equal]"""
+"""Time every rank's step of config 5 on one GPU -- what bench.py --gpus N runs on rank r: filter
+the 64M broadcast segments to the rank's z-slab (sample-balanced; --equal for equal depths),
+plan them, bin and fill the slab -- device-resident, CUDA events. The max over ranks estimates
+the N-GPU step time (the slabs are independent: no collective on the data path).
+Usage: python tools/slab_probe.py N [--equal]"""
 import sys
 
 import torch
 
 sys.path.insert(0, ".")
 import paper_2009_09500_b200 as vx  # noqa: E402
-from paper_2009_09500_b200.shard import sample_balanced_slabs, slab_bounds  # noqa: E402
+from paper_2009_09500_b200.shard import (sample_balanced_slabs, select_slab_segments,  # noqa: E402
+                                         slab_bounds)
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 equal = "--equal" in sys.argv
@@ -20,15 +22,20 @@ ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, 0, 2048, V, 0x5EED0105,
 bb = vx.Batch(None, ctx=ctx, device_ptr=d.data_ptr(), n=n)
 slabs = [slab_bounds(V, N, r) for r in range(N)] if equal else sample_balanced_slabs(bb.slab_samples, V, N)
 bb.close()
+local = torch.empty_like(d)
 worst = 0.0
 for r, (z0, z1) in enumerate(slabs):
     words = torch.zeros(max(V * V * (z1 - z0) // 64, 1), dtype=torch.int64, device="cuda")
     times = []
     for _ in range(3):
-        b = vx.Batch(None, ctx=ctx, device_ptr=d.data_ptr(), n=n)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        src, cnt = d, n
+        if N > 1:
+            cnt = select_slab_segments(ctx, d.data_ptr(), n, z0, z1, local.data_ptr())
+            src = local
+        b = vx.Batch(None, ctx=ctx, device_ptr=src.data_ptr(), n=cnt)
         b.emit_bitmap_device(words.data_ptr(), V, z0, z1, True)
         e1.record()
         torch.cuda.synchronize()
@@ -36,6 +43,6 @@ for r, (z0, z1) in enumerate(slabs):
         b.close()
     t = min(times[1:])
     worst = max(worst, t)
-    print(f"N={N} rank {r}: slab [{z0}, {z1}) {t:.2f} ms")
+    print(f"N={N} rank {r}: slab [{z0}, {z1}) {t:.2f} ms (segments {cnt})")
     del words
 print(f"N={N} {'equal' if equal else 'balanced'}: max over ranks {worst:.2f} ms")
