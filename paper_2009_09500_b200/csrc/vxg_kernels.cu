@@ -324,8 +324,10 @@ __global__ void __launch_bounds__(256) select_slab_kernel(const double* __restri
         a2 = p[2];
         const double sz = a1.x, ez = a2.y;
         const double lo = fmin(sz, ez), hi = fmax(sz, ez);
-        keep = !(lo == lo && hi == hi && fabs(lo) < 1e18 && fabs(hi) < 1e18) ||  // (non-finite)
-               (hi + 2.0 >= (double)z_lo && lo - 2.0 < (double)z_hi);
+        // any non-finite coordinate: keep it (the plan reports it, as on every rank)
+        const bool finite = isfinite(a0.x) && isfinite(a0.y) && isfinite(a1.x) &&
+                            isfinite(a1.y) && isfinite(a2.x) && isfinite(a2.y);
+        keep = !finite || (hi + 2.0 >= (double)z_lo && lo - 2.0 < (double)z_hi);
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

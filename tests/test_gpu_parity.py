@@ -369,6 +369,37 @@ def test_bitmap_streamed_readback(vx, oracle, monkeypatch, V, slab):
     far.close()
 
 
+def test_select_slab_segments(vx, oracle):
+    """The z-slab partitioner's device filter (vxg_select_slab_segments): a rank's slab of the
+    bitmap from its filtered segments equals that slab of the full batch's bitmap (and the slab's
+    sample count); segments with non-finite endpoints are kept for the plan to report."""
+    import torch
+    from paper_2009_09500_b200.shard import select_slab_segments
+    V = 1024
+    segs = np.concatenate([vx.gen_segments(20000, 0, 700, V, 91),
+                           oracle.gen_batch(2000, 0, 300, 0, 92) * 3.0 - 200.0])
+    d = torch.from_numpy(segs).cuda()
+    local = torch.empty_like(d)
+    ctx = vx.default_context()
+    full = vx.Batch(None, device_ptr=d.data_ptr(), n=d.shape[0])
+    for z0, z1 in [(0, 100), (300, 700), (1000, 1024), (512, 513)]:
+        k = select_slab_segments(ctx, d.data_ptr(), d.shape[0], z0, z1, local.data_ptr())
+        assert 0 < k < d.shape[0]
+        nw = V * V * (z1 - z0) // 64
+        w_full = torch.zeros(nw, dtype=torch.int64, device="cuda")
+        w_sel = torch.zeros(nw, dtype=torch.int64, device="cuda")
+        full.emit_bitmap_device(w_full.data_ptr(), V, z0, z1, True)
+        part = vx.Batch(None, device_ptr=local.data_ptr(), n=k)
+        part.emit_bitmap_device(w_sel.data_ptr(), V, z0, z1, True)
+        assert torch.equal(w_full, w_sel), (z0, z1)
+        assert part.slab_samples(z0, z1) == full.slab_samples(z0, z1)
+        part.close()
+    full.close()
+    bad = torch.from_numpy(np.array([[0.0, 0.0, np.nan, 1, 1, 1], [0, 0, 0, 1, 1, 1.0]])).cuda()
+    out = torch.empty_like(bad)
+    assert select_slab_segments(ctx, bad.data_ptr(), 2, 500, 600, out.data_ptr()) == 1
+
+
 def test_bitmap_overwrite_discards_prior_words(vx, oracle):
     """VXG_BITMAP_OVERWRITE zeroes the words on the device: garbage in the caller's buffer
     (host or device) does not survive, on the tile path and on a slab."""
