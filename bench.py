@@ -21,6 +21,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
@@ -62,61 +63,103 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and throttle reasons sampled every ~5 ms during the timed region: NVML polled
+    from a thread in this process (nvidia-ml-py), else `nvidia-smi -lms` line-buffered through
+    stdbuf. (A plain nvidia-smi pipe is block-buffered: a short timed region can end before its
+    first line arrives.)"""
 
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
     FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
+        self.samples: list[tuple[float, float, frozenset]] = []  # (sm MHz, max MHz, reasons)
         self.proc = None
-        self.lines: list[str] = []
+        self.stop = threading.Event()
+        self.t = None
+        self.error = None
+        self.source = None
+
+    def _nvml_loop(self, nv, h):
+        bits = [(name, getattr(nv, attr, 0)) for name, attr in self.REASONS]
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((float(sm), float(mx),
+                                     frozenset(n for n, b in bits if b and (r & b))))
+            except Exception as e:  # (reported once in the summary)
+                self.error = self.error or repr(e)
+            self.stop.wait(0.005)
+
+    def _smi_loop(self):
+        names = [n for n, _ in self.REASONS]
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                self.samples.append((float(parts[1]), float(parts[2]), frozenset(
+                    n for n, v in zip(names, parts[3:7]) if v.lower() == "active")))
+            except ValueError:
+                continue
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-i", str(self.gpu), "-lms", "25"], stdout=subprocess.PIPE,
-                stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.t = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.source = "nvml"
+        except Exception as e:
+            self.error = repr(e)
+            try:
+                cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                       "-i", str(self.gpu), "-lms", "25"]
+                if shutil.which("stdbuf"):
+                    cmd = ["stdbuf", "-oL"] + cmd
+                self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                             stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._smi_loop, daemon=True)
+                self.source = "nvidia-smi"
+            except Exception as e:
+                self.error = (self.error or "") + " / " + repr(e)
+                self.t = None
+        if self.t:
             self.t.start()
-        except Exception:
-            self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc:
-            time.sleep(0.25)
+            time.sleep(0.1)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[3:7]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "source": self.source, "error": self.error}
+        reasons = set()
+        for _, _, r in self.samples:
+            reasons |= r
+        return {"sm_mhz": statistics.median(x[0] for x in self.samples),
+                "sm_max_mhz": max(x[1] for x in self.samples), "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": self.source}
 
 
 def dist_setup(args):
@@ -284,16 +327,16 @@ def main():
 
     # a rank's slab of the bitmap: every step filters the (broadcast) segments down to those
     # that reach the slab on the device, then plans and bins only those
-    local = None
+    slab_segs = None
     if kind == "slab" and (z_lo > 0 or z_hi < V):
         from paper_2009_09500_b200.shard import select_slab_segments
-        local = torch.empty_like(d_segs)
+        slab_segs = torch.empty_like(d_segs)
 
     def step():
         src, cnt = d_segs, n
-        if local is not None:
-            cnt = select_slab_segments(ctx, d_segs.data_ptr(), n, z_lo, z_hi, local.data_ptr())
-            src = local
+        if slab_segs is not None:
+            cnt = select_slab_segments(ctx, d_segs.data_ptr(), n, z_lo, z_hi, slab_segs.data_ptr())
+            src = slab_segs
             if cnt == 0:  # (no segment reaches this slab: nothing to do)
                 return None, 0, 0, 0
         b = vx.Batch(None, ctx=ctx, device_ptr=src.data_ptr(), n=cnt)

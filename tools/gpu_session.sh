@@ -10,7 +10,7 @@ nproc > $out/nproc.txt; lscpu > $out/lscpu.txt 2>&1
 timeout 900 python -m pytest tests -x -q -m gpu > $out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1; echo "smoke rc=$?" >> $out/smoke.log
 for w in cfg4 cfg1 cfg3 cfg5 cfg2; do
-  timeout 900 python bench.py --workload $w --steps 5 --warmup 3 > $out/bench_$w.json 2> $out/bench_$w.err
+  timeout 900 python bench.py --workload $w --steps 20 --warmup 3 > $out/bench_$w.json 2> $out/bench_$w.err
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_reference_cfg4.json 2> $out/bench_reference.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
