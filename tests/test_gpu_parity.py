@@ -400,6 +400,22 @@ def test_select_slab_segments(vx, oracle):
     assert select_slab_segments(ctx, bad.data_ptr(), 2, 500, 600, out.data_ptr()) == 1
 
 
+def test_sample_balanced_slabs_on_device(vx):
+    """The bench's z-slab partition from Batch.slab_samples: the slabs tile [0, V), their sample
+    counts add up to the whole volume's, and each is within a few percent of the mean."""
+    from paper_2009_09500_b200.shard import sample_balanced_slabs
+    V = 1024
+    b = vx.Batch(vx.gen_segments(200000, 0, 600, V, 93))
+    total = b.slab_samples(0, V)
+    for world in (2, 3, 8):
+        slabs = sample_balanced_slabs(b.slab_samples, V, world)
+        assert slabs[0][0] == 0 and slabs[-1][1] == V
+        work = [b.slab_samples(z0, z1) for z0, z1 in slabs]
+        assert sum(work) == total
+        assert max(work) / (total / world) < 1.05, (world, work)
+    b.close()
+
+
 def test_bitmap_overwrite_discards_prior_words(vx, oracle):
     """VXG_BITMAP_OVERWRITE zeroes the words on the device: garbage in the caller's buffer
     (host or device) does not survive, on the tile path and on a slab."""
