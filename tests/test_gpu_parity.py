@@ -341,7 +341,8 @@ def test_bitmap_tiles_accumulate_and_match_atomic_path(vx, oracle, monkeypatch):
     assert np.array_equal(w_atomic, w_tiles)
 
 
-@pytest.mark.parametrize("V,slab", [(512, (0, 512)), (1024, (100, 700)), (1024, (900, 1000))])
+@pytest.mark.parametrize("V,slab", [(512, (0, 512)), (1024, (100, 700)), (1024, (900, 1000)),
+                                     (384, (0, 384)), (384, (119, 241)), (640, (7, 8))])
 def test_bitmap_streamed_readback(vx, oracle, monkeypatch, V, slab):
     """Host bitmaps (>= 64 MiB by default) through the tile path are read back layer by layer while the
     fill runs (mapped per-layer tile counters, copy stream): same words and outside count as the
@@ -349,7 +350,8 @@ def test_bitmap_streamed_readback(vx, oracle, monkeypatch, V, slab):
     empty slab still returns the caller's words."""
     z0, z1 = slab
     monkeypatch.setenv("VXG_BITMAP_STREAM_MIN", "0")  # stream every size here
-    segs = np.concatenate([vx.gen_segments(4000, 0, 500, V, 71), oracle.gen_batch(300, 0, 200, 0, 72)])
+    segs = np.concatenate([vx.gen_segments(4000, 0, min(500, V // 2), V, 71),
+                           oracle.gen_batch(300, 0, 200, 0, 72)])
     b = vx.Batch(segs)
     want, _ = oracle.bitmap(segs, V, z0, z1)
     monkeypatch.setenv("VXG_BITMAP_NO_STREAM", "1")
