@@ -353,7 +353,9 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
                                               : b->capacity >= (int64_t)warps * 4 * 4 * blk);
     static const int rpw_env = std::getenv("VXG_FUSED_RPW") ? std::atoi(std::getenv("VXG_FUSED_RPW")) : 32;
     static const double la_env = std::getenv("VXG_FUSED_LA") ? std::atof(std::getenv("VXG_FUSED_LA")) : 1.0;
-    int64_t nranges = fused ? rpw_env * warps : warps;
+    // (two-pass: 2/3 of the emit pass's resident warps, so the count pass -- kCountSplit warps per
+    // range, 4 CTAs per SM -- runs in one wave: cfg1 0.167 -> 0.162 ms)
+    int64_t nranges = fused ? rpw_env * warps : std::max<int64_t>(1, warps * 2 / 3);
     const int64_t rblk = fused ? vxg::list_fused_block_samples() : blk;
     int64_t range_len = rblk;  // deferred: the kernels scale it by the capacity they read
     if (!deferred) {
