@@ -573,14 +573,7 @@ __global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
     if (pending) g.pieces[pslot] = pp;
 }
 
-// Persistent CTAs: claim a tile, set its samples' bits in shared memory, OR it into the bitmap.
-//
-// Shared layout: a row of TX bits is TX/32 words; a z-slice of TY rows is padded by one word so
-// a step in z moves to the next bank (without the pad, samples of a segment running along z hit
-// the same bank with different words: up to 32-way conflicts on the shared atomics).
-// Work split: a warp takes 32/G pieces at a time, G lanes per piece (G from the mean piece
-// length: short pieces would leave most of a full warp idle).
-// 128 x 120 x 120 voxels (225.5 KB with the padding): near-cubic, so a segment crosses ~14
+// Tile shape: 128 x 120 x 120 voxels (225.5 KB with the padding): near-cubic, so a segment crosses ~14
 // tile faces instead of the ~17 of a 256 x 80 x 80 tile -- fewer pieces to bin and to fill
 // (cfg5: binning 38.4 -> 32.6 ms, fill 86.7 -> 83.1 ms; 128 x 112 x 112 and 256 x 88 x 80 were
 // in between). A row is 16 B of the bitmap, each tile's own (x0 is a multiple of 128).
