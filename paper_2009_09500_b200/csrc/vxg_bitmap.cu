@@ -18,6 +18,7 @@
 // Samples are evaluated exactly as the list path does (include/voxline/parametric.hpp:41-48,
 // FMA-free, llround), so the set of bits equals the set of chain voxels of the reference.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "vxg_device.cuh"
@@ -630,6 +631,7 @@ __device__ __forceinline__ void red_or_shared(uint32_t saddr, uint32_t bit) {
 template <int G>
 __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, uint32_t spare,
                                            const PieceRef& q, int gl) {
+#if VXG_FILL_UNIFORM
     int mx = q.len;
 #pragma unroll
     for (int o = G; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -646,11 +648,58 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, ui
         t = __dadd_rn(t, (double)G);
         j += G;
     }
+#else
+    (void)spare;
+    // every lane runs its own trip count: no per-sample bound test or select in the body (lanes
+    // whose piece is done idle until the warp's longest piece is); whole groups of 4 samples,
+    // then the remainder
+    double t = __ll2double_rn(q.ka + gl);
+    const int steps = q.len > gl ? (q.len - gl + G - 1) / G : 0;
+    auto one = [&]() {
+        const int32_t x = round_pos(sample_axis(q.sx, q.wx, t));
+        const int32_t y = round_pos(sample_axis(q.sy, q.wy, t));
+        const int32_t z = round_pos(sample_axis(q.sz, q.wz, t));
+        const uint32_t w = (uint32_t)(z * kSS + y * kRW + (x >> 5));
+        red_or_shared(sbase + 4u * w, 1u << (x & 31));
+        t = __dadd_rn(t, (double)G);
+    };
+    for (int st = steps >> 2; st > 0; --st) {
+        one();
+        one();
+        one();
+        one();
+    }
+    for (int st = steps & 3; st > 0; --st) one();
+    __syncwarp();
+#endif
     if (q.hasE && gl == 0) {
         const SegRec* r = g.rec + q.seg;
         const int32_t ex = __ldg(&r->ex), ey = __ldg(&r->ey), ez = __ldg(&r->ez);
         red_or_shared(sbase + 4u * (uint32_t)(ez * kSS + ey * kRW + (ex >> 5)), 1u << (ex & 31));
     }
+}
+
+// Tile claimed by fill ticket r: tiles are handed out in blocks of bx x by x bz tiles (x fastest
+// inside a block, blocks x-, then y-, then z-major; partial blocks at the far edges), so the tiles
+// in flight at any time are spatially compact and the pieces of one segment in neighbouring tiles
+// are filled close together in time (their records' second and later gathers hit L2).
+__device__ __forceinline__ long long fill_tile_of(const TileArgs& g, long long r) {
+    if (g.bx <= 0) return r;
+    const long long ntx = g.ntx, nty = g.nty, ntz = g.ntz;
+    const long long per_zl = (long long)g.bz * nty * ntx;
+    const long long z0 = r / per_zl * g.bz;
+    r %= per_zl;
+    const long long dz = min((long long)g.bz, ntz - z0);
+    const long long per_yr = (long long)g.by * ntx * dz;
+    const long long y0 = r / per_yr * g.by;
+    r %= per_yr;
+    const long long dy = min((long long)g.by, nty - y0);
+    const long long per_b = (long long)g.bx * dy * dz;
+    const long long x0 = r / per_b * g.bx;
+    r %= per_b;
+    const long long dx = min((long long)g.bx, ntx - x0);
+    const long long x = x0 + r % dx, y = y0 + (r / dx) % dy, z = z0 + r / (dx * dy);
+    return (z * nty + y) * ntx + x;
 }
 
 // Persistent CTAs: claim a tile, set its samples' bits in shared memory, OR it into the bitmap.
@@ -684,8 +733,8 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         // has read this one's)
         if (tid == 0) s_tile[it & 1] = (long long)atomicAdd(&g.ctl->tile_counter, 1ull);
         __syncthreads();  // (also orders the clearing of the previous tile's bits)
-        const long long tile = s_tile[it & 1];
-        if (tile >= g.ntiles) break;
+        if (s_tile[it & 1] >= g.ntiles) break;
+        const long long tile = fill_tile_of(g, s_tile[it & 1]);
         const long long p0 = __ldg(g.tile_off + tile * kLenClasses),
                         p1 = __ldg(g.tile_off + (tile + 1) * kLenClasses);
         if (p0 == p1) {  // no samples: the bitmap keeps its words
@@ -821,6 +870,8 @@ static cudaError_t launch_fill_g(const TileArgs& g, int num_sms, cudaStream_t s)
     return g.layer_done ? launch_fill_gs<G, true>(g, num_sms, s) : launch_fill_gs<G, false>(g, num_sms, s);
 }
 
+static cudaError_t launch_tiles_fill_g(const TileArgs& g, int num_sms, int G, cudaStream_t s);
+
 // mean_len: mean samples per piece -> lanes per piece (VXG_FILL_G overrides: 4, 8, 16 or 32)
 cudaError_t launch_tiles_fill(const TileArgs& g, int num_sms, double mean_len, cudaStream_t s) {
     // (measured with length-class bins and 128x120x120 tiles: G = 2 is best for the config-3
@@ -828,6 +879,17 @@ cudaError_t launch_tiles_fill(const TileArgs& g, int num_sms, double mean_len, c
     // (G = 8); profiles/r1_fill_G for the earlier 256x80x80 sweep)
     int G = mean_len < 160.0 ? 2 : (mean_len < 320.0 ? 16 : 32);
     if (const char* e = getenv("VXG_FILL_G")) G = atoi(e);
+    TileArgs gg = g;
+    if (const char* e = getenv("VXG_FILL_ORDER")) {  // "bx,by,bz" (experiments)
+        gg.bx = gg.by = gg.bz = 0;
+        sscanf(e, "%d,%d,%d", &gg.bx, &gg.by, &gg.bz);
+        if (gg.bx <= 0 || gg.by <= 0 || gg.bz <= 0) gg.bx = gg.by = gg.bz = 0;
+    }
+    return launch_tiles_fill_g(gg, num_sms, G, s);
+}
+
+static cudaError_t launch_tiles_fill_g(const TileArgs& g, int num_sms, int G, cudaStream_t s) {
+    if (G == 1) return launch_fill_g<1>(g, num_sms, s);
     if (G == 2) return launch_fill_g<2>(g, num_sms, s);
     if (G == 4) return launch_fill_g<4>(g, num_sms, s);
     if (G == 8) return launch_fill_g<8>(g, num_sms, s);

@@ -164,6 +164,52 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
         int nfast = 0;
         if (!(flags & (REC_CHECK | REC_WIDE)) && lim >= row_start + 32)
             nfast = (int)min((lim - row_start) >> 5, (long long)(IPT - j));
+        if (!EMIT && nfast > 0) {
+            // counting only: the run's 32 * nfast samples are split into 32 contiguous lane
+            // sub-ranges of nfast samples, so a sample's predecessor is the lane's own previous
+            // sample (a register) -- no shuffle, ballot or popc per sample; one shuffle joins
+            // the sub-ranges and one warp reduction sums the counts
+            const SegRec R = load_rec(a.rec + w.c);
+            double t = __ll2double_rn(row_start - w.so_c + (long long)lane * nfast);
+            int32_t first_key, key;
+            int cnt = 0;
+            if (flags & REC_POS) {
+                first_key = key = voxel_key(round_pos(sample_axis(R.sx, R.wx, t)),
+                                            round_pos(sample_axis(R.sy, R.wy, t)),
+                                            round_pos(sample_axis(R.sz, R.wz, t)));
+#pragma unroll 4
+                for (int f = 1; f < nfast; ++f) {
+                    t = __dadd_rn(t, 1.0);
+                    const int32_t k2 = voxel_key(round_pos(sample_axis(R.sx, R.wx, t)),
+                                                 round_pos(sample_axis(R.sy, R.wy, t)),
+                                                 round_pos(sample_axis(R.sz, R.wz, t)));
+                    cnt += k2 != key;
+                    key = k2;
+                }
+            } else {
+                first_key = key = voxel_key(round_fast(sample_axis(R.sx, R.wx, t)),
+                                            round_fast(sample_axis(R.sy, R.wy, t)),
+                                            round_fast(sample_axis(R.sz, R.wz, t)));
+#pragma unroll 2
+                for (int f = 1; f < nfast; ++f) {
+                    t = __dadd_rn(t, 1.0);
+                    const int32_t k2 = voxel_key(round_fast(sample_axis(R.sx, R.wx, t)),
+                                                 round_fast(sample_axis(R.sy, R.wy, t)),
+                                                 round_fast(sample_axis(R.sz, R.wz, t)));
+                    cnt += k2 != key;
+                    key = k2;
+                }
+            }
+            // predecessor of a lane's first sample: lane - 1's last one (lane 0: the carry);
+            // k == 0 (lane 0 of a run that starts the segment) is always kept
+            const int32_t up = __shfl_up_sync(0xffffffffu, key, 1);
+            const bool kfirst = lane == 0 && row_start == w.so_c;
+            cnt += (kfirst || first_key != (lane == 0 ? carry : up)) ? 1 : 0;
+            running += (int)__reduce_add_sync(0xffffffffu, (unsigned)cnt);
+            carry = __shfl_sync(0xffffffffu, key, 31);
+            j += nfast;
+            continue;
+        }
         if (nfast > 0) {
             const SegRec R = load_rec(a.rec + w.c);
             double t = __ll2double_rn(row_start - w.so_c + lane);

@@ -82,6 +82,7 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     unsigned long long* scan_status;  // bin scan: look-back words, one per 4096 bins (zeroed)
     unsigned* layer_cnt;              // fill (streamed readback): finished tiles per z-layer
     unsigned* layer_done;             // ... and per-layer done flags in mapped host memory, or null
+    int bx, by, bz;                   // fill: tiles claimed in blocks of bx x by x bz (0: linear)
 };
 
 struct ClipArgs {
