@@ -153,6 +153,11 @@ VXG_API vxg_status vxg_batch_work_item(vxg_batch* b, int64_t i, int64_t k, int32
  * where == VXG_MEM_DEVICE: device pointers; *total still returned (one 8-byte readback). */
 VXG_API vxg_status vxg_batch_emit_list(vxg_batch* b, vxg_voxel* out, int64_t out_cap,
                                        int64_t* chain_off, int64_t* total, vxg_mem where);
+/* BatchResult.total_voxels (src/batch.cpp:148-150) without materialising the list: the count
+ * pass of vxg_batch_emit_list (every sample evaluated, consecutive duplicates dropped) and its
+ * range prefix; one 8-byte readback. Sizes a host list exactly, and is the voxel count of a
+ * batch whose output is a bitmap. */
+VXG_API vxg_status vxg_batch_count_voxels(vxg_batch* b, int64_t* total);
 /* Occupancy bitmap of the batch's samples restricted to planes [z_lo, z_hi) of a V^3 volume.
  * Samples outside [0,V)^3 are skipped and counted in *outside (may be NULL). `words` holds
  * V*V*(z_hi-z_lo)/64 uint64 (rounded up) and is OR-ed into (caller zeroes it).

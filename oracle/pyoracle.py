@@ -86,6 +86,10 @@ class Oracle:
         L.vo_chain_lengths.argtypes = [_f64p, C.c_int64, _i64p, C.c_int]
         L.vo_bitmap.argtypes = [_f64p, C.c_int64, _u64p, C.c_int64, C.c_int64, C.c_int64, _i64p,
                                 C.c_int]
+        L.vo_bitmap_zpart.argtypes = L.vo_bitmap.argtypes
+        L.vo_check_round_pos.restype = C.c_int64
+        L.vo_check_round_pos.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_int, _i64p,
+                                         C.POINTER(C.c_double)]
         L.vo_chain_hashes.argtypes = [_f64p, C.c_int64, _u64p, _i64p, C.c_int]
         L.vo_gen_segment_of_length.argtypes = [C.c_int64, C.c_uint64, _f64p]
         L.vo_gen_segment_in_volume.argtypes = [C.c_int64, C.c_uint64, C.c_int64, _f64p]
@@ -166,16 +170,26 @@ class Oracle:
                "chain_lengths")
         return out[:n]
 
-    def bitmap(self, segs, V: int, z_lo: int = 0, z_hi: int | None = None, nthreads: int = 0):
-        """-> (uint64 words, outside count); bit b = x + V*(y + V*(z - z_lo))."""
+    def bitmap(self, segs, V: int, z_lo: int = 0, z_hi: int | None = None, nthreads: int = 0,
+               zpart: bool = False):
+        """-> (uint64 words, outside count); bit b = x + V*(y + V*(z - z_lo)).
+        zpart: the z-partitioned evaluation (vo_bitmap_zpart) for large batches."""
         s = as_segments(segs)
         z_hi = V if z_hi is None else z_hi
         nbits = V * V * (z_hi - z_lo)
         words = np.zeros((nbits + 63) // 64, np.uint64)
         outside = C.c_int64()
-        _check(self.lib.vo_bitmap(_p(s, _f64p), s.shape[0], _p(words, _u64p), V, z_lo, z_hi,
-                                  C.byref(outside), nthreads), "bitmap")
+        fn = self.lib.vo_bitmap_zpart if zpart else self.lib.vo_bitmap
+        _check(fn(_p(s, _f64p), s.shape[0], _p(words, _u64p), V, z_lo, z_hi, C.byref(outside),
+                  nthreads), "bitmap")
         return words, outside.value
+
+    def check_round_pos(self, ties: int, rnd: int, seed: int = 7, mode: int = 0):
+        """Host check of the GPU's one-DADD rounding (round_pos) against llround ->
+        (mismatches, values checked, first mismatching value); see round_pos_check.c."""
+        n, fb = C.c_int64(), C.c_double()
+        bad = self.lib.vo_check_round_pos(ties, rnd, seed, mode, C.byref(n), C.byref(fb))
+        return bad, n.value, fb.value
 
     def chain_hashes(self, segs, nthreads: int = 0):
         """-> (uint64 hash per chain, int64 length per chain); see vo_chain_hashes."""
@@ -243,6 +257,9 @@ class RefOracle:
         L.ref_read_segments_csv.argtypes = [C.c_char_p, _f64p, C.c_int64, _i64p, C.c_char_p,
                                             C.c_int64]
         L.ref_batch_write.argtypes = [_f64p, C.c_int64, C.c_char_p, C.c_int]
+        L.ref_run_batch_bitmap.argtypes = [_f64p, C.c_int64, C.c_int, C.c_int, _u64p, C.c_int64,
+                                           C.c_int64, C.c_int64, _i64p, _i64p, _i64p]
+        L.ref_sequential_map.argtypes = [_f64p, C.c_int64, _i64p]
 
     def splitmix(self, seed: int, count: int) -> list[int]:
         st = C.c_uint64(seed)
@@ -323,6 +340,30 @@ class RefOracle:
                                       total.value, _p(off, _i64p), C.byref(total),
                                       _p(timing, _i64p)), "run_batch")
         return out[: total.value], off, total.value, timing
+
+    def run_batch_bitmap(self, segs, V: int, z_lo: int = 0, z_hi: int | None = None,
+                         workers: int = 1, group_size: int = 64, words=None):
+        """The bitmap configs' CPU arm: run_batch, then the harness bit-setting pass over its
+        chains. -> (words, total_voxels, outside, (run_batch ns, bit-setting ns))."""
+        s = as_segments(segs)
+        z_hi = V if z_hi is None else z_hi
+        nwords = (V * V * (z_hi - z_lo) + 63) // 64
+        if words is None:
+            words = np.zeros(nwords, np.uint64)
+        total, outside = C.c_int64(), C.c_int64()
+        t = np.zeros(2, np.int64)
+        _check(self.lib.ref_run_batch_bitmap(_p(s, _f64p), s.shape[0], workers, group_size,
+                                             _p(words, _u64p), V, z_lo, z_hi, C.byref(total),
+                                             C.byref(outside), _p(t, _i64p)), "run_batch_bitmap")
+        return words, total.value, outside.value, (int(t[0]), int(t[1]))
+
+    def sequential_map(self, segs) -> int:
+        """src/bench.cpp:188-205: voxelize_parametric per segment on this thread -> total."""
+        s = as_segments(segs)
+        total = C.c_int64()
+        _check(self.lib.ref_sequential_map(_p(s, _f64p), s.shape[0], C.byref(total)),
+               "sequential_map")
+        return total.value
 
     def gen_segment_of_length(self, target: int, seed: int) -> np.ndarray:
         out = np.zeros(6)

@@ -6,9 +6,13 @@
 // oracle/voxline_oracle.c, (2) generate tests/golden fixtures, and (3) serve as the CPU
 // baseline ("kind": "reference") in bench.py. Exceptions are mapped to the codes in
 // oracle/voxline_oracle.h.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include <fstream>
@@ -156,6 +160,74 @@ int ref_run_batch(const double* segs, int64_t n, int workers, int group_size, in
             timing_ns[1] = r.timing.kernel_ns;
             timing_ns[2] = r.timing.assemble_ns;
         }
+    });
+}
+
+// The bitmap configs' CPU arm: the reference's own run_batch (src/batch.cpp:154-162) over the
+// segments, then the harness's bit-setting pass over its chains -- bit x + V*(y + V*(z - z_lo))
+// of 64-bit words for voxels in [0,V)^2 x [z_lo, z_hi); voxels outside [0,V)^3 are counted in
+// *outside. The pass runs on `workers` threads over contiguous chain ranges; a chain's run of
+// voxels in one word is OR-ed in with one atomic. times_ns = {run_batch, bit-setting}.
+int ref_run_batch_bitmap(const double* segs, int64_t n, int workers, int group_size,
+                         uint64_t* words, int64_t V, int64_t z_lo, int64_t z_hi, int64_t* total,
+                         int64_t* outside, int64_t* times_ns) {
+    return guarded([&] {
+        using clk = std::chrono::steady_clock;
+        const auto t0 = clk::now();
+        const voxline::BatchResult r =
+            voxline::run_batch(to_segments(segs, n), {group_size, workers});
+        const auto t1 = clk::now();
+        const std::size_t nc = r.chains.size();
+        const int nt = std::max(1, workers);
+        std::atomic<int64_t> out_total{0};
+        auto body = [&](int t) {
+            const std::size_t c0 = nc * (std::size_t)t / (std::size_t)nt;
+            const std::size_t c1 = nc * (std::size_t)(t + 1) / (std::size_t)nt;
+            int64_t out = 0;
+            for (std::size_t c = c0; c < c1; ++c) {
+                uint64_t cur_w = ~0ull, cur_b = 0;
+                for (const voxline::Voxel& v : r.chains[c].voxels) {
+                    if (v.x < 0 || v.x >= V || v.y < 0 || v.y >= V || v.z < 0 || v.z >= V) {
+                        ++out;
+                        continue;
+                    }
+                    if (v.z < z_lo || v.z >= z_hi) continue;
+                    const uint64_t b = (uint64_t)v.x +
+                                       (uint64_t)V * ((uint64_t)v.y + (uint64_t)V * (uint64_t)(v.z - z_lo));
+                    if ((b >> 6) != cur_w) {
+                        if (cur_b) __atomic_fetch_or(&words[cur_w], cur_b, __ATOMIC_RELAXED);
+                        cur_w = b >> 6;
+                        cur_b = 0;
+                    }
+                    cur_b |= 1ull << (b & 63);
+                }
+                if (cur_b) __atomic_fetch_or(&words[cur_w], cur_b, __ATOMIC_RELAXED);
+            }
+            out_total += out;
+        };
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(body, t);
+        body(0);
+        for (auto& x : th) x.join();
+        const auto t2 = clk::now();
+        *total = r.total_voxels;
+        if (outside) *outside = out_total.load();
+        if (times_ns) {
+            times_ns[0] = std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+            times_ns[1] = std::chrono::duration_cast<std::chrono::nanoseconds>(t2 - t1).count();
+        }
+    });
+}
+
+// The reference harness's sequential method (src/bench.cpp:188-205): one voxelize_parametric
+// call per segment on the calling thread; *total = the sum of chain lengths.
+int ref_sequential_map(const double* segs, int64_t n, int64_t* total) {
+    return guarded([&] {
+        const std::vector<voxline::Segment> v = to_segments(segs, n);
+        int64_t t = 0;
+        for (const voxline::Segment& seg : v)
+            t += static_cast<int64_t>(voxline::voxelize_parametric(seg).voxels.size());
+        *total = t;
     });
 }
 

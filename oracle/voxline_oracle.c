@@ -386,6 +386,159 @@ int vo_bitmap(const double* segs, int64_t n, uint64_t* bits, int64_t V, int64_t 
     return c.err;
 }
 
+/* ---- z-partitioned bitmap (large batches) ---- */
+typedef struct {
+    const double* segs;
+    int64_t* steps;
+    double* w3;
+    int32_t* zr;    /* 2 per segment: a conservative range of the samples' rounded z */
+    uint8_t* chk;   /* 1: samples may approach the int32 edge -> every sample checked */
+    uint64_t* bits;
+    int64_t n, V, z_lo, z_hi, planes, nchunks, outside, first_bad;
+    int err, plain;
+} zpart_ctx;
+
+static void zpart_plan_body(void* vctx, int64_t i) {
+    zpart_ctx* c = (zpart_ctx*)vctx;
+    const double* seg = c->segs + 6 * i;
+    const int e = vo_make_plan(seg, &c->steps[i], c->w3 + 3 * i);
+    if (e) {
+        record_error(&c->first_bad, &c->err, i, e);
+        return;
+    }
+    double lo = seg[2] < seg[5] ? seg[2] : seg[5], hi = seg[2] < seg[5] ? seg[5] : seg[2];
+    double m = 0.0;
+    for (int a = 0; a < 6; ++a) m = fabs(seg[a]) > m ? fabs(seg[a]) : m;
+    c->chk[i] = m > 2147483000.0;
+    /* every sample k < N lies between S.z and E.z up to a few ulp; E is E */
+    c->zr[2 * i] = c->chk[i] ? INT32_MIN : (int32_t)floor(lo) - 2;
+    c->zr[2 * i + 1] = c->chk[i] ? INT32_MAX : (int32_t)ceil(hi) + 2;
+}
+
+/* first k in [lo, hi) whose rounded z is >= B (up) or < B (!up); hi if none (monotone pred) */
+static int64_t z_cross(const double* seg, const double* w, int64_t lo, int64_t hi, int64_t B,
+                       int up) {
+    while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        int32_t z;
+        round_component(seg[2] + w[2] * (double)mid, &z);
+        if (up ? (z >= B) : (z < B)) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+static inline void zpart_set(zpart_ctx* c, const int32_t v[3], int64_t* outside, int plain) {
+    const int64_t V = c->V;
+    if (v[0] < 0 || v[0] >= V || v[1] < 0 || v[1] >= V || v[2] < 0 || v[2] >= V) {
+        ++*outside;
+        return;
+    }
+    if (v[2] < c->z_lo || v[2] >= c->z_hi) return;
+    const uint64_t b = (uint64_t)v[0] + (uint64_t)V * ((uint64_t)v[1] + (uint64_t)V * (uint64_t)(v[2] - c->z_lo));
+    if (plain) c->bits[b >> 6] |= 1ULL << (b & 63);
+    else __atomic_fetch_or(&c->bits[b >> 6], 1ULL << (b & 63), __ATOMIC_RELAXED);
+}
+
+/* task t < nchunks: planes [t*planes, (t+1)*planes) of [0, V); nchunks: z < 0; nchunks+1: z >= V
+ * (those two only count outside samples). Segments flagged chk are evaluated whole by task 0. */
+static void zpart_task(void* vctx, int64_t t) {
+    zpart_ctx* c = (zpart_ctx*)vctx;
+    const int64_t n = c->n;
+    int64_t za, zb;
+    if (t < c->nchunks) {
+        za = t * c->planes;
+        zb = za + c->planes < c->V ? za + c->planes : c->V;
+    } else if (t == c->nchunks) {
+        za = INT32_MIN;
+        zb = 0;
+    } else {
+        za = c->V;
+        zb = (int64_t)INT32_MAX + 1;
+    }
+    int64_t outside = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double* seg = c->segs + 6 * i;
+        const double* w = c->w3 + 3 * i;
+        const int64_t N = c->steps[i];
+        int32_t v[3];
+        double g[3];
+        if (c->chk[i]) {
+            if (t != 0) continue;
+            for (int64_t k = 0; k <= N; ++k) {
+                vo_sample(seg, N, w, k, g);
+                if (vo_round_point(g, v)) {
+                    __atomic_store_n(&c->err, VO_RANGE_ERROR, __ATOMIC_RELAXED);
+                    break;
+                }
+                zpart_set(c, v, &outside, 0); /* (crosses chunks: atomic) */
+            }
+            continue;
+        }
+        if (c->zr[2 * i + 1] < za || c->zr[2 * i] >= zb) continue;
+        int64_t ka, kb;
+        if (w[2] >= 0.0) {
+            ka = z_cross(seg, w, 0, N, za, 1);
+            kb = z_cross(seg, w, ka, N, zb, 1);
+        } else {
+            ka = z_cross(seg, w, 0, N, zb, 0);
+            kb = z_cross(seg, w, ka, N, za, 0);
+        }
+        for (int64_t k = ka; k < kb; ++k) {
+            vo_sample(seg, N, w, k, g);
+            vo_round_point(g, v);
+            zpart_set(c, v, &outside, c->plain);
+        }
+        vo_round_point(seg + 3, v); /* k = N: E itself */
+        if (v[2] >= za && v[2] < zb) zpart_set(c, v, &outside, c->plain);
+    }
+    if (outside) __atomic_fetch_add(&c->outside, outside, __ATOMIC_RELAXED);
+}
+
+int vo_bitmap_zpart(const double* segs, int64_t n, uint64_t* bits, int64_t V, int64_t z_lo,
+                    int64_t z_hi, int64_t* outside, int nthreads) {
+    if (n <= 0) return VO_INVALID_ARGUMENT;
+    if (V <= 0 || z_lo < 0 || z_hi > V || z_lo > z_hi) return VO_INVALID_ARGUMENT;
+    zpart_ctx c;
+    memset(&c, 0, sizeof c);
+    c.segs = segs;
+    c.steps = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    c.w3 = (double*)malloc(sizeof(double) * 3 * (size_t)n);
+    c.zr = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)n);
+    c.chk = (uint8_t*)malloc((size_t)n);
+    if (!c.steps || !c.w3 || !c.zr || !c.chk) {
+        free(c.steps);
+        free(c.w3);
+        free(c.zr);
+        free(c.chk);
+        return VO_LOGIC_ERROR;
+    }
+    c.n = n;
+    c.bits = bits;
+    c.V = V;
+    c.z_lo = z_lo;
+    c.z_hi = z_hi;
+    c.first_bad = -1;
+    c.plain = (V * V) % 64 == 0; /* words never straddle planes: a chunk owns its words */
+    parallel_for(n, nthreads, 4096, zpart_plan_body, &c);
+    int e = c.first_bad >= 0 ? c.err : VO_OK;
+    if (!e) {
+        const int nt = resolve_threads(nthreads);
+        c.planes = V / (8 * (int64_t)nt);
+        if (c.planes < 1) c.planes = 1;
+        c.nchunks = (V + c.planes - 1) / c.planes;
+        c.err = 0;
+        parallel_for(c.nchunks + 2, nthreads, 1, zpart_task, &c);
+        e = c.err;
+        if (outside) *outside = c.outside;
+    }
+    free(c.steps);
+    free(c.w3);
+    free(c.zr);
+    free(c.chk);
+    return e;
+}
+
 /* ------------------------------------------------------------------ generators */
 /* src/bench.cpp:38-47: uniform direction on the unit sphere (Marsaglia) */
 static void sphere_direction(uint64_t* st, double d[3]) {

@@ -56,10 +56,17 @@ int vo_chain_lengths(const double* segs, int64_t n, int64_t* lengths, int nthrea
 
 /* Occupancy bitmap of every sample voxel (no reference counterpart; the set of rounded
  * samples == the set of chain voxels). Layout: bit b = x + V*(y + V*(z - z_lo)), 64-bit
- * little-endian words, only planes z_lo <= z < z_hi. Voxels outside [0,V)^2 x [z_lo,z_hi)
- * are counted in *outside and not set. */
+ * little-endian words, only planes z_lo <= z < z_hi. Samples outside the volume [0,V)^3 are
+ * counted in *outside; in-volume samples outside the slab are skipped. */
 int vo_bitmap(const double* segs, int64_t n, uint64_t* bits, int64_t V, int64_t z_lo,
               int64_t z_hi, int64_t* outside, int nthreads);
+
+/* The same bitmap and outside count, computed z-partitioned for large batches: the volume's
+ * planes are cut into chunks and each task owns one chunk's words (plain ORs, no atomics),
+ * walking only the k-range of each segment whose rounded z falls in its chunk (found by
+ * bisection: the rounded z of S + W*k is monotone in k). Pinned against vo_bitmap. */
+int vo_bitmap_zpart(const double* segs, int64_t n, uint64_t* bits, int64_t V, int64_t z_lo,
+                    int64_t z_hi, int64_t* outside, int nthreads);
 
 /* Per-chain order-sensitive hash + length (checks multi-GB GPU outputs without storing them):
  * h_i = sum_j (x_j*P1 + y_j*P2 + z_j*P3) * (j+1) mod 2^64, constants in voxline_oracle.c. */

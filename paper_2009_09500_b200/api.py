@@ -211,6 +211,12 @@ class Batch:
                                                         C.byref(total), MEM_DEVICE))
         return total.value
 
+    def count_voxels(self) -> int:
+        """BatchResult.total_voxels without materialising the list (count pass only)."""
+        total = C.c_int64()
+        self.ctx.check(self.ctx.lib.vxg_batch_count_voxels(self.h, C.byref(total)))
+        return total.value
+
     def emit_bitmap(self, V: int, z_lo: int = 0, z_hi: int | None = None, clip: bool = False,
                     words: np.ndarray | None = None, overwrite: bool | None = None):
         """Bitmap of planes [z_lo, z_hi) into `words` (host). The words are OR-ed into unless

@@ -417,6 +417,36 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
     return VXG_OK;
 }
 
+// BatchResult.total_voxels without the list: count pass + range scan, one readback.
+vxg_status count_voxels_device(vxg_batch* b, int64_t* total) {
+    vxg_context* ctx = b->ctx;
+    if (const vxg_status s = plan_ready(b)) return s;
+    const int64_t blk = vxg::list_block_samples();
+    const int64_t warps = vxg::list_resident_warps(ctx->num_sms);
+    int64_t nranges = std::max<int64_t>(1, warps * 2 / 3);
+    const int64_t blocks = ceil_div(std::max<int64_t>(b->capacity, 1), blk);
+    const int64_t range_len = ceil_div(blocks, nranges) * blk;
+    nranges = ceil_div(std::max<int64_t>(b->capacity, 1), range_len);
+    if (!b->ranges.ensure(ctx, sizeof(long long) * (size_t)(4 * nranges + 1)))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "count_voxels: out of device memory");
+    cudaMemsetAsync(ctl_slot(b, 1), 0, sizeof(Control), ctx->stream);
+    long long* rc = b->ranges.as<long long>();
+    vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->n, b->capacity, nranges,
+                    range_len, rc, rc + 3 * nranges, nullptr, 0, nullptr, ctl_slot(b, 1),
+                    nullptr, 1, nullptr};
+    cudaEventRecord(ctx->ev[2], ctx->stream);
+    const cudaError_t e = vxg::launch_list_count(a, ctx->stream);
+    ctx->launches += 2;
+    cudaEventRecord(ctx->ev[3], ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "count_voxels");
+    Control c;
+    const vxg_status s = read_ctl(ctx, ctl_slot(b, 1), c, "count_voxels");
+    cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);
+    if (s) return s;
+    *total = c.total;
+    return VXG_OK;
+}
+
 // Clip every segment to [z_lo, z_hi): entries + offsets; returns entries/samples.
 vxg_status run_clip(vxg_batch* b, int64_t z_lo, int64_t z_hi, int64_t* n_entries,
                     int64_t* samples) {
@@ -1134,6 +1164,13 @@ VXG_API vxg_status vxg_batch_emit_list(vxg_batch* b, vxg_voxel* out, int64_t out
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     b->timing.assemble_ns = ns_since(t1);
     return e == cudaSuccess ? VXG_OK : ctx->cuda_fail(e, "batch_voxelize readback");
+}
+
+VXG_API vxg_status vxg_batch_count_voxels(vxg_batch* b, int64_t* total) {
+    if (!b || !total) return VXG_INVALID_ARGUMENT;
+    b->ctx->ok();
+    cudaSetDevice(b->ctx->device);
+    return count_voxels_device(b, total);
 }
 
 VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t V, int64_t z_lo,

@@ -555,6 +555,9 @@ __global__ void __launch_bounds__(kScanBlock) tiles_scan_lb_kernel(TileArgs g) {
 // Pass B: write the pieces into their tiles' bins. tile_cur holds every bin's start on entry (the
 // scan wrote it), so the slot is one atomicAdd; the store of a piece is deferred to the next
 // piece so the atomic's round trip overlaps the walk instead of stalling it.
+// (Deeper software pipelines -- 2 to 4 pieces in flight, their slots held in registers -- were
+// measured slower: 93 registers instead of 77 cost more warps than the overlap gained; cfg5
+// scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3.)
 __global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
     const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (tix >= g.n) return;
@@ -630,7 +633,7 @@ __device__ __forceinline__ void red_or_shared(uint32_t saddr, uint32_t bit) {
 // straight-line (a select instead of a branch pair per sample).
 template <int G>
 __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, uint32_t spare,
-                                           const PieceRef& q, int gl) {
+                                           const PieceRef& q, int gl, const void* next_rec) {
 #if VXG_FILL_UNIFORM
     int mx = q.len;
 #pragma unroll
@@ -669,6 +672,7 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, ui
         one();
         one();
     }
+    if ((g.pf & 4) && next_rec) prefetch_l1(next_rec);
     for (int st = steps & 3; st > 0; --st) one();
     __syncwarp();
 #endif
@@ -756,12 +760,14 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         uint4 r1 = pb + grp < p1 ? pcs[pb + grp] : make_uint4(0u, 0u, 0u, 0u);
         uint4 r2 = pb + step + grp < p1 ? pcs[pb + step + grp] : make_uint4(0u, 0u, 0u, 0u);
         for (; pb < p1; pb += step) {
-            if (r2.z) prefetch_l1(g.rec + r2.x);
+            const SegRec* nrec = r2.z ? g.rec + r2.x : nullptr;
+            if (nrec && (g.pf & 1)) prefetch_l1(nrec);
+            if (nrec && (g.pf & 2)) prefetch_l2(nrec);
             PieceRef q;
             decode_piece(g, r1, q);
             r1 = r2;
             r2 = pb + 2 * step + grp < p1 ? pcs[pb + 2 * step + grp] : make_uint4(0u, 0u, 0u, 0u);
-            fill_piece<G>(g, sbase, spare, q, gl);
+            fill_piece<G>(g, sbase, spare, q, gl, nrec);
         }
         __syncthreads();
         // OR the tile into the bitmap: a row of kTX bits is 4 words = 2 x 16 B; each thread
@@ -880,6 +886,8 @@ cudaError_t launch_tiles_fill(const TileArgs& g, int num_sms, double mean_len, c
     int G = mean_len < 160.0 ? 2 : (mean_len < 320.0 ? 16 : 32);
     if (const char* e = getenv("VXG_FILL_G")) G = atoi(e);
     TileArgs gg = g;
+    gg.pf = 1;
+    if (const char* e = getenv("VXG_FILL_PF")) gg.pf = atoi(e);
     if (const char* e = getenv("VXG_FILL_ORDER")) {  // "bx,by,bz" (experiments)
         gg.bx = gg.by = gg.bz = 0;
         sscanf(e, "%d,%d,%d", &gg.bx, &gg.by, &gg.bz);

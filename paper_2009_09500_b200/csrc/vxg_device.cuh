@@ -96,6 +96,10 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // S + W*t with separate multiply and add (include/voxline/parametric.hpp:44-47).
 __device__ __forceinline__ double sample_axis(double s, double w, double t) {
     return __dadd_rn(s, __dmul_rn(w, t));

@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(1024) range_scan_kernel(ListArgs a) {
     }
     if (tid == 0) {
         a.range_pre[a.nranges] = s_carry;
-        a.chain_off[a.nseg] = s_carry;
+        if (a.chain_off) a.chain_off[a.nseg] = s_carry;  // (count only: no list)
         a.ctl->total = s_carry;
     }
 }

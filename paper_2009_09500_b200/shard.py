@@ -10,9 +10,13 @@ The path shards without a data-path collective:
   counts; bench.py's default) or `slab_bounds(V, world, rank)` (equal depths); the device walk
   clips every segment to its slab (vxg_bitmap.cu), slabs are disjoint, no reduction.
 
-The collectives here are for verification and reporting only: `gather_bitmap` / `gather_list`
-reassemble the full result on every rank, `max_over_ranks` / `sum_over_ranks` reduce scalars
-(bench.py times each step as the max over ranks).
+The collectives here are input distribution, verification and reporting, never a reduction of
+results: `distribute_segments` gives every rank the whole batch from one host->device slice per
+rank plus an all-gather over NVLink (the z-slab ranks each need every segment that reaches their
+slab); `gather_bitmap` / `gather_list` reassemble the full result on every rank and
+`list_digest` / `words_digest` let ranks compare results without moving them;
+`max_over_ranks` / `sum_over_ranks` reduce scalars (bench.py times each step as the max over
+ranks).
 """
 from __future__ import annotations
 
@@ -71,6 +75,102 @@ def sample_balanced_cuts(offsets: np.ndarray, world: int) -> np.ndarray:
     cuts = np.searchsorted(off, targets, side="left").astype(np.int64)
     cuts[0], cuts[-1] = 0, n
     return np.minimum(np.maximum.accumulate(cuts), n)
+
+
+def batch_sample_cuts(batch, world: int) -> np.ndarray:
+    """Segment cut points of a planned Batch for `world` ranks, balanced by samples (the list
+    configs' partition): rank r owns segments [c_r, c_{r+1})."""
+    p = batch.plans()
+    off = np.empty(batch.n + 1, np.int64)
+    off[:-1] = p["output_offset"]
+    off[-1] = batch.capacity
+    return sample_balanced_cuts(off, world)
+
+
+def row_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows [a, b) of an n-row array that rank `rank` of `world` uploads (equal slices)."""
+    return rank * n // world, (rank + 1) * n // world
+
+
+def distribute_segments(host_segs: np.ndarray, out, group=None) -> None:
+    """Fill the device tensor `out` ((n, 6) float64, on every rank) with all n segments of
+    `host_segs` (pinned host memory, the same array content on every rank) moving only 1/world
+    of them across each rank's PCIe link: rank r copies its equal slice host->device, then one
+    all-gather over the process group (NCCL: NVLink) assembles the whole batch everywhere.
+    (gloo, for functional tests: the gather runs through host memory.)"""
+    import torch
+    dist = _dist()
+    n = out.shape[0]
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        out.copy_(torch.from_numpy(host_segs), non_blocking=True)
+        return
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if n % world:
+        raise ValueError("distribute_segments: the segment count must divide by the world size")
+    a, b = row_range(n, world, rank)
+    src = torch.from_numpy(host_segs[a:b])
+    if dist.get_backend(group) == "nccl":
+        mine = out[a:b]
+        mine.copy_(src, non_blocking=True)
+        dist.all_gather_into_tensor(out, mine.contiguous(), group=group)
+    else:
+        parts = [torch.empty((b - a, 6), dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, src.clone(), group=group)
+        out.copy_(torch.cat(parts), non_blocking=True)
+
+
+_DIGEST_P = (0x9E3779B97F4A7C15, 0xC2B2AE3D27D4EB4F, 0x165667B19E3779F9, 0x27D4EB2F165667C5)
+
+
+def _signed64(u: int) -> int:
+    return u - (1 << 64) if u >= 1 << 63 else u
+
+
+def list_digest(voxels, chain_off) -> tuple[int, int, int]:
+    """Position-sensitive digest of a voxel list slice ((M, 3) int32 device tensor) and its chain
+    offsets ((k + 1,) int64, rebased to 0 here): (voxels, sum_j (x P1 + y P2 + z P3) (j + 1),
+    sum_i len_i (i + 1) P4), all mod 2^64 (torch int64 arithmetic wraps). Equal lists give equal
+    digests; a rank's digest is compared with the same slice of the one-rank list."""
+    import torch
+    dev = voxels.device
+    P = [_signed64(p) for p in _DIGEST_P]
+    m = voxels.shape[0]
+    h = torch.zeros((), dtype=torch.int64, device=dev)
+    step = 1 << 27
+    for a in range(0, m, step):
+        v = voxels[a:a + step].to(torch.int64)
+        j = torch.arange(a + 1, a + 1 + v.shape[0], dtype=torch.int64, device=dev)
+        h += ((v[:, 0] * P[0] + v[:, 1] * P[1] + v[:, 2] * P[2]) * j).sum()
+    c = chain_off.to(torch.int64)
+    ln = c[1:] - c[:-1]
+    i = torch.arange(1, ln.shape[0] + 1, dtype=torch.int64, device=dev)
+    hc = (ln * i * P[3]).sum()
+    return int(m), int(h.item()), int(hc.item())
+
+
+def words_digest(words) -> int:
+    """Position-sensitive digest of a bitmap slice (int64/uint64 words, device tensor):
+    sum_i ((w_i xor (i + 1) P2) P1) mod 2^64, computed in chunks."""
+    import torch
+    P = [_signed64(p) for p in _DIGEST_P]
+    w = words.reshape(-1).view(torch.int64)
+    h = torch.zeros((), dtype=torch.int64, device=w.device)
+    step = 1 << 28
+    for a in range(0, w.shape[0], step):
+        x = w[a:a + step]
+        i = torch.arange(a + 1, a + 1 + x.shape[0], dtype=torch.int64, device=w.device)
+        h += (torch.bitwise_xor(x, i * P[1]) * P[0]).sum()
+    return int(h.item())
+
+
+def gather_objects(obj, group=None) -> list:
+    """all_gather_object: every rank's small Python object, in rank order."""
+    dist = _dist()
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return [obj]
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
 
 
 def _dist():

@@ -54,13 +54,21 @@ def test_sm100a_cubin_only():
     funcs = {}
     for chunk in sass.split("Function : ")[1:]:
         funcs[chunk.split()[0]] = chunk
-    emit = [body for name, body in funcs.items() if "emit_list_kernel" in name or
-            "emit_bitmap_kernel" in name]
-    assert emit
-    for body in emit:
-        # S + W*k as separate DMUL / DADD and llround as DADD.RZ: no fused multiply-add
-        assert "DMUL" in body and "DADD" in body and "DADD.RZ" in body
-        assert "DFMA" not in body
+    # every kernel that evaluates samples S + W*k must be free of fused multiply-adds (the
+    # reference's FMA-free arithmetic); each must be present. (Kernels that also run make_plan
+    # -- plan_kernel, single_chain_kernel -- contain the DFMAs of the correctly rounded
+    # __ddiv_rn / __dsqrt_rn sequences, so they are not in this list.)
+    hot = ["list_fused_kernel", "list_count_kernel", "list_emit_kernel", "tiles_fill_kernel",
+           "emit_bitmap_kernel"]
+    for k in hot:
+        bodies = [body for name, body in funcs.items() if k in name]
+        assert bodies, f"{k} missing from the library"
+        for body in bodies:
+            assert "DMUL" in body and "DADD" in body, k
+            assert "DFMA" not in body, k
+    # and the one-DADD rounding (round_pos, DADD.RM) is what the hot loops use
+    assert "DADD.RM" in funcs[next(n for n in funcs if "tiles_fill_kernel" in n)]
+    assert "DADD.RM" in funcs[next(n for n in funcs if "list_fused_kernel" in n)]
 
 
 def test_no_gpu_fails_loudly():

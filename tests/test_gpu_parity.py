@@ -517,17 +517,112 @@ def test_device_batch_deferred_plan(vx, oracle, n, lmax):
     b.close()
 
 
+# ------------------------------------------------------------------ bulk plans (batch_preprocess)
+def _quarter_grid(n, seed):
+    rng = np.random.default_rng(seed)
+    return np.round(rng.uniform(-80, 80, size=(n, 6)) * 4) / 4
+
+
+def _plan_parity(vx, oracle, segs, d=None):
+    """Every plan field of a batch against the oracle's batch_preprocess (src/batch.cpp:57-73):
+    N_i, W_i as raw uint64 bit patterns, output offsets, N_max and the capacity."""
+    b = vx.Batch(None, device_ptr=d.data_ptr(), n=d.shape[0]) if d is not None else vx.Batch(segs)
+    p = b.plans()
+    o = oracle.batch_preprocess(segs)
+    assert np.array_equal(p["step_count"], o["steps"])
+    w = np.stack([p["wx"], p["wy"], p["wz"]], axis=1)
+    assert np.array_equal(w.view(np.uint64), o["step_vectors"].view(np.uint64))
+    assert np.array_equal(p["output_offset"], o["offsets"])
+    assert b.max_steps == o["max_steps"] and b.capacity == o["capacity"]
+    b.close()
+    return o["capacity"]
+
+
+def test_bulk_plans_tie_corpora(vx, oracle):
+    """Plans of corpora built to expose rounding and FMA contraction: the decimal grid (317 of
+    2.8M samples round differently under FMA), the quarter grid (ties in
+    round(S) == round(E) and in N), the reference tests' mixed corpora, random doubles."""
+    for segs in (np.asarray(decimal_grid_corpus(200000, 4321)), _quarter_grid(200000, 17),
+                 np.asarray(mixed_batch(20000, 402, 3, 500.0)),
+                 np.random.default_rng(5).uniform(-1e6, 1e6, size=(200000, 6))):
+        _plan_parity(vx, oracle, segs)
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg4", "cfg3"])
+def test_bulk_plans_full_configs(vx, oracle, cfg):
+    """batch_preprocess at the bench's full sizes and seeds: cfg1 (65,536 x N=128), cfg4 (4M, N ~
+    U{1..2048}), cfg3 (16M x N=64): every N_i, W_i bit pattern and offset equals the oracle's."""
+    import torch
+    n, lf, lm, V, seed = {"cfg1": (65536, 128, 0, 512, 0x5EED0101),
+                          "cfg4": (4 << 20, 0, 2048, 4096, 0x5EED0104),
+                          "cfg3": (16 << 20, 64, 0, 1024, 0x5EED0103)}[cfg]
+    ctx = vx.default_context()
+    d = torch.empty((n, 6), dtype=torch.float64, device="cuda")
+    ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, lf, lm, V, seed, d.data_ptr(), 1))
+    segs = d.cpu().numpy()
+    assert np.array_equal(segs.view(np.uint64),
+                          oracle.gen_batch(n, lf, lm, V, seed, nthreads=0).view(np.uint64))
+    _plan_parity(vx, oracle, segs, d)
+
+
+def test_count_voxels(vx, oracle):
+    """vxg_batch_count_voxels (the count pass alone) equals BatchResult.total_voxels of the
+    oracle and the list path's total, on short, long and tie-heavy corpora."""
+    for segs in (vx.gen_segments(20000, 128, 0, 512, 3), vx.gen_segments(5000, 0, 2048, 4096, 4),
+                 _quarter_grid(30000, 9), np.asarray(decimal_grid_corpus(30000, 77))):
+        b = vx.Batch(segs)
+        t = b.count_voxels()
+        _, _, total = b.emit_list()
+        assert t == total == oracle.run_batch(segs)[2]
+        b.close()
+
+
+def _tie_lines(n, seed, ulps):
+    """Axis-parallel and diagonal segments whose samples S + W*k land exactly on (or a few ulp
+    beside) half-integers: W is an exact small dyadic step and S.x sits on/next to a tie."""
+    rng = np.random.default_rng(seed)
+    segs = np.empty((n, 6))
+    base = rng.integers(2, 3000, size=(n, 3)).astype(np.float64) + 0.5
+    for i in range(n):
+        u = ulps[i % len(ulps)]
+        s = base[i].copy()
+        for _ in range(abs(u)):
+            s[0] = np.nextafter(s[0], np.inf if u > 0 else 0.0)
+        L = float(rng.integers(1, 400))
+        dirs = [(L, 0.0, 0.0), (L, L, 0.0), (L, L / 2, L / 4), (L, 0.0, L)]
+        d = dirs[i % len(dirs)]
+        segs[i, :3] = s
+        segs[i, 3:] = s + np.asarray(d)
+    return segs
+
+
+def test_round_pos_ties_in_situ(vx, oracle):
+    """The one-DADD rounding (round_pos, records with every coordinate >= 1) on samples that sit
+    exactly on ties and within +-3 ulp of them: voxel lists and bitmaps equal the oracle's
+    (llround, ties away from zero). The host-side proof check is
+    tests/test_oracle_golden.py::test_round_pos_identity_host."""
+    segs = _tie_lines(40000, 11, [0, 1, -1, 2, -2, 3, -3])
+    assert segs.min() >= 1.0  # REC_POS: the round_pos path
+    _compare(vx, oracle, segs)
+    V = 4096
+    words, outside = vx.voxelize_bitmap(segs, V, 0, V, clip=False)
+    ow, oo = oracle.bitmap(segs, V, nthreads=0, zpart=True)
+    assert outside == oo
+    assert np.array_equal(words, ow)
+
+
 # ------------------------------------------------------------------ full BASELINE sizes
 @pytest.mark.slow
 def test_full_config4_list_hashes(vx, oracle):
-    """Config 4 at full size: 4M segments, N ~ U{1..2048}: every chain's length and
-    order-sensitive hash equal the oracle's (4.3 G samples); first/last voxels pinned."""
+    """Config 4 at full size and the bench's seed: 4M segments, N ~ U{1..2048}: every chain's
+    length and order-sensitive hash equal the oracle's (4.3 G samples); first/last voxels
+    pinned."""
     import torch
     from tests.gpu_checks import device_chain_hashes
     n = 4 * 1024 * 1024
     d = torch.empty((n, 6), dtype=torch.float64, device="cuda")
     ctx = vx.default_context()
-    ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, 0, 2048, 4096, 0x5EED0004, d.data_ptr(), 1))
+    ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, 0, 2048, 4096, 0x5EED0104, d.data_ptr(), 1))
     b = vx.Batch(None, device_ptr=d.data_ptr(), n=n)
     out = torch.empty((b.capacity, 3), dtype=torch.int32, device="cuda")
     chain = torch.empty(n + 1, dtype=torch.int64, device="cuda")
@@ -593,3 +688,42 @@ def test_full_config5_slabs_consistent(vx, oracle):
     bs.emit_bitmap_device(w.data_ptr(), V, 0, V, True)
     ow, _ = oracle.bitmap(sub.cpu().numpy(), V)
     assert np.array_equal(w.cpu().numpy().view(np.uint64), ow)
+
+
+@pytest.mark.slow
+def test_full_config5_bitmap_oracle(vx, oracle):
+    """Config 5 at full size and the bench's seed (64M segments, N ~ U{1..2048}, 4096^3, 68.8 G
+    samples): the full-volume device bitmap and its outside count equal the oracle's bit for bit
+    (oracle: z-partitioned over all host cores); then, for N = 2, 4, 8 ranks, the bench's own
+    per-rank pipeline -- sample-balanced slabs (shard.sample_balanced_slabs over
+    Batch.slab_samples) -> on-device slab filter (vxg_select_slab_segments) -> Batch -> clipped
+    emit_bitmap -- reassembles that same bitmap."""
+    import torch
+    from paper_2009_09500_b200.shard import sample_balanced_slabs, select_slab_segments
+    V, n = 4096, 64 << 20
+    ctx = vx.default_context()
+    d = torch.empty((n, 6), dtype=torch.float64, device="cuda")
+    ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, 0, 2048, V, 0x5EED0105, d.data_ptr(), 1))
+    nwords = V * V * V // 64
+    full = torch.zeros(nwords, dtype=torch.int64, device="cuda")
+    b = vx.Batch(None, device_ptr=d.data_ptr(), n=n)
+    out_dev = b.emit_bitmap_device(full.data_ptr(), V, 0, V, False)
+    segs = d.cpu().numpy()
+    ow, oo = oracle.bitmap(segs, V, nthreads=0, zpart=True)
+    assert out_dev == oo
+    assert np.array_equal(full.cpu().numpy().view(np.uint64), ow)
+    del ow, segs
+    plane = V * V // 64
+    local = torch.empty_like(d)
+    for world in (2, 4, 8):
+        slabs = sample_balanced_slabs(b.slab_samples, V, world)
+        assert slabs[0][0] == 0 and slabs[-1][1] == V
+        cat = torch.zeros(nwords, dtype=torch.int64, device="cuda")
+        for z0, z1 in slabs:
+            k = select_slab_segments(ctx, d.data_ptr(), n, z0, z1, local.data_ptr())
+            part = vx.Batch(None, device_ptr=local.data_ptr(), n=k)
+            part.emit_bitmap_device(cat.data_ptr() + 8 * z0 * plane, V, z0, z1, True)
+            part.close()
+        assert torch.equal(cat, full), world
+        del cat
+    b.close()

@@ -147,3 +147,37 @@ def test_volume_generator_plans_exact(oracle, ref):
             assert steps.min() >= 1 and steps.max() <= Lm
         vox, _, _ = oracle.run_batch(segs)
         assert vox.min() >= 1 and vox.max() <= V - 2
+
+
+def test_round_pos_identity_host(oracle):
+    """The GPU hot loops' rounding (vxg_device.cuh round_pos: RM(c + 2^51 + 0.5), mantissa >> 1)
+    equals llround (src/geometry.cpp:21) on every tie k + 0.5 (k < 2^24) and both its neighbours,
+    on 2^22 random values in [0, 2^31 - 1) and 2^22 near-ties (+-8 ulp), and on edge values: 58.7M
+    values, emulated on the host with the same IEEE-754 addition in round-toward-minus-infinity."""
+    bad, n, first = oracle.check_round_pos(1 << 24, 1 << 22, seed=7)
+    assert n > 5 * 10 ** 7
+    assert bad == 0, f"round_pos differs from llround at {first!r}"
+    # the check has teeth: the same addition in round-to-nearest (ties to even) must fail
+    bad_rn, _, _ = oracle.check_round_pos(1 << 12, 1 << 10, seed=7, mode=1)
+    assert bad_rn > 0
+
+
+@pytest.mark.parametrize("V,z_lo,z_hi", [(256, 0, 256), (256, 17, 200), (100, 3, 97), (128, 0, 1),
+                                         (96, 0, 96)])
+def test_bitmap_zpart_matches_bitmap(oracle, V, z_lo, z_hi):
+    """The z-partitioned oracle bitmap (used for the full config-5 parity run) equals the plain
+    per-sample one, outside count included, on volume-crossing and out-of-volume segments."""
+    rng = np.random.default_rng(V + z_lo)
+    segs = rng.uniform(-60, V + 60, size=(4000, 6))
+    segs[::7] = np.round(segs[::7] * 2) / 2  # ties
+    a, oa = oracle.bitmap(segs, V, z_lo, z_hi, nthreads=4)
+    b, ob = oracle.bitmap(segs, V, z_lo, z_hi, nthreads=4, zpart=True)
+    assert oa == ob
+    assert np.array_equal(a, b)
+
+
+def test_bitmap_zpart_volume_generator(oracle):
+    segs = oracle.gen_batch(20000, 0, 512, 1024, 0x5EED0105)
+    a, oa = oracle.bitmap(segs, 1024, nthreads=4)
+    b, ob = oracle.bitmap(segs, 1024, nthreads=4, zpart=True)
+    assert oa == ob and np.array_equal(a, b)
