@@ -189,6 +189,21 @@ VXG_API vxg_status vxg_batch_slab_samples(vxg_batch* b, int64_t z_lo, int64_t z_
  * passes before it (assemble_ns: list count pass + range scan, or the bitmap binning passes). */
 VXG_API vxg_status vxg_batch_timing(const vxg_batch* b, vxg_timing* t);
 
+/* run_batch (src/batch.cpp:154-162) on DEVICE-resident segments into device buffers, for small
+ * batches in ONE kernel launch: plan, count, output prefix (decoupled look-back over tiles of 64
+ * segments) and emit fused (the latency regime, config 1). out: room for out_cap voxels;
+ * chain_off: n + 1 entries. total != NULL: synchronous, *total = BatchResult.total_voxels.
+ * total == NULL: only enqueued on the context's stream; vxg_run_batch_device_result reads the
+ * result of the last such call (the segments must stay valid until then). Batches holding a
+ * segment with more than 2^14 steps take the multi-pass path (same results). */
+VXG_API vxg_status vxg_run_batch_device(vxg_context* ctx, const vxg_segment* segs, int64_t n,
+                                        vxg_voxel* out, int64_t out_cap, int64_t* chain_off,
+                                        int64_t* total);
+/* Result of the last vxg_run_batch_device call enqueued without a total: synchronises; also
+ * N_max and the capacity (sum of N_i + 1) of its plan (either may be NULL). */
+VXG_API vxg_status vxg_run_batch_device_result(vxg_context* ctx, int64_t* total,
+                                               int64_t* max_steps, int64_t* capacity);
+
 /* run_batch (src/batch.cpp:154-162) with host buffers: upload, plan, emit, read back.
  * out needs room for the capacity (use vxg_batch_* for a two-step sized call). */
 VXG_API vxg_status vxg_run_batch(vxg_context* ctx, const vxg_segment* segs, int64_t n,

@@ -10,7 +10,8 @@ from ._lib import (CudaError, InvalidArgument, LogicError, OutOfRange, RangeErro
 from .api import (Batch, BatchPlan, batch_preprocess, batch_voxelize, chain_length_bounds,
                   compute_mvps, effective_item_count, gen_arbitrary_batch, gen_segment_of_length,
                   gen_segments, kernel_work_item, make_plan, pinned_empty, round_point, run_batch,
-                  run_batch_flat, segment_length, voxelize_bitmap, voxelize_parametric,
+                  run_batch_flat, run_batch_device, run_batch_device_result, segment_length,
+                  voxelize_bitmap, voxelize_parametric,
                   read_segments_csv, write_chains, batch_to_file)
 from ._lib import IoError
 
@@ -21,6 +22,7 @@ __all__ = [
     "Batch", "run_batch_flat", "voxelize_bitmap", "gen_segments", "pinned_empty", "Context",
     "default_context", "VoxGpuError", "InvalidArgument", "RangeError", "OutOfRange", "LogicError",
     "CudaError", "IoError", "read_segments_csv", "write_chains", "batch_to_file",
+    "run_batch_device", "run_batch_device_result",
 ]
 
 

@@ -119,6 +119,8 @@ SIGNATURES = {
     "vxg_batch_work_item": (C.c_int, [_vp, _i64, _i64, _vp, C.POINTER(C.c_int)]),
     "vxg_batch_emit_list": (C.c_int, [_vp, _vp, _i64, _vp, _i64p, C.c_int]),
     "vxg_batch_count_voxels": (C.c_int, [_vp, _i64p]),
+    "vxg_run_batch_device": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _vp, _i64p]),
+    "vxg_run_batch_device_result": (C.c_int, [_vp, _i64p, _i64p, _i64p]),
     "vxg_batch_emit_bitmap": (C.c_int, [_vp, _vp, _i64, _i64, _i64, C.c_int, _i64p, C.c_int]),
     "vxg_batch_slab_samples": (C.c_int, [_vp, _i64, _i64, _i64p]),
     "vxg_select_slab_segments": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64p]),

@@ -355,6 +355,26 @@ def effective_item_count(plan: BatchPlan):
     return (live.value, red.value)
 
 
+def run_batch_device(segs_ptr: int, n: int, out_ptr: int, out_cap: int, chain_ptr: int,
+                     ctx=None, sync: bool = True):
+    """run_batch on device-resident segments into device buffers in one kernel launch (small
+    batches; vxg_run_batch_device). sync: return BatchResult.total_voxels; else only enqueue
+    (run_batch_device_result() reads it)."""
+    ctx = ctx or default_context()
+    total = C.c_int64()
+    ctx.check(ctx.lib.vxg_run_batch_device(ctx.h, segs_ptr, n, out_ptr, out_cap, chain_ptr,
+                                           C.byref(total) if sync else None))
+    return total.value if sync else None
+
+
+def run_batch_device_result(ctx=None):
+    """(total_voxels, max_steps, capacity) of the last asynchronous run_batch_device call."""
+    ctx = ctx or default_context()
+    t, m, c = C.c_int64(), C.c_int64(), C.c_int64()
+    ctx.check(ctx.lib.vxg_run_batch_device_result(ctx.h, C.byref(t), C.byref(m), C.byref(c)))
+    return t.value, m.value, c.value
+
+
 def run_batch_flat(segments):
     """run_batch with flat outputs: (voxels int32 (M,3), chain_offsets int64 (n+1,), total)."""
     b = Batch(segments)

@@ -109,6 +109,10 @@ struct vxg_context {
     int32_t* h_single = nullptr;
     Control* h_single_ctl = nullptr;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    // one-launch small-batch path (vxg_run_batch_device): look-back words, control block, the
+    // last asynchronous call's arguments (re-routed to the multi-pass path if needed)
+    struct SmallState;
+    SmallState* small = nullptr;
 
     vxg_status fail(vxg_status s, int64_t seg, const char* fmt, ...) {
         char buf[512];
@@ -154,6 +158,16 @@ struct DBuf {
         return static_cast<T*>(p);
     }
     ~DBuf() { release(); }
+};
+
+struct vxg_context::SmallState {
+    DBuf status, ctl;
+    Control* h_ctl = nullptr;  // pinned readback
+    bool pending = false;
+    const vxg_segment* segs = nullptr;
+    int64_t n = 0, out_cap = 0;
+    vxg_voxel* out = nullptr;
+    int64_t* chain = nullptr;
 };
 
 struct vxg_batch {
@@ -763,6 +777,10 @@ VXG_API void vxg_destroy(vxg_context* ctx) {
         cudaStreamDestroy(ctx->copy_stream);
     }
     if (ctx->h_layers) cudaFreeHost(ctx->h_layers);
+    if (ctx->small) {
+        if (ctx->small->h_ctl) cudaFreeHost(ctx->small->h_ctl);
+        delete ctx->small;  // (its buffers go back to the cache, released next)
+    }
     ctx->cache.release();
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->h_ctl) cudaFreeHost(ctx->h_ctl);
@@ -1279,6 +1297,113 @@ VXG_API vxg_status vxg_run_batch(vxg_context* ctx, const vxg_segment* segs, int6
     vxg_batch_destroy(b);
     return s;
 }
+
+// ------------------------------------------------------------------------------- small batches
+namespace {
+
+// The multi-pass path for a batch the one-launch kernel handed back (a segment with N > 2^14).
+vxg_status small_reroute(vxg_context* ctx, const vxg_segment* segs, int64_t n, vxg_voxel* out,
+                         int64_t out_cap, int64_t* chain, int64_t* total) {
+    vxg_batch* b = nullptr;
+    vxg_status s = vxg_batch_create(ctx, segs, n, VXG_MEM_DEVICE, &b);
+    if (s) return s;
+    s = emit_list_device(b, reinterpret_cast<int32_t*>(out), out_cap,
+                         reinterpret_cast<long long*>(chain), total);
+    vxg_batch_destroy(b);
+    return s;
+}
+
+vxg_status small_result(vxg_context* ctx, int64_t* total, int64_t* max_steps, int64_t* capacity) {
+    vxg_context::SmallState* st = ctx->small;
+    st->pending = false;
+    cudaError_t e = cudaMemcpyAsync(st->h_ctl, st->ctl.p, sizeof(Control), cudaMemcpyDeviceToHost,
+                                    ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "run_batch_device");
+    const Control c = *st->h_ctl;
+    if (c.n_entries) {  // long segment: the multi-pass path
+        int64_t t = 0;
+        vxg_status s = small_reroute(ctx, st->segs, st->n, st->out, st->out_cap, st->chain, &t);
+        if (s) return s;
+        if (total) *total = t;
+        if (max_steps) *max_steps = (int64_t)c.max_steps;
+        if (capacity) *capacity = (int64_t)c.pad0;
+        return VXG_OK;
+    }
+    // (plan errors first: they are batch_preprocess's; ctl_status reports the lowest segment)
+    const vxg_status s = ctl_status(ctx, c, "run_batch");
+    if (s) return s;
+    if (total) *total = c.total;
+    if (max_steps) *max_steps = (int64_t)c.max_steps;
+    if (capacity) *capacity = (int64_t)c.pad0;
+    return VXG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+VXG_API vxg_status vxg_run_batch_device(vxg_context* ctx, const vxg_segment* segs, int64_t n,
+                                        vxg_voxel* out, int64_t out_cap, int64_t* chain_off,
+                                        int64_t* total) {
+    if (!ctx) return VXG_INVALID_ARGUMENT;
+    ctx->ok();
+    if (n <= 0) return ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_preprocess: empty segment list");
+    if (!segs || !chain_off || (!out && out_cap > 0))
+        return ctx->fail(VXG_INVALID_ARGUMENT, -1, "run_batch_device: null buffer");
+    if (!is_aligned16(segs) || (reinterpret_cast<uintptr_t>(out) & 3u))
+        return ctx->fail(VXG_INVALID_ARGUMENT, -1, "run_batch_device: misaligned buffer");
+    cudaSetDevice(ctx->device);
+    if (!ctx->small) {
+        ctx->small = new (std::nothrow) vxg_context::SmallState();
+        if (!ctx->small) return ctx->fail(VXG_OUT_OF_MEMORY, -1, "run_batch_device: oom");
+    }
+    vxg_context::SmallState* st = ctx->small;
+    if (st->pending) {  // the previous asynchronous call's errors are reported by its result
+        const vxg_status s = small_result(ctx, nullptr, nullptr, nullptr);
+        if (s) return s;
+    }
+    if (!st->h_ctl &&
+        cudaHostAlloc(reinterpret_cast<void**>(&st->h_ctl), sizeof(Control), cudaHostAllocDefault) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        st->h_ctl = nullptr;
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "run_batch_device: pinned memory");
+    }
+    const long long ntiles = vxg::small_tile_count(n);
+    if (!st->status.ensure(ctx, sizeof(unsigned long long) * (size_t)ntiles) ||
+        !st->ctl.ensure(ctx, sizeof(Control)))
+        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "run_batch_device: out of device memory");
+    cudaMemsetAsync(st->status.p, 0, sizeof(unsigned long long) * (size_t)ntiles, ctx->stream);
+    cudaMemsetAsync(st->ctl.p, 0, sizeof(Control), ctx->stream);
+    vxg::SmallArgs a{reinterpret_cast<const double*>(segs), n, ntiles,
+                     reinterpret_cast<int32_t*>(out), out_cap,
+                     reinterpret_cast<long long*>(chain_off),
+                     st->status.as<unsigned long long>(), st->ctl.as<Control>()};
+    const cudaError_t e = vxg::launch_list_small(a, ctx->stream);
+    ctx->launches++;
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "list_small_kernel");
+    st->pending = true;
+    st->segs = segs;
+    st->n = n;
+    st->out = out;
+    st->out_cap = out_cap;
+    st->chain = chain_off;
+    if (!total) return VXG_OK;
+    return small_result(ctx, total, nullptr, nullptr);
+}
+
+VXG_API vxg_status vxg_run_batch_device_result(vxg_context* ctx, int64_t* total,
+                                               int64_t* max_steps, int64_t* capacity) {
+    if (!ctx) return VXG_INVALID_ARGUMENT;
+    ctx->ok();
+    if (!ctx->small || !ctx->small->pending)
+        return ctx->fail(VXG_LOGIC_ERROR, -1, "run_batch_device_result: no call pending");
+    cudaSetDevice(ctx->device);
+    return small_result(ctx, total, max_steps, capacity);
+}
+
+}  // extern "C"
 
 // ------------------------------------------------------------------------------- generators
 VXG_API vxg_status vxg_gen_segments(vxg_context* ctx, int64_t n, const int64_t* lens,

@@ -44,6 +44,16 @@ struct ListArgs {
     const Control* plan_ctl;
 };
 
+struct SmallArgs {           // one-launch run_batch of a small batch (list_small_kernel)
+    const double* segs;         // AoS, 6 doubles per segment, 16-B aligned
+    long long n, ntiles;
+    int32_t* out;               // 3 int32 per voxel
+    long long out_cap;
+    long long* chain_off;       // n + 1
+    unsigned long long* status; // ntiles look-back words (zeroed)
+    Control* ctl;               // total, max_steps, pad0 = capacity, n_entries = long segment
+};
+
 struct SingleArgs {          // one segment, one CTA (single_chain_kernel)
     double seg[6];
     long long cap;              // voxels `out` can hold (more are counted, not written)
@@ -122,6 +132,8 @@ cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s);  // count pass
 cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s);   // emit pass
 cudaError_t launch_list_fused(const ListArgs& a, int num_sms, cudaStream_t s);  // both, overlapped
 cudaError_t launch_single_chain(const SingleArgs& a, cudaStream_t s);
+long long small_tile_count(long long n);
+cudaError_t launch_list_small(const SmallArgs& a, cudaStream_t s);
 int list_resident_warps(int num_sms);
 int list_fused_block_samples();  // fused kernel's staged block
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);

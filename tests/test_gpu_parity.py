@@ -577,6 +577,54 @@ def test_count_voxels(vx, oracle):
         b.close()
 
 
+@pytest.mark.parametrize("case", ["cfg1", "mixed", "ties", "long", "one", "errors", "cap"])
+def test_run_batch_device_one_launch(vx, oracle, case):
+    """vxg_run_batch_device (plan + count + look-back prefix + emit in one kernel) against the
+    oracle: config-1 shape, arbitrary lengths with zero-step segments, ties, a batch holding a
+    segment too long for it (re-routed to the multi-pass path), n = 1, a range error (lowest
+    segment reported), an undersized output buffer; also the asynchronous form."""
+    import torch
+    segs = {"cfg1": lambda: vx.gen_segments(65536, 128, 0, 512, 0x5EED0101),
+            "mixed": lambda: np.concatenate([vx.gen_segments(3000, 0, 700, 1024, 5),
+                                             np.array([[3.2, 4.4, 5.1, 3.3, 4.2, 5.0]] * 70)]),
+            "ties": lambda: _quarter_grid(50000, 31),
+            "long": lambda: np.concatenate([vx.gen_segments(500, 0, 300, 1024, 6),
+                                            [[0.0, 0.0, 0.0, 40000.0, 3.0, 1.0]]]),
+            "one": lambda: np.array([[0.1, 0.3, 0.7, 12.45, 4.9, 0.2]]),
+            "errors": lambda: np.array([[0, 0, 0, 5, 5, 5], [0, 0, 0, 1, 1, 1],
+                                        [0, 0, 0, 3e9, 0, 0], [0, 0, 0, 1, 2, 3],
+                                        [np.nan, 0, 0, 1, 1, 1]], dtype=np.float64),
+            "cap": lambda: vx.gen_segments(2000, 64, 0, 256, 8)}[case]()
+    d = torch.from_numpy(np.ascontiguousarray(segs, dtype=np.float64)).cuda()
+    n = d.shape[0]
+    if case == "errors":
+        out = torch.empty((1000, 3), dtype=torch.int32, device="cuda")
+        chain = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        with pytest.raises(vx.RangeError) as ei:
+            vx.run_batch_device(d.data_ptr(), n, out.data_ptr(), 1000, chain.data_ptr())
+        assert ei.value.args[1] == 2  # the lowest failing segment, as batch_preprocess reports
+        return
+    ovox, ooff, ototal = oracle.run_batch(segs)
+    cap = ototal - 1 if case == "cap" else ototal
+    out = torch.empty((max(cap, 1), 3), dtype=torch.int32, device="cuda")
+    chain = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    if case == "cap":
+        with pytest.raises(vx.LogicError):
+            vx.run_batch_device(d.data_ptr(), n, out.data_ptr(), cap, chain.data_ptr())
+        return
+    total = vx.run_batch_device(d.data_ptr(), n, out.data_ptr(), cap, chain.data_ptr())
+    assert total == ototal
+    assert np.array_equal(chain.cpu().numpy(), ooff)
+    assert np.array_equal(out.cpu().numpy()[:total], ovox)
+    out.zero_()
+    for _ in range(3):  # asynchronous form: enqueue several, read the last
+        vx.run_batch_device(d.data_ptr(), n, out.data_ptr(), cap, chain.data_ptr(), sync=False)
+    t, mx, capa = vx.run_batch_device_result()
+    o = oracle.batch_preprocess(segs)
+    assert t == ototal and capa == o["capacity"] and mx == o["max_steps"]
+    assert np.array_equal(out.cpu().numpy()[:total], ovox)
+
+
 def _tie_lines(n, seed, ulps):
     """Axis-parallel and diagonal segments whose samples S + W*k land exactly on (or a few ulp
     beside) half-integers: W is an exact small dyadic step and S.x sits on/next to a tie."""
