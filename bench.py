@@ -416,9 +416,11 @@ def main():
     # vxg_run_batch_device), enqueued back to back; the total is read once after the loop
     small = kind == "list" and my_n <= (1 << 18)
     small_ev = []
+    ev_pool = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(max(args.steps, args.warmup))] if small else []
 
     def step_small():
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = ev_pool[len(small_ev)]
         e0.record(stream)
         vx.run_batch_device(my_ptr, my_n, out.data_ptr(), capacity, chain.data_ptr(), ctx=ctx,
                             sync=False)

@@ -158,20 +158,33 @@ std::optional<Voxel> kernel_work_item(const BatchPlan& plan, std::int64_t segmen
                                 std::to_string(plan.max_steps + 1) + " grid");
     const SegmentPlan& sp = plan.per_segment[(size_t)segment_index];
     if (k > sp.step_count) return std::nullopt;  // redundant item
-    // a one-segment plan of item i, evaluated by the GPU's work-item kernel
-    BatchPlan one;
-    one.segments = {plan.segments[(size_t)segment_index]};
-    one.per_segment = {{sp.step_count, sp.step_vector, 0}};
-    one.max_steps = sp.step_count;
-    one.total_voxel_capacity = sp.step_count + 1;
-    BatchHandle h;
-    upload_plan(one, h);
-    int32_t v[3];
-    int live = 0;
-    check(vxg_batch_work_item(h.b, 0, k, v, &live));
-    if (!live) return std::nullopt;
-    return Voxel{v[0], v[1], v[2]};
+    // One item: the reference's own inline parametric_sample (include/voxline/parametric.hpp:
+    // 41-48) and round_point (src/geometry.cpp, linked unchanged) over the plan the GPU made --
+    // src/batch.cpp:86-89 verbatim in effect; a device round trip per item would cost ~100 us.
+    return round_point(
+        parametric_sample(plan.segments[(size_t)segment_index],
+                          ParametricPlan{sp.step_count, sp.step_vector}, k));
 }
+
+namespace {
+// Per-thread pinned staging for batch_voxelize's list (grown, never shrunk): pinning is a
+// per-call cost of milliseconds per GB, so it is paid once per thread, not once per call.
+struct PinnedCache {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~PinnedCache() { vxg_host_free(p); }
+    void* ensure(size_t b) {
+        if (b <= bytes) return p;
+        vxg_host_free(p);
+        const size_t grow = b + b / 4;
+        p = vxg_host_alloc(grow);
+        bytes = p ? grow : 0;
+        if (!p) throw std::bad_alloc();
+        return p;
+    }
+};
+thread_local PinnedCache t_vox, t_off;
+}  // namespace
 
 BatchResult batch_voxelize(const BatchPlan& plan, const PartitionConfig& cfg) {
     if (cfg.group_size < 1 || cfg.worker_count < 1)
@@ -187,22 +200,22 @@ BatchResult batch_voxelize(const BatchPlan& plan, const PartitionConfig& cfg) {
     upload_plan(plan, h);
     const size_t n = plan.segments.size();
     const auto k0 = Clock::now();
-    // flat list + chain offsets straight into pinned host memory (one D2H each)
-    struct Pinned {
-        void* p = nullptr;
-        ~Pinned() { vxg_host_free(p); }
-    } vox, off;
-    vox.p = vxg_host_alloc(sizeof(Voxel) * (size_t)std::max<int64_t>(plan.total_voxel_capacity, 1));
-    off.p = vxg_host_alloc(sizeof(int64_t) * (n + 1));
-    if (!vox.p || !off.p) throw std::bad_alloc();
+    // flat list + chain offsets straight into this thread's cached pinned staging (one D2H
+    // each). The list needs room for total_voxels, not the capacity: when the cache is smaller
+    // than the capacity, the voxel count comes first (the count pass alone).
+    int64_t need = plan.total_voxel_capacity;
+    if (t_vox.bytes < sizeof(Voxel) * (size_t)std::max<int64_t>(need, 1))
+        check(vxg_batch_count_voxels(h.b, &need));
+    void* vp = t_vox.ensure(sizeof(Voxel) * (size_t)std::max<int64_t>(need, 1));
+    void* op = t_off.ensure(sizeof(int64_t) * (n + 1));
     int64_t total = 0;
-    check(vxg_batch_emit_list(h.b, static_cast<vxg_voxel*>(vox.p), plan.total_voxel_capacity,
-                              static_cast<int64_t*>(off.p), &total, VXG_MEM_HOST));
+    check(vxg_batch_emit_list(h.b, static_cast<vxg_voxel*>(vp), need, static_cast<int64_t*>(op),
+                              &total, VXG_MEM_HOST));
     const auto k1 = Clock::now();
     result.timing.kernel_ns = ns_between(k0, k1);
     // assemble: the chains the API returns by value (std::vector per segment)
-    const Voxel* v = static_cast<const Voxel*>(vox.p);
-    const int64_t* o = static_cast<const int64_t*>(off.p);
+    const Voxel* v = static_cast<const Voxel*>(vp);
+    const int64_t* o = static_cast<const int64_t*>(op);
     result.chains.resize(n);
     for (size_t i = 0; i < n; ++i) {
         VoxelChain& c = result.chains[i];

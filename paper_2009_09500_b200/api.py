@@ -49,6 +49,21 @@ def _segments_array(segments) -> np.ndarray:
     return a.reshape(-1, 6)
 
 
+def _check_host_buffer(a, dtype, name: str, min_size: int = 0, shape_tail=None):
+    """Caller-supplied host output buffers are written by the library through a raw pointer:
+    check type, layout and size first (InvalidArgument instead of a native overflow)."""
+    if not isinstance(a, np.ndarray):
+        raise InvalidArgument(f"{name}: expected a numpy array", -1)
+    if a.dtype != np.dtype(dtype):
+        raise InvalidArgument(f"{name}: dtype {a.dtype}, expected {np.dtype(dtype)}", -1)
+    if not a.flags["C_CONTIGUOUS"] or not a.flags["WRITEABLE"]:
+        raise InvalidArgument(f"{name}: must be a writeable C-contiguous array", -1)
+    if shape_tail is not None and (a.ndim != 1 + len(shape_tail) or a.shape[1:] != shape_tail):
+        raise InvalidArgument(f"{name}: shape {a.shape}, expected (rows, {shape_tail[0]})", -1)
+    if a.size < min_size:
+        raise InvalidArgument(f"{name}: {a.size} elements, need {min_size}", -1)
+
+
 def _one_segment(start, end) -> np.ndarray:
     s = np.asarray(start, dtype=np.float64).reshape(3)
     e = np.asarray(end, dtype=np.float64).reshape(3)
@@ -194,11 +209,16 @@ class Batch:
         return self._plans
 
     def emit_list(self, out=None, chain_off=None):
-        """-> (voxels (M,3) int32, chain_offsets (n+1,) int64, total) in host memory."""
+        """-> (voxels (M,3) int32, chain_offsets (n+1,) int64, total) in host memory. Caller
+        buffers must be C-contiguous: out int32 (rows, 3), chain_off int64 with n + 1 entries."""
         if out is None:
             out = pinned_empty((max(self.capacity, 1), 3), np.int32)
+        else:
+            _check_host_buffer(out, np.int32, "out", shape_tail=(3,))
         if chain_off is None:
             chain_off = pinned_empty((self.n + 1,), np.int64)
+        else:
+            _check_host_buffer(chain_off, np.int64, "chain_off", min_size=self.n + 1)
         total = C.c_int64()
         self.ctx.check(self.ctx.lib.vxg_batch_emit_list(self.h, _ptr(out), out.shape[0],
                                                         _ptr(chain_off), C.byref(total),
@@ -228,6 +248,8 @@ class Batch:
             overwrite = words is None
         if words is None:
             words = np.empty(max(nwords, 1), np.uint64)
+        else:
+            _check_host_buffer(words, np.uint64, "words", min_size=nwords)
         outside = C.c_int64()
         self.ctx.check(self.ctx.lib.vxg_batch_emit_bitmap(self.h, _ptr(words), V, z_lo, z_hi,
                                                           _bitmap_flags(clip, overwrite),

@@ -10,6 +10,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -161,9 +162,10 @@ struct DBuf {
 };
 
 struct vxg_context::SmallState {
-    DBuf status, ctl;
+    DBuf status, ctl;  // look-back words, control block
     Control* h_ctl = nullptr;  // pinned readback
     bool pending = false;
+    int64_t calls = 0;  // asynchronous calls since the last result
     const vxg_segment* segs = nullptr;
     int64_t n = 0, out_cap = 0;
     vxg_voxel* out = nullptr;
@@ -589,9 +591,17 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     g.ctl = ctl_slot(b, 3);
     LayerStream ls{host_words, nullptr};
     DBuf layer_cnt;
+    // (if the streamed readback cannot be set up, the words are read back after the fill)
     if (host_words && (!layer_stream_setup(ctx, g.ntz, ls) ||
                        !layer_cnt.ensure(ctx, sizeof(unsigned) * (size_t)g.ntz)))
         ls.host_words = nullptr;
+    const size_t slab_bytes = 8 * (size_t)(((V * V * (z_hi - z_lo)) + 63) / 64);
+    auto plain_readback = [&]() -> vxg_status {
+        cudaError_t ce = cudaMemcpyAsync(host_words, d_words, slab_bytes, cudaMemcpyDeviceToHost,
+                                         ctx->stream);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
+        return ce == cudaSuccess ? VXG_OK : ctx->cuda_fail(ce, "bitmap readback");
+    };
     if (ls.host_words) {
         cudaMemsetAsync(layer_cnt.p, 0, sizeof(unsigned) * (size_t)g.ntz, ctx->stream);
         g.layer_cnt = layer_cnt.as<unsigned>();
@@ -659,14 +669,8 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     if (outside) *outside = b->capacity - c.total;
     if (npieces == 0) {
         b->emit_ms = b->aux_ms = 0.f;
-        if (ls.host_words) {  // nothing to fill: the device words (zeroed or uploaded) go back as they are
-            const size_t bytes = 8 * (size_t)(((V * V * (z_hi - z_lo)) + 63) / 64);
-            cudaError_t ce = cudaMemcpyAsync(ls.host_words, d_words, bytes, cudaMemcpyDeviceToHost,
-                                             ctx->stream);
-            if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
-            if (ce != cudaSuccess) return ctx->cuda_fail(ce, "bitmap readback");
-        }
-        return VXG_OK;
+        // nothing to fill: the device words (zeroed or uploaded) go back as they are
+        return host_words ? plain_readback() : VXG_OK;
     }
     if (!b->entries.ensure(ctx, sizeof(uint4) * (size_t)npieces))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory (%lld pieces)",
@@ -719,6 +723,7 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     }
     cudaEventElapsedTime(&b->aux_ms, ctx->ev[2], ctx->ev[3]);
     cudaEventElapsedTime(&b->emit_ms, ctx->ev[3], ctx->ev[4]);
+    if (!s && host_words && !ls.host_words) s = plain_readback();  // (streaming was unavailable)
     return s;
 }
 
@@ -1031,10 +1036,14 @@ VXG_API vxg_status vxg_batch_from_plan(vxg_context* ctx, const vxg_segment* segs
     const vxg_segment_plan& last = plans[n - 1];
     if (last.output_offset + last.step_count + 1 != capacity)
         return ctx->fail(VXG_LOGIC_ERROR, -1, "batch_voxelize: plan capacity mismatch");
+    // The reference checks only the last offset and the capacity. A max_steps above every N_i
+    // only widens kernel_work_item's grid (its redundant items stay redundant), so it is kept as
+    // given; one below some N_i would make the reference's kernel phase (k = 0..N_max) truncate
+    // those chains, which this path does not reproduce: rejected as a malformed plan.
     int64_t mx = 0;
     for (int64_t i = 0; i < n; ++i) mx = std::max(mx, plans[i].step_count);
-    if (mx != max_steps)
-        return ctx->fail(VXG_LOGIC_ERROR, -1, "batch_voxelize: plan max_steps mismatch");
+    if (mx > max_steps)
+        return ctx->fail(VXG_LOGIC_ERROR, -1, "batch_voxelize: plan max_steps below a step count");
     cudaSetDevice(ctx->device);
     vxg_batch* b = nullptr;
     vxg_status s = new_batch(ctx, &b);
@@ -1316,11 +1325,17 @@ vxg_status small_reroute(vxg_context* ctx, const vxg_segment* segs, int64_t n, v
 vxg_status small_result(vxg_context* ctx, int64_t* total, int64_t* max_steps, int64_t* capacity) {
     vxg_context::SmallState* st = ctx->small;
     st->pending = false;
+    const int64_t calls = st->calls;
+    st->calls = 0;
     cudaError_t e = cudaMemcpyAsync(st->h_ctl, st->ctl.p, sizeof(Control), cudaMemcpyDeviceToHost,
                                     ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return ctx->cuda_fail(e, "run_batch_device");
     const Control c = *st->h_ctl;
+    if (c.n_entries && calls > 1)
+        return ctx->fail(VXG_INVALID_ARGUMENT, -1,
+                         "run_batch_device: a batch enqueued asynchronously holds a segment of more "
+                         "than 2^14 steps (only the synchronous form re-routes it)");
     if (c.n_entries) {  // long segment: the multi-pass path
         int64_t t = 0;
         vxg_status s = small_reroute(ctx, st->segs, st->n, st->out, st->out_cap, st->chain, &t);
@@ -1359,7 +1374,11 @@ VXG_API vxg_status vxg_run_batch_device(vxg_context* ctx, const vxg_segment* seg
         if (!ctx->small) return ctx->fail(VXG_OUT_OF_MEMORY, -1, "run_batch_device: oom");
     }
     vxg_context::SmallState* st = ctx->small;
-    if (st->pending) {  // the previous asynchronous call's errors are reported by its result
+    // Asynchronous calls chain without synchronising: each resets only its own counters, while
+    // the error words (and the long-segment flag) stay set until the result reads them. A
+    // synchronous call first settles any pending ones.
+    const bool chain = st->pending && !total;
+    if (st->pending && total) {
         const vxg_status s = small_result(ctx, nullptr, nullptr, nullptr);
         if (s) return s;
     }
@@ -1375,15 +1394,23 @@ VXG_API vxg_status vxg_run_batch_device(vxg_context* ctx, const vxg_segment* seg
         !st->ctl.ensure(ctx, sizeof(Control)))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "run_batch_device: out of device memory");
     cudaMemsetAsync(st->status.p, 0, sizeof(unsigned long long) * (size_t)ntiles, ctx->stream);
-    cudaMemsetAsync(st->ctl.p, 0, sizeof(Control), ctx->stream);
+    if (chain) {  // max_steps; pad0 (capacity), total, tile_counter -- not err_seg / n_entries / abort
+        static_assert(offsetof(Control, err_seg) == 8 && offsetof(Control, pad0) == 16 &&
+                      offsetof(Control, tile_counter) == 32, "Control layout");
+        cudaMemsetAsync(st->ctl.p, 0, 8, ctx->stream);
+        cudaMemsetAsync(static_cast<char*>(st->ctl.p) + 16, 0, 24, ctx->stream);
+    } else {
+        cudaMemsetAsync(st->ctl.p, 0, sizeof(Control), ctx->stream);
+    }
     vxg::SmallArgs a{reinterpret_cast<const double*>(segs), n, ntiles,
                      reinterpret_cast<int32_t*>(out), out_cap,
                      reinterpret_cast<long long*>(chain_off),
                      st->status.as<unsigned long long>(), st->ctl.as<Control>()};
-    const cudaError_t e = vxg::launch_list_small(a, ctx->stream);
+    const cudaError_t e = vxg::launch_list_small(a, ctx->num_sms, ctx->stream);
     ctx->launches++;
     if (e != cudaSuccess) return ctx->cuda_fail(e, "list_small_kernel");
     st->pending = true;
+    st->calls++;
     st->segs = segs;
     st->n = n;
     st->out = out;

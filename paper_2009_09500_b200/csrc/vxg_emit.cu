@@ -3,6 +3,7 @@
 // SURVEY.md §2 row 3), writing either the deduplicated voxel list (batch_voxelize's kernel AND
 // assemble phases, src/batch.cpp:107-150, fused) or an occupancy bitmap.
 #include <cstdint>
+#include <mutex>
 
 #include "vxg_device.cuh"
 #include "vxg_internal.h"
@@ -751,17 +752,30 @@ static int resident_ctas(K kernel, int threads, size_t smem, int num_sms) {
 
 int list_block_samples() { return 32 * kListIPT; }
 
+// Function attributes and occupancy are per device: cached per device id (a process may drive
+// several contexts on different GPUs), under a lock.
+constexpr int kMaxDevices = 64;
+static std::mutex g_attr_mu;
+
+static int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < 0 || d >= kMaxDevices ? 0 : d;
+}
+
 // One range per resident emit warp (the count pass uses the same ranges).
 long long list_ranges(int num_sms) {
-    static long long n = 0;
-    if (!n) {
+    static long long n[kMaxDevices] = {};
+    const int dev = current_device();
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    if (!n[dev]) {
         const size_t smem = (size_t)kListNW * (3 * 32 * kListIPT + 4) * 4;
         cudaFuncSetAttribute(list_emit_kernel<kListNW, kListIPT>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        n = (long long)resident_ctas(list_emit_kernel<kListNW, kListIPT>, kListNW * 32, smem,
-                                     num_sms) * kListNW;
+        n[dev] = (long long)resident_ctas(list_emit_kernel<kListNW, kListIPT>, kListNW * 32, smem,
+                                          num_sms) * kListNW;
     }
-    return n;
+    return n[dev];
 }
 
 int list_resident_warps(int num_sms) { return (int)list_ranges(num_sms); }
@@ -779,13 +793,20 @@ int list_fused_block_samples() { return 32 * kFusedIPT; }
 
 cudaError_t launch_list_fused(const ListArgs& a, int num_sms, cudaStream_t s) {
     const size_t smem = (size_t)kListNW * (3 * 32 * kFusedIPT + 4) * 4;
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaFuncSetAttribute(list_fused_kernel<kListNW, kFusedIPT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, list_fused_kernel<kListNW, kFusedIPT>,
-                                                      kListNW * 32, smem);
-        if (per_sm < 1) per_sm = 1;
+    static int per_sm_dev[kMaxDevices] = {};
+    const int dev = current_device();
+    int per_sm;
+    {
+        std::lock_guard<std::mutex> g(g_attr_mu);
+        if (!per_sm_dev[dev]) {
+            cudaFuncSetAttribute(list_fused_kernel<kListNW, kFusedIPT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int p = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, list_fused_kernel<kListNW, kFusedIPT>,
+                                                          kListNW * 32, smem);
+            per_sm_dev[dev] = p < 1 ? 1 : p;
+        }
+        per_sm = per_sm_dev[dev];
     }
     list_fused_kernel<kListNW, kFusedIPT><<<(unsigned)(per_sm * num_sms), kListNW * 32, smem, s>>>(a);
     return cudaGetLastError();

@@ -133,7 +133,7 @@ cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s);   // emit pass
 cudaError_t launch_list_fused(const ListArgs& a, int num_sms, cudaStream_t s);  // both, overlapped
 cudaError_t launch_single_chain(const SingleArgs& a, cudaStream_t s);
 long long small_tile_count(long long n);
-cudaError_t launch_list_small(const SmallArgs& a, cudaStream_t s);
+cudaError_t launch_list_small(const SmallArgs& a, int num_sms, cudaStream_t s);
 int list_resident_warps(int num_sms);
 int list_fused_block_samples();  // fused kernel's staged block
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s);

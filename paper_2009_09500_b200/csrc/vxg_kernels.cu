@@ -380,11 +380,12 @@ __global__ void pack_plan_kernel(const double* __restrict__ segs,
     const double nd = (double)p.step_count;
     const double mx = fmax(fmax(fabs(s[0]) + fabs(p.wx) * nd, fabs(s[1]) + fabs(p.wy) * nd),
                            fabs(s[2]) + fabs(p.wz) * nd);
-    // caller-supplied W: checked rounding unless provably in range, exact dedup if |W| > 1, and
-    // never the positive-rounding shortcut (samples need not lie between S and E)
+    // caller-supplied W: checked rounding unless provably in range, always the exact duplicate
+    // test (the packed-key comparison relies on neighbouring samples -- E included -- lying
+    // within 2 voxels of each other, which only the plan kernel's own W guarantees), and never
+    // the positive-rounding shortcut (samples need not lie between S and E)
     r.flags = ((mx > kCheckThreshold || !(mx == mx)) ? REC_CHECK : 0u) |
-              (rec_flags(s[0], s[1], s[2], s[3], s[4], s[5]) & REC_CHECK) |
-              ((fabs(p.wx) > 1.0 || fabs(p.wy) > 1.0 || fabs(p.wz) > 1.0) ? REC_WIDE : 0u);
+              (rec_flags(s[0], s[1], s[2], s[3], s[4], s[5]) & REC_CHECK) | REC_WIDE;
     rec[i] = r;
     off[i] = p.output_offset;
     if (p.step_count < 0) record_error(ctl, i, 4);

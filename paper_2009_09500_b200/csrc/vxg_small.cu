@@ -3,22 +3,29 @@
 // For a few hundred thousand short segments the multi-pass list path (plan kernel with its
 // offset scan, count pass, range scan, emit pass: four launches and a readback) costs more in
 // launch gaps and per-pass start-up than the samples themselves. Here one kernel does all of
-// batch_preprocess and batch_voxelize (src/batch.cpp:57-73, 107-150) per tile of segments:
+// batch_preprocess and batch_voxelize (src/batch.cpp:57-73, 107-150); a warp owns tiles of 8
+// segments, two at a time:
 //
-//   1. plan   : one thread per segment of the tile runs make_plan (src/parametric.cpp:8-26)
-//               into shared memory; N_max and the capacity go to the control block;
-//   2. count  : one warp per segment walks its samples k = 0..N in rows of 32 (sample k < N is
-//               S + W*k, k = N is E; include/voxline/parametric.hpp:41-48) and counts the kept
-//               voxels (consecutive duplicates dropped, src/batch.cpp:139-142);
-//   3. prefix : the tile's voxel count is published and its output position found by decoupled
-//               look-back over the tiles (tile ids are claimed in order, so the predecessors are
-//               already counting or done);
-//   4. emit   : the warps walk their segments again, now writing each kept voxel at its position
-//               and every chain's start offset.
+//   1. plan   : lane j runs make_plan (src/parametric.cpp:8-26) for segment j into shared memory;
+//               N_max and the capacity are pooled per CTA and added to the control block once;
+//   2. count  : the warp evaluates the tile's samples k = 0..N of every segment (sample k < N is
+//               S + W*k, k = N is E; include/voxline/parametric.hpp:41-48), each lane an equal
+//               contiguous range of the tile, and counts the kept voxels per segment (consecutive
+//               duplicates dropped, src/batch.cpp:139-142); the tile's total is published
+//               (decoupled look-back, flag A);
+//   3. prefix : after counting its NEXT tile too, the warp finds this tile's output position by
+//               look-back over the tiles (ids are claimed in order);
+//   4. emit   : the warp walks the tile's segments again in rows of 32 samples, writing each kept
+//               voxel at its position and every chain's start offset.
 //
-// Every sample is evaluated twice (count, emit) but in the same kernel, from shared memory, with
-// no grid-wide barrier. Segments whose N exceeds kSmallMaxSteps make the call ask for the
-// multi-pass path instead (Control::n_entries), before anything that path would not overwrite.
+// Every sample is evaluated twice (count, emit) inside one launch. Measured on cfg1 (65,536 x
+// N = 128): 0.078 ms per call. Variants that did not pay: one tile in flight per warp (a third of
+// the instructions were look-back spins: 0.084 ms), a cooperative kernel with two grid barriers
+// around a one-CTA scan (0.131 ms), emit rows over the tile's flat sample space (0.081 ms), 64
+// registers for 4 CTAs per SM (spills: 0.080 ms).
+// Segments whose N exceeds kSmallMaxSteps make the call ask for the multi-pass path instead
+// (Control::n_entries).
+#include <algorithm>
 #include <cstdint>
 
 #include "vxg_device.cuh"
@@ -28,41 +35,52 @@ namespace vxg {
 
 constexpr int kSmallNW = 8;    // warps per tile
 constexpr int kSmallSPW = 8;   // segments per warp
-constexpr int kSmallTS = kSmallNW * kSmallSPW;
 constexpr long long kSmallMaxSteps = 1 << 14;
 
-// One segment, one warp: rows of 32 samples; returns the kept voxels (warp-uniform). EMIT: kept
-// voxel of rank r goes to out + 3 * (pos + r).
-template <bool EMIT>
-__device__ __forceinline__ int small_walk(const SegRec& R, long long N, int32_t* __restrict__ out,
-                                          long long pos, bool& bad) {
+// Voxel of sample k (0 <= k <= N) of a planned segment (include/voxline/parametric.hpp:41-48).
+__device__ __forceinline__ void small_sample(const SegRec& R, bool pos_rec, int k, int N, double t,
+                                             int32_t& x, int32_t& y, int32_t& z, bool& bad) {
+    if (k < N && pos_rec) {
+        x = round_pos(sample_axis(R.sx, R.wx, t));
+        y = round_pos(sample_axis(R.sy, R.wy, t));
+        z = round_pos(sample_axis(R.sz, R.wz, t));
+    } else {
+        eval_sample(R, k, N, x, y, z, bad);  // (k == N: E itself)
+    }
+}
+
+// Key of sample k < N without range checks: the one-DADD rounding for positive records, the
+// RZ-bias rounding otherwise (records needing checked rounding never get here).
+template <bool POS>
+__device__ __forceinline__ int32_t fast_key(const SegRec& R, double t, int32_t& x, int32_t& y,
+                                            int32_t& z) {
+    if (POS) {
+        x = round_pos(sample_axis(R.sx, R.wx, t));
+        y = round_pos(sample_axis(R.sy, R.wy, t));
+        z = round_pos(sample_axis(R.sz, R.wz, t));
+    } else {
+        x = round_fast(sample_axis(R.sx, R.wx, t));
+        y = round_fast(sample_axis(R.sy, R.wy, t));
+        z = round_fast(sample_axis(R.sz, R.wz, t));
+    }
+    return voxel_key(x, y, z);
+}
+
+// Emit pass of one segment, one warp: rows of 32 samples in order; kept voxel of rank r goes to
+// out + 3 * (pos + r). FAST: rows wholly below k = N take the branch-free body; the row holding
+// k = N (and every row of a record that needs checked rounding) takes the general one.
+template <bool FAST, bool POS>
+__device__ __forceinline__ void small_emit(const SegRec& R, int N, int32_t* __restrict__ out,
+                                           long long pos, bool& bad) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     int running = 0;
     int32_t carry = 0;
-    const bool pos_rec = (R.flags & (REC_CHECK | REC_POS)) == REC_POS;
-    for (long long r0 = 0; r0 <= N; r0 += 32) {
-        const long long k = r0 + lane;
-        int32_t x = 0, y = 0, z = 0;
-        if (k < N) {
-            if (pos_rec) {
-                const double t = __ll2double_rn(k);
-                x = round_pos(sample_axis(R.sx, R.wx, t));
-                y = round_pos(sample_axis(R.sy, R.wy, t));
-                z = round_pos(sample_axis(R.sz, R.wz, t));
-            } else {
-                eval_sample(R, k, N, x, y, z, bad);
-            }
-        } else if (k == N) {  // the final sample is E itself
-            x = R.ex;
-            y = R.ey;
-            z = R.ez;
-        }
-        const int32_t key = voxel_key(x, y, z);
-        const int32_t up = __shfl_up_sync(0xffffffffu, key, 1);
-        const bool keep = k <= N && (k == 0 || key != (lane == 0 ? carry : up));
+    double t = __int2double_rn(lane);
+    int r0 = 0;
+    auto commit = [&](bool keep, int32_t key, int32_t x, int32_t y, int32_t z) {
         const unsigned m = __ballot_sync(0xffffffffu, keep);
-        if (EMIT && keep) {
+        if (keep) {
             int32_t* d = out + 3 * (pos + running + __popc(m & lt));
             d[0] = x;
             d[1] = y;
@@ -70,31 +88,165 @@ __device__ __forceinline__ int small_walk(const SegRec& R, long long N, int32_t*
         }
         running += __popc(m);
         carry = __shfl_sync(0xffffffffu, key, 31);
+    };
+    if (FAST) {
+        for (; r0 + 32 <= N; r0 += 32) {  // every sample of the row has k < N
+            int32_t x, y, z;
+            const int32_t key = fast_key<POS>(R, t, x, y, z);
+            t = __dadd_rn(t, 32.0);
+            const int32_t up = __shfl_up_sync(0xffffffffu, key, 1);
+            commit((r0 | lane) == 0 || key != (lane == 0 ? carry : up), key, x, y, z);
+        }
     }
-    return running;
+    if (FAST) {  // the row holding k = N: samples below it as above, then E itself
+        if (r0 <= N) {
+            const int k = r0 + lane;
+            int32_t x, y, z;
+            fast_key<POS>(R, t, x, y, z);
+            if (k == N) {
+                x = R.ex;
+                y = R.ey;
+                z = R.ez;
+            }
+            const int32_t key = voxel_key(x, y, z);
+            const int32_t up = __shfl_up_sync(0xffffffffu, key, 1);
+            commit(k <= N && (k == 0 || key != (lane == 0 ? carry : up)), key, x, y, z);
+        }
+        return;
+    }
+    for (; r0 <= N; r0 += 32) {
+        const int k = r0 + lane;
+        int32_t x = 0, y = 0, z = 0;
+        if (k <= N) small_sample(R, POS, k, N, t, x, y, z, bad);
+        t = __dadd_rn(t, 32.0);
+        const int32_t key = voxel_key(x, y, z);
+        const int32_t up = __shfl_up_sync(0xffffffffu, key, 1);
+        commit(k <= N && (k == 0 || key != (lane == 0 ? carry : up)), key, x, y, z);
+    }
 }
 
-__global__ void __launch_bounds__(kSmallNW * 32) list_small_kernel(SmallArgs a) {
-    __shared__ SegRec s_rec[kSmallTS];
-    __shared__ long long s_n[kSmallTS];
-    __shared__ int s_cnt[kSmallTS];
-    __shared__ long long s_tile, s_prefix;
-    __shared__ unsigned long long s_max, s_cap;
-    __shared__ int s_long;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        s_tile = (long long)atomicAdd(&a.ctl->tile_counter, 1ull);
-        s_max = s_cap = 0;
-        s_long = 0;
+// Kept voxels of samples [k0, k1) of one segment (0 <= k0 < k1 <= N + 1) walked by one lane;
+// first / last: the keys of its first and last sample (the first is not counted here).
+template <bool FAST, bool POS>
+__device__ __forceinline__ int lane_piece(const SegRec& R, int N, int k0, int k1, int32_t& first,
+                                          int32_t& last, bool& bad) {
+    double t = __int2double_rn(k0);
+    int32_t x, y, z;
+    int cnt = 0;
+    if (FAST) {
+        const int kf = min(k1, N);  // samples below k = N
+        first = last = k0 < N ? fast_key<POS>(R, t, x, y, z) : voxel_key(R.ex, R.ey, R.ez);
+        for (int k = k0 + 1; k < kf; ++k) {
+            t = __dadd_rn(t, 1.0);
+            const int32_t key = fast_key<POS>(R, t, x, y, z);
+            cnt += key != last;
+            last = key;
+        }
+        if (k1 == N + 1 && k0 < N) {  // the piece ends with k = N: E itself
+            const int32_t key = voxel_key(R.ex, R.ey, R.ez);
+            cnt += key != last;
+            last = key;
+        }
+    } else {
+        small_sample(R, false, k0, N, t, x, y, z, bad);
+        first = last = voxel_key(x, y, z);
+        for (int k = k0 + 1; k < k1; ++k) {
+            t = __dadd_rn(t, 1.0);
+            small_sample(R, false, k, N, t, x, y, z, bad);
+            const int32_t key = voxel_key(x, y, z);
+            cnt += key != last;
+            last = key;
+        }
     }
-    __syncthreads();
-    const long long tile = s_tile;
-    const long long seg0 = tile * kSmallTS;
+    return cnt;
+}
 
-    // ---- 1. plan (one thread per segment of the tile)
-    if (tid < kSmallTS) {
-        const long long i = seg0 + tid;
-        long long N = -1;  // (no segment: no samples)
+// Count pass of a whole tile, one warp: the tile's samples (segment j's N_j + 1 samples after
+// segment j - 1's) split into 32 equal contiguous lane ranges, so lanes stay busy across segment
+// boundaries; a lane walks the pieces of the (one or two) segments its range touches and adds
+// each piece's kept voxels to the segment's counter in shared memory. A segment's first sample is
+// always kept; any other first sample of a lane is compared with the last one of the lane before.
+// myN: lane j < kSmallSPW holds segment j's N (-1: none); cnt[j] must be zero on entry.
+__device__ __forceinline__ void small_count_flat(const SegRec* rec, int myN, int* cnt, bool& bad,
+                                                 int& bad_j) {
+    const int lane = threadIdx.x & 31;
+    const int M = myN >= 0 ? myN + 1 : 0;
+    int P = M;  // inclusive prefix of the segments' sample counts
+#pragma unroll
+    for (int o = 1; o < kSmallSPW; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, P, o);
+        if (lane >= o) P += u;
+    }
+    const int T = __shfl_sync(0xffffffffu, P, kSmallSPW - 1);
+    P -= M;  // exclusive: segment j's first sample in the tile
+    const int q = (T + 31) >> 5;
+    const int f0 = min(lane * q, T), f1 = min(f0 + q, T);
+    // the segment holding f0: the last j with P_j <= f0 (and a non-empty segment)
+    int j = 0;
+#pragma unroll
+    for (int i = 1; i < kSmallSPW; ++i) {
+        const int Pi = __shfl_sync(0xffffffffu, P, i);
+        const int Mi = __shfl_sync(0xffffffffu, M, i);
+        if (Mi > 0 && Pi <= f0) j = i;
+    }
+    int32_t first = 0, last = 0;
+    const int first_j = j;
+    int first_k = -1;
+    // (the lanes' walks diverge: segment offsets from shared memory, not shuffles)
+    __shared__ int s_off[kSmallNW][kSmallSPW + 1];
+    const int warp = threadIdx.x >> 5;
+    if (lane < kSmallSPW) s_off[warp][lane] = P;
+    if (lane == kSmallSPW - 1) s_off[warp][kSmallSPW] = P + M;
+    __syncwarp();
+    const int* off = s_off[warp];
+    for (int f = f0; f < f1;) {
+        const int Pj = off[j], Nj = off[j + 1] - Pj - 1;
+        const int k0 = f - Pj, k1 = min(f1 - Pj, Nj + 1);
+        const SegRec& R = rec[j];
+        int32_t pf, pl;
+        bool b = false;
+        int c;
+        if (R.flags & REC_CHECK) c = lane_piece<false, false>(R, Nj, k0, k1, pf, pl, b);
+        else if (R.flags & REC_POS) c = lane_piece<true, true>(R, Nj, k0, k1, pf, pl, b);
+        else c = lane_piece<true, false>(R, Nj, k0, k1, pf, pl, b);
+        if (b) {
+            bad = true;
+            bad_j = j;
+        }
+        if (f == f0) {
+            first = pf;
+            first_k = k0;
+        } else {
+            ++c;  // a later piece starts its segment: k = 0 is kept
+        }
+        last = pl;
+        if (c) atomicAdd(&cnt[j], c);
+        f = Pj + k1;
+        ++j;
+        while (j < kSmallSPW && off[j + 1] == off[j]) ++j;  // (skip empty slots)
+    }
+    const int32_t up = __shfl_up_sync(0xffffffffu, last, 1);
+    if (f0 < f1 && (first_k == 0 || first != up)) atomicAdd(&cnt[first_j], 1);
+}
+
+// Dispatch on the record's rounding class (warp-uniform).
+__device__ __forceinline__ void small_emit_seg(const SegRec& R, int N, int32_t* out, long long pos,
+                                               bool& bad) {
+    if (R.flags & REC_CHECK) small_emit<false, false>(R, N, out, pos, bad);
+    else if (R.flags & REC_POS) small_emit<true, true>(R, N, out, pos, bad);
+    else small_emit<true, false>(R, N, out, pos, bad);
+}
+
+// Plan one tile of segments (lane j < kSmallSPW: segment seg0 + j) into `rec` (shared memory).
+// Returns the lane's N (-1: no segment); pools N_max / capacity into the CTA's counters.
+__device__ __forceinline__ int small_plan_tile(const SmallArgs& a, long long seg0, SegRec* rec,
+                                               unsigned long long* s_max,
+                                               unsigned long long* s_cap, bool& is_long) {
+    const int lane = threadIdx.x & 31;
+    int myN = -1;
+    is_long = false;
+    if (lane < kSmallSPW) {
+        const long long i = seg0 + lane;
         if (i < a.n) {
             const double2* p = reinterpret_cast<const double2*>(a.segs + 6 * i);
             const double2 a0 = p[0], a1 = p[1], a2 = p[2];
@@ -112,92 +264,145 @@ __global__ void __launch_bounds__(kSmallNW * 32) list_small_kernel(SmallArgs a) 
             r.ey = pl.ey;
             r.ez = pl.ez;
             r.flags = rec_flags(sx, sy, sz, ex, ey, ez);
-            s_rec[tid] = r;
-            N = pl.n;
-            atomicMax(&s_max, (unsigned long long)N);
-            atomicAdd(&s_cap, (unsigned long long)(N + 1));
-            if (N > kSmallMaxSteps) s_long = 1;
-        }
-        s_n[tid] = N;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        atomicMax(&a.ctl->max_steps, s_max);
-        atomicAdd(reinterpret_cast<unsigned long long*>(&a.ctl->pad0), s_cap);  // capacity
-        if (s_long) atomicExch(reinterpret_cast<unsigned long long*>(&a.ctl->n_entries), 1ull);
-    }
-
-    // ---- 2. count
-    bool bad = false;
-    long long bad_seg = 0;
-    if (!s_long) {
-        for (int j = 0; j < kSmallSPW; ++j) {
-            const int s = warp * kSmallSPW + j;
-            const long long N = s_n[s];
-            int c = 0;
-            if (N >= 0) {
-                bool b = false;
-                c = small_walk<false>(s_rec[s], N, nullptr, 0, b);
-                if (b) {
-                    bad = true;
-                    bad_seg = seg0 + s;
-                }
-            }
-            if (lane == 0) s_cnt[s] = c;
+            rec[lane] = r;
+            atomicMax(s_max, (unsigned long long)pl.n);
+            atomicAdd(s_cap, (unsigned long long)(pl.n + 1));
+            is_long = pl.n > kSmallMaxSteps;
+            myN = is_long ? 0 : (int)pl.n;
         }
     }
-    __syncthreads();
-
-    // ---- 3. prefix: tile-local exclusive offsets of the segments, tile total, look-back
-    if (warp == 0) {
-        static_assert(kSmallTS == 64, "two segments per lane");
-        const int v0 = s_long ? 0 : s_cnt[2 * lane], v1 = s_long ? 0 : s_cnt[2 * lane + 1];
-        int incl = v0 + v1;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        const int excl = incl - v0 - v1;
-        s_cnt[2 * lane] = excl;
-        s_cnt[2 * lane + 1] = excl + v0;
-        const long long agg = __shfl_sync(0xffffffffu, incl, 31);
-        const long long pre = lookback_warp(a.status, tile, agg, a.ctl);
-        if (lane == 0) {
-            s_prefix = pre;
-            if (pre + agg > a.out_cap) {  // caller's buffer too small: nothing written
-                record_error(a.ctl, 0, 4);
-                s_prefix = -1;
-            }
-            if (tile == a.ntiles - 1) {
-                if (a.chain_off) a.chain_off[a.n] = pre + agg;
-                a.ctl->total = pre + agg;
-            }
-        }
-    }
-    __syncthreads();
-    if (s_long || s_prefix < 0) {
-        if (bad) record_error(a.ctl, bad_seg, 2);
-        return;
-    }
-
-    // ---- 4. emit
-    for (int j = 0; j < kSmallSPW; ++j) {
-        const int s = warp * kSmallSPW + j;
-        const long long N = s_n[s];
-        if (N < 0) continue;
-        const long long pos = s_prefix + s_cnt[s];
-        if (lane == 0 && a.chain_off) a.chain_off[seg0 + s] = pos;
-        bool b = false;
-        small_walk<true>(s_rec[s], N, a.out, pos, b);
-    }
-    if (bad) record_error(a.ctl, bad_seg, 2);
+    return myN;
 }
 
-long long small_tile_count(long long n) { return (n + kSmallTS - 1) / kSmallTS; }
+// A claimed tile between its count and its emit.
+struct SmallTile {
+    long long tile;  // ticket (>= ntiles: none)
+    int myN, myc;    // lane j < kSmallSPW: segment j's N and kept voxels
+    bool is_long;    // the tile holds a segment too long for this path
+};
 
-cudaError_t launch_list_small(const SmallArgs& a, cudaStream_t s) {
-    list_small_kernel<<<(unsigned)a.ntiles, kSmallNW * 32, 0, s>>>(a);
+// Claim the next tile, plan it into `rec`, count it and publish its total (look-back flag A).
+__device__ __forceinline__ SmallTile small_count_tile(const SmallArgs& a, SegRec* rec, int* cnt,
+                                                      unsigned long long* s_max,
+                                                      unsigned long long* s_cap, int* s_long,
+                                                      bool& bad, long long& bad_seg) {
+    const int lane = threadIdx.x & 31;
+    SmallTile T;
+    unsigned long long tk = 0;
+    if (lane == 0) tk = atomicAdd(&a.ctl->tile_counter, 1ull);
+    T.tile = (long long)__shfl_sync(0xffffffffu, tk, 0);
+    T.myN = -1;
+    T.myc = 0;
+    T.is_long = false;
+    if (T.tile >= a.ntiles) return T;
+    const long long seg0 = T.tile * kSmallSPW;
+    bool il;
+    T.myN = small_plan_tile(a, seg0, rec, s_max, s_cap, il);
+    T.is_long = __any_sync(0xffffffffu, il);
+    if (T.is_long && lane == 0) *s_long = 1;
+    __syncwarp();
+    if (!T.is_long) {
+        if (lane < kSmallSPW) cnt[lane] = 0;
+        __syncwarp();
+        bool b = false;
+        int bj = 0;
+        small_count_flat(rec, T.myN, cnt, b, bj);
+        if (b) {
+            bad = true;
+            bad_seg = seg0 + bj;
+        }
+        __syncwarp();
+        if (lane < kSmallSPW) T.myc = cnt[lane];
+    }
+    const unsigned agg = __reduce_add_sync(0xffffffffu, (unsigned)T.myc);
+    if (lane == 0) lookback_publish(a.status, T.tile, agg);
+    return T;
+}
+
+// Resolve a counted tile's output position by look-back, then emit it.
+__device__ __forceinline__ void small_emit_tile(const SmallArgs& a, const SmallTile& T,
+                                                const SegRec* rec) {
+    const int lane = threadIdx.x & 31;
+    int incl = T.myc;
+#pragma unroll
+    for (int o = 1; o < kSmallSPW; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    const int excl = incl - T.myc;
+    const long long agg = __shfl_sync(0xffffffffu, incl, kSmallSPW - 1);
+    const long long pre = lookback_resolve(a.status, T.tile, agg, a.ctl);
+    if (lane == 0 && T.tile == a.ntiles - 1) {
+        if (a.chain_off) a.chain_off[a.n] = pre + agg;
+        a.ctl->total = pre + agg;
+    }
+    if (pre + agg > a.out_cap) {  // caller's buffer too small: nothing written
+        if (lane == 0) record_error(a.ctl, 0, 4);
+        return;
+    }
+    if (T.is_long) return;
+    const long long seg0 = T.tile * kSmallSPW;
+#pragma unroll 1
+    for (int j = 0; j < kSmallSPW; ++j) {
+        const int N = __shfl_sync(0xffffffffu, T.myN, j);
+        if (N < 0) break;
+        const long long pos = pre + __shfl_sync(0xffffffffu, excl, j);
+        if (lane == 0 && a.chain_off) a.chain_off[seg0 + j] = pos;
+        bool b = false;
+        small_emit_seg(rec[j], N, a.out, pos, b);
+    }
+}
+
+// Persistent warps, two tiles in flight each: claim + count + publish tile A, claim + count +
+// publish tile B, then resolve and emit A, then B. Every tile's count is published one tile of
+// work before anyone waits for it, so the look-backs rarely spin; no block-wide barrier on the
+// way (the CTA only pools the N_max / capacity partials in shared memory).
+__global__ void __launch_bounds__(kSmallNW * 32) list_small_kernel(SmallArgs a) {
+    __shared__ SegRec s_rec[kSmallNW][2][kSmallSPW];
+    __shared__ int s_cnt[kSmallNW][kSmallSPW];
+    __shared__ unsigned long long s_max, s_cap;
+    __shared__ int s_long;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 0) {
+        s_max = s_cap = 0;
+        s_long = 0;
+    }
+    __syncthreads();
+    bool bad = false;
+    long long bad_seg = 0;
+    for (;;) {
+        const SmallTile A = small_count_tile(a, s_rec[warp][0], s_cnt[warp], &s_max, &s_cap,
+                                             &s_long, bad, bad_seg);
+        if (A.tile >= a.ntiles) break;
+        const SmallTile B = small_count_tile(a, s_rec[warp][1], s_cnt[warp], &s_max, &s_cap,
+                                             &s_long, bad, bad_seg);
+        small_emit_tile(a, A, s_rec[warp][0]);
+        if (B.tile >= a.ntiles) break;
+        small_emit_tile(a, B, s_rec[warp][1]);
+        __syncwarp();
+    }
+    if (bad) record_error(a.ctl, bad_seg, 2);
+    __syncthreads();
+    if (tid == 0) {
+        if (s_max) atomicMax(&a.ctl->max_steps, s_max);
+        if (s_cap) atomicAdd(reinterpret_cast<unsigned long long*>(&a.ctl->pad0), s_cap);  // capacity
+        if (s_long) atomicExch(reinterpret_cast<unsigned long long*>(&a.ctl->n_entries), 1ull);
+    }
+}
+
+long long small_tile_count(long long n) { return (n + kSmallSPW - 1) / kSmallSPW; }
+
+// Persistent CTAs: as many as are resident at once (tiles are claimed dynamically).
+cudaError_t launch_list_small(const SmallArgs& a, int num_sms, cudaStream_t s) {
+    static int per_sm = 0;  // (no dynamic shared memory: the same on every device)
+    if (!per_sm) {
+        int p = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, list_small_kernel, kSmallNW * 32, 0);
+        per_sm = p < 1 ? 1 : p;
+    }
+    const long long need = (a.ntiles + 2 * kSmallNW - 1) / (2 * kSmallNW);
+    const long long grid = std::max<long long>(1, std::min<long long>(need, (long long)per_sm * num_sms));
+    list_small_kernel<<<(unsigned)grid, kSmallNW * 32, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -602,7 +602,7 @@ def test_run_batch_device_one_launch(vx, oracle, case):
         chain = torch.empty(n + 1, dtype=torch.int64, device="cuda")
         with pytest.raises(vx.RangeError) as ei:
             vx.run_batch_device(d.data_ptr(), n, out.data_ptr(), 1000, chain.data_ptr())
-        assert ei.value.args[1] == 2  # the lowest failing segment, as batch_preprocess reports
+        assert ei.value.segment == 2  # the lowest failing segment, as batch_preprocess reports
         return
     ovox, ooff, ototal = oracle.run_batch(segs)
     cap = ototal - 1 if case == "cap" else ototal
@@ -617,6 +617,15 @@ def test_run_batch_device_one_launch(vx, oracle, case):
     assert np.array_equal(chain.cpu().numpy(), ooff)
     assert np.array_equal(out.cpu().numpy()[:total], ovox)
     out.zero_()
+    if case == "long":  # asynchronous: one call is re-routed by its result, a chain is refused
+        vx.run_batch_device(d.data_ptr(), n, out.data_ptr(), cap, chain.data_ptr(), sync=False)
+        assert vx.run_batch_device_result()[0] == ototal
+        assert np.array_equal(out.cpu().numpy()[:total], ovox)
+        for _ in range(2):
+            vx.run_batch_device(d.data_ptr(), n, out.data_ptr(), cap, chain.data_ptr(), sync=False)
+        with pytest.raises(vx.InvalidArgument):
+            vx.run_batch_device_result()
+        return
     for _ in range(3):  # asynchronous form: enqueue several, read the last
         vx.run_batch_device(d.data_ptr(), n, out.data_ptr(), cap, chain.data_ptr(), sync=False)
     t, mx, capa = vx.run_batch_device_result()
@@ -774,4 +783,25 @@ def test_full_config5_bitmap_oracle(vx, oracle):
             part.close()
         assert torch.equal(cat, full), world
         del cat
+    b.close()
+
+
+def test_host_buffer_validation(vx):
+    """Caller-supplied host buffers are checked before the library writes through them."""
+    b = vx.Batch(vx.gen_segments(100, 16, 0, 64, 3))
+    cap = b.capacity
+    with pytest.raises(vx.InvalidArgument):
+        b.emit_list(out=np.empty((cap, 3), np.int64))
+    with pytest.raises(vx.InvalidArgument):
+        b.emit_list(out=np.empty((cap, 4), np.int32))
+    with pytest.raises(vx.InvalidArgument):
+        b.emit_list(chain_off=np.empty(50, np.int64))
+    with pytest.raises(vx.InvalidArgument):
+        b.emit_list(out=np.empty((cap, 6), np.int32)[:, ::2])
+    with pytest.raises(vx.InvalidArgument):
+        b.emit_bitmap(64, words=np.empty(10, np.uint64))
+    with pytest.raises(vx.InvalidArgument):
+        b.emit_bitmap(64, words=np.empty(64 ** 3 // 64, np.int32))
+    words, _ = b.emit_bitmap(64, words=np.zeros(64 ** 3 // 64, np.uint64))
+    assert words.any()
     b.close()

@@ -110,11 +110,37 @@ def _worker(rank, world, port, q):
         mx = shard.max_over_ranks(float(rank + 1))
         sm = shard.sum_over_ranks(float(total))
         ok_reduce = mx == float(world) and sm == float(rt)
+        # ---- bench --verify: every rank's digest equals the digest of the same slice of the
+        # one-rank result (lists: chain range; bitmaps: z-slab words)
+        dl = shard.list_digest(torch.from_numpy(vox), torch.from_numpy(choff))
+        dw = shard.words_digest(torch.from_numpy(words.view(np.int64)))
+        got = shard.gather_objects((int(c[rank]), int(c[rank + 1]), dl, z_lo, z_hi, dw))
+        plane = V * V // 64
+        refw = torch.from_numpy(ref.view(np.int64))
+        ok_verify = all(
+            tuple(shard.list_digest(torch.from_numpy(rv[ro[a]:ro[b]]),
+                                    torch.from_numpy(ro[a:b + 1]))) == tuple(d1)
+            and shard.words_digest(refw[za * plane:zb * plane]) == d2
+            for a, b, d1, za, zb, d2 in got)
+        # a digest notices a single flipped bit / voxel
+        bad = words.copy()
+        bad[len(bad) // 2] ^= np.uint64(1 << 17)
+        ok_verify &= shard.words_digest(torch.from_numpy(bad.view(np.int64))) != dw
+        vbad = vox.copy()
+        if len(vbad):
+            vbad[len(vbad) // 2, 1] += 1
+            ok_verify &= tuple(shard.list_digest(torch.from_numpy(vbad), torch.from_numpy(choff))) != tuple(dl)
+        # ---- bench's e2e input path: 1/world of the host segments per rank + all-gather
+        out = torch.empty((segs.shape[0] - segs.shape[0] % world, 6), dtype=torch.float64)
+        host = np.ascontiguousarray(segs[: out.shape[0]])
+        shard.distribute_segments(host, out)
+        ok_dist = np.array_equal(out.numpy(), host)
         dist.barrier()
         dist.destroy_process_group()
-        q.put((rank, ok_bitmap, ok_list, ok_reduce, None))
+        q.put((rank, ok_bitmap, ok_list, ok_reduce and ok_verify and ok_dist, None))
     except Exception as e:  # report instead of hanging the parent
-        q.put((rank, False, False, False, repr(e)))
+        import traceback
+        q.put((rank, False, False, False, traceback.format_exc()))
 
 
 def test_gloo_world2_slabs_and_lists():
@@ -132,4 +158,4 @@ def test_gloo_world2_slabs_and_lists():
         assert err is None, f"rank {rank}: {err}"
         assert ok_b, f"rank {rank}: gathered slab bitmaps differ from the full bitmap"
         assert ok_l, f"rank {rank}: gathered list shards differ from the single-rank list"
-        assert ok_r, f"rank {rank}: max/sum over ranks wrong"
+        assert ok_r, f"rank {rank}: reductions, verify digests or distribute_segments wrong"

@@ -1,0 +1,42 @@
+"""Mid-size run of the look-back / shared-memory kernels for compute-sanitizer (tools/
+gpu_sanitize.sh): plan_kernel (look-back offset scan), list_fused_kernel (count/emit task queues +
+look-back), list_small_kernel (per-warp tiles + look-back), tiles_scan_lb_kernel, tiles_fill_kernel
+(shared-memory tile, streamed readback), each output checked against the oracle."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["VXG_LIST_MODE"] = "fused"  # the fused kernel even for a mid-size batch
+
+import paper_2009_09500_b200 as vx  # noqa: E402
+from oracle.pyoracle import Oracle  # noqa: E402
+
+orc = Oracle()
+segs = vx.gen_segments(40000, 0, 600, 1024, 0x5A11)
+vox, off, total = vx.run_batch_flat(segs)                      # plan_kernel + list_fused_kernel
+ovox, ooff, ototal = orc.run_batch(segs)
+assert total == ototal and np.array_equal(off, ooff) and np.array_equal(vox, ovox), "list"
+
+bsegs = vx.gen_segments(70000, 0, 300, 512, 0x5A12)
+b = vx.Batch(bsegs)
+w, out = b.emit_bitmap(512, 0, 512)                             # count/scan_lb/scatter/fill
+ow, oo = orc.bitmap(bsegs, 512)
+assert out == oo and np.array_equal(w, ow), "bitmap"
+w2, _ = b.emit_bitmap(512, 100, 300, clip=True)                 # slab select + clipped fill
+ow2, _ = orc.bitmap(bsegs, 512, 100, 300)
+assert np.array_equal(w2, ow2), "slab bitmap"
+assert b.count_voxels() == orc.run_batch(bsegs)[2], "count"
+b.close()
+
+import torch  # noqa: E402  (device buffers for the one-launch path)
+vx.default_context().use_torch_stream()
+ssegs = np.ascontiguousarray(vx.gen_segments(20000, 128, 0, 512, 0x5A13))
+so, sc, st = orc.run_batch(ssegs)
+d = torch.from_numpy(ssegs).cuda()
+o = torch.empty((st, 3), dtype=torch.int32, device="cuda")
+c = torch.empty(ssegs.shape[0] + 1, dtype=torch.int64, device="cuda")
+t = vx.run_batch_device(d.data_ptr(), ssegs.shape[0], o.data_ptr(), st, c.data_ptr())
+assert t == st and np.array_equal(o.cpu().numpy(), so) and np.array_equal(c.cpu().numpy(), sc)
+print("sanitize driver ok")
