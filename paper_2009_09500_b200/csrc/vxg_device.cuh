@@ -100,6 +100,14 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+// cnt += (a != b) as one compare + one predicated add (the compiler's select-and-add form is
+// three instructions; this sits in the count loops' per-sample body)
+__device__ __forceinline__ void count_ne(int& cnt, int32_t a, int32_t b) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+        : "+r"(cnt)
+        : "r"(a), "r"(b));
+}
+
 // S + W*t with separate multiply and add (include/voxline/parametric.hpp:44-47).
 __device__ __forceinline__ double sample_axis(double s, double w, double t) {
     return __dadd_rn(s, __dmul_rn(w, t));

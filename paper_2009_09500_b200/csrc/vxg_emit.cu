@@ -171,6 +171,11 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
             // sample (a register) -- no shuffle, ballot or popc per sample; one shuffle joins
             // the sub-ranges and one warp reduction sums the counts
             const SegRec R = load_rec(a.rec + w.c);
+#if VXG_COUNT_PF
+            // the next segment's record (and flags) into L2 while this run is walked: the count
+            // tasks are the first to touch a range's records (from DRAM)
+            if (lane == 0 && w.c + 1 < a.nseg) prefetch_l2(a.rec + w.c + 1);
+#endif
             double t = __ll2double_rn(row_start - w.so_c + (long long)lane * nfast);
             int32_t first_key, key;
             int cnt = 0;
@@ -184,7 +189,7 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
                     const int32_t k2 = voxel_key(round_pos(sample_axis(R.sx, R.wx, t)),
                                                  round_pos(sample_axis(R.sy, R.wy, t)),
                                                  round_pos(sample_axis(R.sz, R.wz, t)));
-                    cnt += k2 != key;
+                    count_ne(cnt, k2, key);
                     key = k2;
                 }
             } else {
@@ -197,7 +202,7 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
                     const int32_t k2 = voxel_key(round_fast(sample_axis(R.sx, R.wx, t)),
                                                  round_fast(sample_axis(R.sy, R.wy, t)),
                                                  round_fast(sample_axis(R.sz, R.wz, t)));
-                    cnt += k2 != key;
+                    count_ne(cnt, k2, key);
                     key = k2;
                 }
             }

@@ -139,7 +139,7 @@ __device__ __forceinline__ int lane_piece(const SegRec& R, int N, int k0, int k1
         for (int k = k0 + 1; k < kf; ++k) {
             t = __dadd_rn(t, 1.0);
             const int32_t key = fast_key<POS>(R, t, x, y, z);
-            cnt += key != last;
+            count_ne(cnt, key, last);
             last = key;
         }
         if (k1 == N + 1 && k0 < N) {  // the piece ends with k = N: E itself
