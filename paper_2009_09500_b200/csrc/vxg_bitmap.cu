@@ -557,7 +557,8 @@ __global__ void __launch_bounds__(kScanBlock) tiles_scan_lb_kernel(TileArgs g) {
 // piece so the atomic's round trip overlaps the walk instead of stalling it.
 // (Deeper software pipelines -- 2 to 4 pieces in flight, their slots held in registers -- were
 // measured slower: 93 registers instead of 77 cost more warps than the overlap gained; cfg5
-// scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3.)
+// scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3. Batching 4-16 pieces per thread in shared
+// memory and issuing their atomics back to back did not pay either: 19.9 / 20.0 / 21.5 ms.)
 __global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
     const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (tix >= g.n) return;
