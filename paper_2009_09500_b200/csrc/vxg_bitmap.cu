@@ -755,7 +755,11 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         constexpr long long step = (long long)NW * PPW;
         // the piece entries run two steps ahead and their records are prefetched into L1 one
         // step ahead (a random 48-B gather per piece; registers are at the 64 limit, so no
-        // second PieceRef: the prefetch costs one instruction and no register)
+        // second PieceRef: the prefetch costs one instruction and no register). Measured on
+        // cfg5 (round 2): no prefetch, L2 or L1+L2 prefetches all within 1% (75.1-75.8 ms); the
+        // next step's records held in registers cost more than they hid (32 warps: 103 ms with
+        // spills; 24 warps: 77.8; 16 warps: 85.6); 24 warps without it: 75.45 ms (noise level);
+        // tiles claimed in 4x4x4 blocks cut the DRAM reads 109 -> 92 GB at the same time.
         long long pb = p0 + (long long)warp * PPW;
         const uint4* pcs = g.pieces;
         uint4 r1 = pb + grp < p1 ? pcs[pb + grp] : make_uint4(0u, 0u, 0u, 0u);
