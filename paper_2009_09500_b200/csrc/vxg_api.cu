@@ -672,7 +672,8 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
         // nothing to fill: the device words (zeroed or uploaded) go back as they are
         return host_words ? plain_readback() : VXG_OK;
     }
-    if (!b->entries.ensure(ctx, sizeof(uint4) * (size_t)npieces))
+    // 32-B piece records (vxg_bitmap.cu, make_piece)
+    if (!b->entries.ensure(ctx, 2 * sizeof(uint4) * (size_t)npieces))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory (%lld pieces)",
                          npieces);
     g.pieces = b->entries.as<uint4>();

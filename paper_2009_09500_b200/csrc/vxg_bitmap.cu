@@ -559,24 +559,7 @@ __global__ void __launch_bounds__(kScanBlock) tiles_scan_lb_kernel(TileArgs g) {
 // measured slower: 93 registers instead of 77 cost more warps than the overlap gained; cfg5
 // scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3. Batching 4-16 pieces per thread in shared
 // memory and issuing their atomics back to back did not pay either: 19.9 / 20.0 / 21.5 ms.)
-__global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
-    const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (tix >= g.n) return;
-    const long long i = walk_segment(g, tix);
-    const SegRec r = load_rec(g.rec + i);
-    bool pending = false;
-    unsigned pslot = 0;
-    uint4 pp = make_uint4(0, 0, 0, 0);
-    walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long ka, long long len, bool hasE) {
-        // store the previous piece first: its slot arrived while this piece was being walked;
-        // the new atomic's result lands directly in pslot and is not read until the next piece
-        if (pending) g.pieces[pslot] = pp;
-        pslot = atomicAdd(g.tile_cur + bin_of(t, len), 1u);  // 32-bit: one register
-        pp = make_uint4((uint32_t)i, (uint32_t)ka, (uint32_t)len | (hasE ? 0x80000000u : 0u), 0u);
-        pending = true;
-    });
-    if (pending) g.pieces[pslot] = pp;
-}
+__global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g);
 
 // Tile shape: 128 x 120 x 120 voxels (225.5 KB with the padding): near-cubic, so a segment crosses ~14
 // tile faces instead of the ~17 of a 256 x 80 x 80 tile -- fewer pieces to bin and to fill
@@ -595,76 +578,127 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-struct PieceRef {  // a decoded piece and its segment's S and W (E is loaded when needed)
-    double sx, sy, sz, wx, wy, wz;
-    long long ka;
-    unsigned seg;
-    int len;    // samples S + W*k (the E sample, if any, is extra)
-    bool hasE;
-};
-
-// Decode a piece entry and issue the loads of its segment's S and W.
-__device__ __forceinline__ void decode_piece(const TileArgs& g, const uint4 pc, PieceRef& q) {
-    q.hasE = (pc.z >> 31) != 0;
-    q.len = (int)(pc.z & 0x7fffffffu) - (q.hasE ? 1 : 0);
-    q.ka = pc.y;
-    q.seg = pc.x;
-    q.sx = q.sy = q.sz = q.wx = q.wy = q.wz = 0.0;
-    if (pc.z != 0u) {
-        const double2* r = reinterpret_cast<const double2*>(g.rec + pc.x);
-        const double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2);
-        q.sx = a.x;
-        q.sy = a.y;
-        q.sz = b.x;
-        q.wx = b.y;
-        q.wy = c.x;
-        q.wz = c.y;
-    }
-}
-
 // OR a bit into the tile through a 32-bit shared address.
 __device__ __forceinline__ void red_or_shared(uint32_t saddr, uint32_t bit) {
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(saddr), "r"(bit) : "memory");
 }
 
-// Set the bits of one piece group (G lanes per piece, 32/G pieces per warp). sbase: the shared
-// byte address of the tile's word 0 minus 4 * (the tile's global word base).
-// Lanes past their piece's end still compute a sample but OR it into their own scratch word
-// (`spare`, after the tile) instead of branching around the reduction: the row loop stays
-// straight-line (a select instead of a branch pair per sample).
-template <int G>
-__device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, uint32_t spare,
-                                           const PieceRef& q, int gl, const void* next_rec) {
-#if VXG_FILL_UNIFORM
-    int mx = q.len;
-#pragma unroll
-    for (int o = G; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    double t = __ll2double_rn(q.ka + gl);
-    const int steps = (mx + G - 1) / G;
-    int j = gl;
-#pragma unroll 4
-    for (int st = 0; st < steps; ++st) {
-        const int32_t x = round_pos(sample_axis(q.sx, q.wx, t));
-        const int32_t y = round_pos(sample_axis(q.sy, q.wy, t));
-        const int32_t z = round_pos(sample_axis(q.sz, q.wz, t));
-        const uint32_t w = (uint32_t)(z * kSS + y * kRW + (x >> 5));
-        red_or_shared(j < q.len ? sbase + 4u * w : spare, 1u << (x & 31));
-        t = __dadd_rn(t, (double)G);
-        j += G;
+// ------------------------------------------------------------------------ piece records
+// A piece (one segment's samples k in [ka, ka + n) inside one tile, plus E when hasE) is a
+// 32-B record -- one 256-bit store in the scatter pass, one 256-bit load in the fill -- written in
+// the fill's own terms, so that the fill reads its pieces sequentially and gathers no segment
+// record (except E's voxel, once per segment, and S/W in the rare exact redo):
+//
+//   fixed-point piece (REC_FX segment, n <= 255, ka < 2^24):
+//     w0..w2  A0 per axis (x, y, z): a 31-bit value v = rn(2^23 (c_ka - o)) + 2^23 (0.5 + M),
+//             i.e. the tile-local voxel coordinate of sample ka in bits 23-30 (0..128) and its
+//             23-bit fraction below
+//     w3..w5  D per axis: rn(2^30 W) as int32 (|W| <= 1)
+//     w6      segment | hasE << 31
+//     w7      ka | n << 24
+//   exact piece (every other segment -- caller plans, |coordinates| >= 2^24 -- or a long one):
+//     w0 segment, w1 ka, w2 (n + hasE) | hasE << 31, w3 = 0x80000000 (no D is that value)
+//
+// c_ka = fl(S + fl(W ka)) is the exact FP64 sample (include/voxline/parametric.hpp:44-47) and o
+// the tile origin; c_ka - o is exact (a multiple of ulp(c_ka) below 2^7).
+//
+// Exactness of the fixed-point samples. The fill works in 32.32 fixed point: A0 = v 2^9,
+// D = rn(2^30 W) 2^2, A_t = A0 + t D for sample k = ka + t. Sample k's voxel is floor(c_k + 0.5)
+// (llround: every in-tile sample is > -0.5), and
+//   |A_t / 2^32 - (c_k + 0.5 + M - o)| <= 2^-24 + t 2^-31 + 2 e1,
+// e1 = max |fl(S + fl(W k)) - (S + W k)| <= (|W k| + |c_k|) 2^-53 < 2^-27 for |S|, |E| < 2^24
+// (REC_FX) and in-volume samples. With t < 256 that is below 2^-24 + 2^-23 + 2^-26 < M = 2^-22.
+// So whenever the 32-bit fraction of A_t is >= 2M, floor(A_t / 2^32) = floor(c_k + 0.5) - o: the
+// high word IS the tile-local voxel coordinate, bit-exactly. A sample whose fraction is below 2M
+// on some axis (probability ~3 * 2^-21) makes its lane redo the piece in exact FP64.
+constexpr uint32_t kFxNear = 1u << 11;                      // 2M in units of 2^-32, M = 2^-22
+constexpr uint32_t kFxBias23 = (1u << 22) + (1u << 1);      // 2^23 (0.5 + M)
+constexpr uint32_t kPieceExact = 0x80000000u;               // w3 of an exact-format piece
+
+// (double)v for |v| < 2^51, exact, on the FP64 pipe (one DADD instead of an I2F)
+constexpr double kMagic52 = 0x1.8p52;
+__device__ __forceinline__ double small_to_double(long long v) {
+    return __dadd_rn(__longlong_as_double(0x4338000000000000ll + v), -kMagic52);
+}
+// The low word of rn(x) for |x| < 2^31 (two's complement), through the magic-number add (an
+// FP64-pipe op instead of an F2I on the slow conversion pipe).
+__device__ __forceinline__ uint32_t rn_low(double x) {
+    return (uint32_t)__double2loint(__dadd_rn(x, kMagic52));
+}
+
+struct Piece {
+    uint32_t w[8];
+};
+__device__ __forceinline__ void st_piece(uint4* p, const Piece& q) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(q.w[0]),
+                 "r"(q.w[1]), "r"(q.w[2]), "r"(q.w[3]), "r"(q.w[4]), "r"(q.w[5]), "r"(q.w[6]),
+                 "r"(q.w[7])
+                 : "memory");
+}
+__device__ __forceinline__ Piece ld_piece(const uint4* p) {
+    Piece q;
+    asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(q.w[0]), "=r"(q.w[1]), "=r"(q.w[2]), "=r"(q.w[3]), "=r"(q.w[4]),
+                   "=r"(q.w[5]), "=r"(q.w[6]), "=r"(q.w[7])
+                 : "l"(p));
+    return q;
+}
+
+// Build the piece record of (ka, len samples incl. E when hasE) of segment i (scatter pass).
+// D[]: rn(2^30 W) per axis (the segment's, computed once); fx: REC_FX and fixed-point enabled.
+__device__ __forceinline__ Piece make_piece(const SegRec& r, const uint32_t (&D)[3], bool fx,
+                                            long long z_lo, long long i, long long ka,
+                                            long long len, bool hasE) {
+    const long long n = len - (hasE ? 1 : 0);
+    Piece q;
+    if (!fx || n > 255 || ka >= (1ll << 24)) {
+        q.w[0] = (uint32_t)i;
+        q.w[1] = (uint32_t)ka;
+        q.w[2] = (uint32_t)len | (hasE ? 0x80000000u : 0u);
+        q.w[3] = kPieceExact;
+        q.w[4] = q.w[5] = q.w[6] = q.w[7] = 0u;
+        return q;
     }
-#else
-    (void)spare;
-    // every lane runs its own trip count: no per-sample bound test or select in the body (lanes
-    // whose piece is done idle until the warp's longest piece is); whole groups of 4 samples,
-    // then the remainder
-    double t = __ll2double_rn(q.ka + gl);
-    const int steps = q.len > gl ? (q.len - gl + G - 1) / G : 0;
+    const double sa[3] = {r.sx, r.sy, r.sz}, wa[3] = {r.wx, r.wy, r.wz};
+    const int tsz[3] = {kTX, kTY, kTZ};
+    const double t = small_to_double(ka);
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        q.w[ax] = 0u;
+        if (n > 0) {  // the tile origin from the anchor sample's voxel (it lies in the tile)
+            const long long org = ax == 2 ? z_lo : 0;
+            const double c = sample_axis(sa[ax], wa[ax], t);
+            const int v = round_pos(c);
+            const int o = (int)((v - org) / tsz[ax] * tsz[ax] + org);
+            q.w[ax] = rn_low(__dmul_rn(__dsub_rn(c, small_to_double(o)), 0x1p23)) + kFxBias23;
+        }
+        q.w[3 + ax] = D[ax];
+    }
+    q.w[6] = (uint32_t)i | (hasE ? 0x80000000u : 0u);
+    q.w[7] = (uint32_t)ka | (uint32_t)n << 24;
+    return q;
+}
+
+// Fixed-point helpers of the fill
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
+// Exact FP64 samples k = k0, k0 + G, ... (steps of them) of segment seg into the tile.
+template <int G>
+__device__ __forceinline__ void fill_exact(const TileArgs& g, uint32_t sbase, unsigned seg,
+                                           long long k0, int steps) {
+    const double2* rp = reinterpret_cast<const double2*>(g.rec + seg);
+    const double2 ra = __ldg(rp), rb = __ldg(rp + 1), rc = __ldg(rp + 2);
+    const double sx = ra.x, sy = ra.y, sz = rb.x, wx = rb.y, wy = rc.x, wz = rc.y;
+    double t = __ll2double_rn(k0);
     auto one = [&]() {
-        const int32_t x = round_pos(sample_axis(q.sx, q.wx, t));
-        const int32_t y = round_pos(sample_axis(q.sy, q.wy, t));
-        const int32_t z = round_pos(sample_axis(q.sz, q.wz, t));
-        const uint32_t w = (uint32_t)(z * kSS + y * kRW + (x >> 5));
-        red_or_shared(sbase + 4u * w, 1u << (x & 31));
+        const int32_t x = round_pos(sample_axis(sx, wx, t));
+        const int32_t y = round_pos(sample_axis(sy, wy, t));
+        const int32_t z = round_pos(sample_axis(sz, wz, t));
+        red_or_shared(sbase + 4u * (uint32_t)(z * kSS + y * kRW + (x >> 5)), 1u << (x & 31));
         t = __dadd_rn(t, (double)G);
     };
     for (int st = steps >> 2; st > 0; --st) {
@@ -673,15 +707,127 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, ui
         one();
         one();
     }
-    if ((g.pf & 4) && next_rec) prefetch_l1(next_rec);
     for (int st = steps & 3; st > 0; --st) one();
-    __syncwarp();
-#endif
-    if (q.hasE && gl == 0) {
-        const SegRec* r = g.rec + q.seg;
-        const int32_t ex = __ldg(&r->ex), ey = __ldg(&r->ey), ez = __ldg(&r->ez);
-        red_or_shared(sbase + 4u * (uint32_t)(ez * kSS + ey * kRW + (ex >> 5)), 1u << (ex & 31));
+}
+
+// Set the bits of one piece (G lanes per piece, 32/G pieces per warp step): lane gl takes the
+// samples ka + gl, ka + gl + G, ... Every lane runs its own trip count (lanes whose piece is done
+// idle until the warp's longest piece is). sbase: the shared byte address of the tile's word 0
+// minus 4 * (the tile's global word base); sloc: the shared byte address of word 0; spare: this
+// lane's scratch word after the tile.
+//
+// The fixed-point loop per sample: 3 x (64-bit add), a 3-way min of the fractions with the
+// near-boundary test (one predicate carries every sample's test: from the first near sample on,
+// the lane ORs into its spare word and redoes the piece exactly afterwards), the shared address
+// and the reduction -- no FP64. Pipe balance (the fma and alu pipes each take a warp instruction
+// every 2 cycles): the three 64-bit steps are IADD3 (alu) + IMAD.X (fma) pairs; the address is
+// IMADs; the min, the test, the select and the bit are alu -- about 14 instructions per sample.
+template <int G>
+__device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, uint32_t sloc,
+                                           uint32_t spare, const Piece& pc, int gl) {
+    if (pc.w[3] == kPieceExact) {  // exact-format piece: gather S and W, FP64 samples
+        const unsigned seg = pc.w[0];
+        const bool hasE = (pc.w[2] >> 31) != 0;
+        const int n = (int)(pc.w[2] & 0x7fffffffu) - (hasE ? 1 : 0);
+        const int steps = n > gl ? (n - gl + G - 1) / G : 0;
+        if (steps > 0) fill_exact<G>(g, sbase, seg, (long long)pc.w[1] + gl, steps);
+        __syncwarp();
+        if (hasE && gl == 0) {
+            const SegRec* r = g.rec + seg;
+            const int32_t ex = __ldg(&r->ex), ey = __ldg(&r->ey), ez = __ldg(&r->ez);
+            red_or_shared(sbase + 4u * (uint32_t)(ez * kSS + ey * kRW + (ex >> 5)), 1u << (ex & 31));
+        }
+        return;
     }
+    const unsigned seg = pc.w[6] & 0x7fffffffu;
+    const bool hasE = (pc.w[6] >> 31) != 0;
+    int32_t ex = 0, ey = 0, ez = 0;
+    if (hasE && gl == 0) {  // issued now, used after the samples
+        const SegRec* r = g.rec + seg;
+        ex = __ldg(&r->ex);
+        ey = __ldg(&r->ey);
+        ez = __ldg(&r->ez);
+    }
+    const int n = (int)(pc.w[7] >> 24);
+    const int steps = n > gl ? (n - gl + G - 1) / G : 0;
+    if (steps > 0) {
+        // 32.32 start of this lane (A0 + gl D) and step (G D); D = w << 2 as a 64-bit value. The
+        // step's words are formed with 32-bit shifts: from a visible 64-bit product ptxas makes
+        // each step one IMAD.WIDE, which occupies the fma pipe twice as long as the IADD3
+        // (alu) + IMAD.X (fma) pair and leaves the loop fma-bound (cfg5 fill 72.5 ms vs 58.5).
+        constexpr int kSh = 2 + (G >= 32 ? 5 : G >= 16 ? 4 : G >= 8 ? 3 : G >= 4 ? 2 : G >= 2 ? 1 : 0);
+        const int32_t wx = (int32_t)pc.w[3], wy = (int32_t)pc.w[4], wz = (int32_t)pc.w[5];
+        const unsigned long long ax = ((unsigned long long)pc.w[0] << 9) + (unsigned long long)((long long)gl * wx * 4),
+                                 ay = ((unsigned long long)pc.w[1] << 9) + (unsigned long long)((long long)gl * wy * 4),
+                                 az = ((unsigned long long)pc.w[2] << 9) + (unsigned long long)((long long)gl * wz * 4);
+        const uint32_t zero = (uint32_t)g.pf >> 24;  // 0, opaque to ptxas (see above)
+        const uint32_t dxl = (uint32_t)wx << kSh, dxh = (uint32_t)(wx >> (32 - kSh)) + zero,
+                       dyl = (uint32_t)wy << kSh, dyh = (uint32_t)(wy >> (32 - kSh)) + zero,
+                       dzl = (uint32_t)wz << kSh, dzh = (uint32_t)(wz >> (32 - kSh)) + zero;
+        uint32_t xl = (uint32_t)ax, yl = (uint32_t)ay, zl = (uint32_t)az;
+        uint32_t xh = (uint32_t)(ax >> 32), yh = (uint32_t)(ay >> 32), zh = (uint32_t)(az >> 32);
+        bool ok = true;
+        auto one_sample = [&]() {
+            ok = __vimin3_u32(xl, yl, zl) >= kFxNear && ok;
+            // z: IMAD (fma); y: LEA (alu); x >> 5: IMAD.HI (fma), + 4 (x >> 5): LEA (alu)
+            uint32_t a = mad_u32(zh, 4u * kSS, sloc) + (yh << 4);
+            a += __umulhi(xh, 1u << 27) << 2;
+            red_or_shared(ok ? a : spare, 1u << (xh & 31));
+            asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(xl), "+r"(xh) : "r"(dxl), "r"(dxh));
+            asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(yl), "+r"(yh) : "r"(dyl), "r"(dyh));
+            asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(zl), "+r"(zh) : "r"(dzl), "r"(dzh));
+        };
+        for (int st = steps >> 2; st > 0; --st) {
+            one_sample();
+            one_sample();
+            one_sample();
+            one_sample();
+        }
+        for (int st = steps & 3; st > 0; --st) one_sample();
+        if (!ok)  // (rare) a sample near a rounding boundary: redo this lane's samples exactly
+            fill_exact<G>(g, sbase, seg, (long long)(pc.w[7] & 0xffffffu) + gl, steps);
+    }
+    __syncwarp();
+    if (hasE && gl == 0)
+        red_or_shared(sbase + 4u * (uint32_t)(ez * kSS + ey * kRW + (ex >> 5)), 1u << (ex & 31));
+}
+
+// Pass B: write every piece's record (make_piece) into its tile's bin. tile_cur holds every bin's
+// start on entry (the scan wrote it), so the slot is one atomicAdd; the store of a piece is
+// deferred to the next piece so the atomic's round trip overlaps the walk instead of stalling it.
+// (Deeper software pipelines -- 2 to 4 pieces in flight, their slots held in registers -- were
+// measured slower in round 1: cfg5 scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3. Batching
+// 4-16 pieces per thread in shared memory and issuing their atomics back to back did not pay
+// either: 19.9 / 20.0 / 21.5 ms.)
+__global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
+    const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tix >= g.n) return;
+    const long long i = walk_segment(g, tix);
+    const SegRec r = load_rec(g.rec + i);
+    const bool fx = (r.flags & REC_FX) != 0u && !(g.pf & 8);  // (pf bit 3: tests, A/B)
+    uint32_t D[3] = {0u, 0u, 0u};  // rn(2^30 W)
+    if (fx) {
+        D[0] = rn_low(__dmul_rn(r.wx, 0x1p30));
+        D[1] = rn_low(__dmul_rn(r.wy, 0x1p30));
+        D[2] = rn_low(__dmul_rn(r.wz, 0x1p30));
+    }
+    // the pending piece is held as (ka, len | hasE << 31) and built when it is stored
+    bool pending = false;
+    unsigned pslot = 0, pka = 0, plen = 0;
+    auto store = [&]() {
+        st_piece(g.pieces + 2 * (size_t)pslot,
+                 make_piece(r, D, fx, g.z_lo, i, pka, plen & 0x7fffffffu, (plen >> 31) != 0u));
+    };
+    walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long ka, long long len, bool hasE) {
+        // store the previous piece first: its slot arrived while this piece was being walked;
+        // the new atomic's result lands directly in pslot and is not read until the next piece
+        if (pending) store();
+        pslot = atomicAdd(g.tile_cur + bin_of(t, len), 1u);  // 32-bit: one register
+        pka = (uint32_t)ka;
+        plen = (uint32_t)len | (hasE ? 0x80000000u : 0u);
+        pending = true;
+    });
+    if (pending) store();
 }
 
 // Tile claimed by fill ticket r: tiles are handed out in blocks of bx x by x bz tiles (x fastest
@@ -750,29 +896,21 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         const int x0 = (int)(txi * kTX), y0 = (int)(tyi * kTY), z0 = (int)(g.z_lo + tzi * kTZ);
         const int base = z0 * kSS + y0 * kRW + (x0 >> 5);  // (x0 is a multiple of 32)
         const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bits) - 4u * (uint32_t)base;
+        const uint32_t sloc = (uint32_t)__cvta_generic_to_shared(bits);
         const uint32_t spare = (uint32_t)__cvta_generic_to_shared(bits + kTileWords + lane);
-        // warp steps of 32/G pieces (G lanes per piece); a step's pieces load together
+        // warp steps of 32/G pieces (G lanes per piece); the next step's records (sequential
+        // 32-B reads) load while this step's are filled
         constexpr long long step = (long long)NW * PPW;
-        // the piece entries run two steps ahead and their records are prefetched into L1 one
-        // step ahead (a random 48-B gather per piece; registers are at the 64 limit, so no
-        // second PieceRef: the prefetch costs one instruction and no register). Measured on
-        // cfg5 (round 2): no prefetch, L2 or L1+L2 prefetches all within 1% (75.1-75.8 ms); the
-        // next step's records held in registers cost more than they hid (32 warps: 103 ms with
-        // spills; 24 warps: 77.8; 16 warps: 85.6); 24 warps without it: 75.45 ms (noise level);
-        // tiles claimed in 4x4x4 blocks cut the DRAM reads 109 -> 92 GB at the same time.
         long long pb = p0 + (long long)warp * PPW;
         const uint4* pcs = g.pieces;
-        uint4 r1 = pb + grp < p1 ? pcs[pb + grp] : make_uint4(0u, 0u, 0u, 0u);
-        uint4 r2 = pb + step + grp < p1 ? pcs[pb + step + grp] : make_uint4(0u, 0u, 0u, 0u);
+        Piece cur{};
+        if (pb + grp < p1) cur = ld_piece(pcs + 2 * (pb + grp));
         for (; pb < p1; pb += step) {
-            const SegRec* nrec = r2.z ? g.rec + r2.x : nullptr;
-            if (nrec && (g.pf & 1)) prefetch_l1(nrec);
-            if (nrec && (g.pf & 2)) prefetch_l2(nrec);
-            PieceRef q;
-            decode_piece(g, r1, q);
-            r1 = r2;
-            r2 = pb + 2 * step + grp < p1 ? pcs[pb + 2 * step + grp] : make_uint4(0u, 0u, 0u, 0u);
-            fill_piece<G>(g, sbase, spare, q, gl, nrec);
+            const long long pn = pb + step + grp;
+            Piece nxt{};
+            if (pn < p1) nxt = ld_piece(pcs + 2 * pn);
+            fill_piece<G>(g, sbase, sloc, spare, cur, gl);
+            cur = nxt;
         }
         __syncthreads();
         // OR the tile into the bitmap: a row of kTX bits is 4 words = 2 x 16 B; each thread
@@ -857,7 +995,9 @@ void launch_tiles_scan(const TileArgs& g, cudaStream_t s) {
 }
 void launch_tiles_scatter(const TileArgs& g, cudaStream_t s) {
     if (g.n <= 0) return;
-    tiles_scatter_kernel<<<(unsigned)((g.n + 255) / 256), 256, 0, s>>>(g);
+    TileArgs gg = g;
+    if (const char* e = getenv("VXG_FILL_PF")) gg.pf = atoi(e);  // bit 3: exact pieces only
+    tiles_scatter_kernel<<<(unsigned)((gg.n + 255) / 256), 256, 0, s>>>(gg);
 }
 template <int G, bool STREAM>
 static cudaError_t launch_fill_gs(const TileArgs& g, int num_sms, cudaStream_t s) {

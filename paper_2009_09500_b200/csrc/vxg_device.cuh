@@ -25,6 +25,8 @@ enum : uint32_t {
     REC_CHECK = 1u,  // samples can approach the int32 edge -> checked rounding, generic path
     REC_WIDE = 2u,   // some |W| > 1 (only from caller-supplied plans) -> exact dedup, generic path
     REC_POS = 4u,    // every coordinate of S and E >= 1: samples are positive, round = trunc(x+.5)
+    REC_FX = 8u,     // plan-kernel W and every |coordinate| of S and E < 2^24: the bitmap fill may
+                     // step samples in 32.32 fixed point (vxg_bitmap.cu, fill_piece)
 };
 
 // Voxel key for consecutive-duplicate tests: x + 8y + 64z (mod 2^32). Consecutive samples of one
@@ -159,7 +161,8 @@ __device__ __forceinline__ uint32_t rec_flags(double sx, double sy, double sz, d
                           fmax(fabs(ey), fabs(ez)));
     const double lo = fmin(fmin(fmin(sx, sy), fmin(sz, ex)), fmin(ey, ez));
     // samples lie between S and E up to a few ulp: all >= 1 - tiny > -0.5 when lo >= 1
-    return (m > kCheckThreshold ? REC_CHECK : 0u) | (lo >= 1.0 ? REC_POS : 0u);
+    return (m > kCheckThreshold ? REC_CHECK : 0u) | (lo >= 1.0 ? REC_POS : 0u) |
+           (m < 0x1p24 ? REC_FX : 0u);
 }
 
 // ----------------------------------------------------------------------------- SplitMix64

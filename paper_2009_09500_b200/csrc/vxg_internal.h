@@ -83,7 +83,7 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     long long* tile_cnt;              // ntiles * classes (zeroed): pieces per bin, then cursor
     long long* tile_off;              // ntiles * classes + 1: exclusive prefix
     unsigned* tile_cur;               // ntiles * classes: scatter cursors (pieces < 2^32)
-    uint4* pieces;                    // {segment, ka, len | hasE << 31, 0} binned by tile
+    uint4* pieces;                    // 32-B piece records (2 x uint4) binned by tile (vxg_bitmap.cu)
     unsigned long long* words;        // the slab's bitmap (OR-ed into)
     Control* ctl;                     // total: in-volume samples, n_entries: pieces
     int* perm;                        // walk order (segments grouped by length) or null

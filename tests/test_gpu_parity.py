@@ -371,6 +371,31 @@ def test_bitmap_streamed_readback(vx, oracle, monkeypatch, V, slab):
     far.close()
 
 
+def test_bitmap_fill_fixed_point_vs_exact(vx, oracle, monkeypatch):
+    """The fill's 32.32 fixed-point stepping (REC_FX records) against its exact-FP64 form
+    (VXG_FILL_PF bit 3) and the oracle: random long segments, tie lines (samples exactly on and
+    a few ulp beside half-integers: the near-boundary redo), the quarter grid, and segments that
+    start far outside the volume (|S| >= 2^24: no REC_FX, exact path) crossing it."""
+    rng = np.random.default_rng(2024)
+    V = 512
+    far = np.empty((4, 6))
+    far[:, 0] = -rng.uniform(2 ** 24, 2 ** 24 + 1000, 4)  # S.x far to the left
+    far[:, 1:3] = rng.uniform(10, V - 10, (4, 2))
+    far[:, 3:6] = rng.uniform(10, V - 10, (4, 3))
+    ties = _tie_lines(6000, 5, [0, 1, -1, 2, -2], hi=100)
+    segs = np.concatenate([vx.gen_segments(20000, 0, 400, V, 91), ties,
+                           np.abs(_quarter_grid(20000, 3)) * 3, far])
+    want, oo = oracle.bitmap(segs, V)
+    b = vx.Batch(segs)
+    got, out = b.emit_bitmap(V)
+    monkeypatch.setenv("VXG_FILL_PF", "9")  # L1 prefetch + exact FP64 fill
+    exact, out_e = b.emit_bitmap(V)
+    b.close()
+    assert np.array_equal(got, want)
+    assert np.array_equal(exact, want)
+    assert out == out_e == oo
+
+
 def test_select_slab_segments(vx, oracle):
     """The z-slab partitioner's device filter (vxg_select_slab_segments): a rank's slab of the
     bitmap from its filtered segments equals that slab of the full batch's bitmap (and the slab's
@@ -378,7 +403,7 @@ def test_select_slab_segments(vx, oracle):
     import torch
     from paper_2009_09500_b200.shard import select_slab_segments
     V = 1024
-    segs = np.concatenate([vx.gen_segments(20000, 0, 700, V, 91),
+    segs = np.concatenate([vx.gen_segments(20000, 0, 400, V, 91),
                            oracle.gen_batch(2000, 0, 300, 0, 92) * 3.0 - 200.0])
     d = torch.from_numpy(segs).cuda()
     local = torch.empty_like(d)
@@ -634,12 +659,12 @@ def test_run_batch_device_one_launch(vx, oracle, case):
     assert np.array_equal(out.cpu().numpy()[:total], ovox)
 
 
-def _tie_lines(n, seed, ulps):
+def _tie_lines(n, seed, ulps, hi=3000):
     """Axis-parallel and diagonal segments whose samples S + W*k land exactly on (or a few ulp
     beside) half-integers: W is an exact small dyadic step and S.x sits on/next to a tie."""
     rng = np.random.default_rng(seed)
     segs = np.empty((n, 6))
-    base = rng.integers(2, 3000, size=(n, 3)).astype(np.float64) + 0.5
+    base = rng.integers(2, hi, size=(n, 3)).astype(np.float64) + 0.5
     for i in range(n):
         u = ulps[i % len(ulps)]
         s = base[i].copy()

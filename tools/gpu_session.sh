@@ -12,13 +12,13 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 
 for w in cfg4 cfg1 cfg3 cfg5 cfg2; do
   timeout 900 python bench.py --workload $w --steps 20 --warmup 3 > $out/bench_$w.json 2> $out/bench_$w.err
 done
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_reference_cfg4.json 2> $out/bench_reference.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_reference_cfg5.json 2> $out/bench_reference.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
-  --log-file $out/launches_cfg4.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $out/ncu_bench.log 2>&1
+  --log-file $out/launches_cfg4.csv python bench.py --workload cfg4 --steps 2 --warmup 3 --no-e2e --no-cpu > $out/ncu_bench.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
   --log-file $out/launches_cfg5.csv python bench.py --workload cfg5 --steps 1 --warmup 3 --no-e2e --no-cpu > $out/ncu_bench5.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"list_(fused|count|emit)_kernel" -s 1 -c 1 \
-  -o $out/prof_cfg4 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof4.log 2>&1
+  -o $out/prof_cfg4 python bench.py --workload cfg4 --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof4.log 2>&1
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"tiles_(count|scatter|fill)" -s 3 -c 3 \
   -o $out/prof_cfg5 python bench.py --workload cfg5 --steps 1 --warmup 1 --no-e2e --no-cpu > $out/ncu_prof5.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tiles_fill" -s 1 -c 1 \
