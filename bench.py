@@ -58,8 +58,10 @@ WORKLOADS = {
 }
 DEFAULT_WORKLOAD = "cfg5"
 L2_BYTES = 126 * 1024 * 1024
-FP64_PEAK_TOPS = 18.42  # measured DADD/DMUL issue rate (tools/microbench_fp64.cu)
-FP64_PER_SAMPLE = 10    # 3 DMUL + 3 DADD (S + W*k) + 3 DADD.RM (llround) + 1 DADD (k)
+# the bitmap fill's inner loop: warp instructions per 32 in-tile samples (63 per 4-sample unrolled
+# iteration of fx_loop_int, read from cuobjdump -sass of tiles_fill_kernel<32, 2, false>)
+FILL_SLOTS_PER_ROW = 15.75
+SM_MAX_MHZ_FALLBACK = 1965.0  # B200 max SM clock (MEASURED_PEAKS.json sm_max_mhz)
 
 
 def peaks():
@@ -502,18 +504,28 @@ def main():
                     "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                     "algorithmic_bytes": alg_bytes, "peak_source": peak_src}
     else:
-        # the fill is bound by its exact FP64 evaluation (10 DADD/DMUL per sample), not by HBM:
-        # the bitmap it writes is 8 GiB for 68.8 G samples
-        fp64 = FP64_PER_SAMPLE * rank_samples / (emit_avg / 1e3) / 1e12
+        # The fill writes an 8 GiB bitmap for 68.8 G samples (cfg5): HBM is not its bound (the
+        # hbm object below). It is issue-bound: every in-tile sample costs its lane the fixed-
+        # point loop body, FILL_SLOTS_PER_ROW warp instructions per 32 samples (fx_loop_int in
+        # csrc/vxg_bitmap.cu, counted in the compiled SASS), against a peak of one warp
+        # instruction per cycle per SM sub-partition. frac = the share of the issue slots that do
+        # that work (the rest: per-piece setup, lanes idling at piece ends, stalls).
+        num_sms = torch.cuda.get_device_properties(local).multi_processor_count
+        sm_max_mhz = float(clocks.summary().get("sm_max_mhz") or 0.0) or SM_MAX_MHZ_FALLBACK
+        rows = rank_samples / 32.0
+        issue = FILL_SLOTS_PER_ROW * rows / (emit_avg / 1e3) / 1e9
+        issue_peak = 4 * num_sms * sm_max_mhz * 1e6 / 1e9
         alg_bytes = 8 * ((V * V * (z_hi - z_lo) + 63) // 64) + 48 * sel_n[0]
         achieved = alg_bytes / (emit_avg / 1e3) / 1e9
         dominant = "tiles_fill_kernel"
-        roofline = {"bound": "fp64", "achieved": fp64, "peak": FP64_PEAK_TOPS, "unit": "TOP/s",
-                    "frac": fp64 / FP64_PEAK_TOPS, "traffic": traffic,
-                    "traffic_source": traffic_src,
-                    "work": f"{FP64_PER_SAMPLE} FP64 ops x {rank_samples} samples of the slab",
-                    "peak_source": "measured DADD/DMUL issue rate on this pool's B200s "
-                                   "(tools/microbench_fp64.cu, profiles/r1_microbench_fp64.txt)",
+        roofline = {"bound": "issue", "achieved": issue, "peak": issue_peak,
+                    "unit": "G warp-instructions/s", "frac": issue / issue_peak,
+                    "traffic": traffic, "traffic_source": traffic_src,
+                    "work": f"{FILL_SLOTS_PER_ROW} loop instructions x {rank_samples} samples / 32 "
+                            "(32.32 fixed-point steps, the near-boundary test, the shared address "
+                            "and the shared-memory OR per sample)",
+                    "peak_source": f"4 sub-partitions x {num_sms} SMs x {sm_max_mhz:.0f} MHz "
+                                   "(one warp instruction per cycle each)",
                     "hbm": {"achieved": achieved, "peak": hbm, "unit": "GB/s",
                             "frac": achieved / hbm, "algorithmic_bytes": alg_bytes,
                             "peak_source": peak_src}}

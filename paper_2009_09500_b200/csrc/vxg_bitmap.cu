@@ -435,7 +435,9 @@ __global__ void __launch_bounds__(256) slab_select_kernel(TileArgs g, int* sel,
 }
 
 // Pass A: pieces per tile, in-volume samples.
-__global__ void __launch_bounds__(256) tiles_count_kernel(TileArgs g) {
+// (256, 3): at most 80 registers, 3 CTAs per SM -- 84 registers round to 88 and leave 2 CTAs,
+// 64 (4 CTAs) spill: cfg5 binning 35.5 / 32.3 / 33.2 ms for 2 / 3 / 4 CTAs (round 2)
+__global__ void __launch_bounds__(256, 3) tiles_count_kernel(TileArgs g) {
     const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     long long inside = 0, inbox = 0;
     if (tix < g.n) {
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(kScanBlock) tiles_scan_lb_kernel(TileArgs g) {
 // measured slower: 93 registers instead of 77 cost more warps than the overlap gained; cfg5
 // scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3. Batching 4-16 pieces per thread in shared
 // memory and issuing their atomics back to back did not pay either: 19.9 / 20.0 / 21.5 ms.)
-__global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g);
+__global__ void __launch_bounds__(256, 3) tiles_scatter_kernel(TileArgs g);
 
 // Tile shape: 128 x 120 x 120 voxels (225.5 KB with the padding): near-cubic, so a segment crosses ~14
 // tile faces instead of the ~17 of a 256 x 80 x 80 tile -- fewer pieces to bin and to fill
@@ -710,6 +712,53 @@ __device__ __forceinline__ void fill_exact(const TileArgs& g, uint32_t sbase, un
     for (int st = steps & 3; st > 0; --st) one();
 }
 
+// The fixed-point sample loop of a piece's lane (steps samples from A0 + gl D by G D, D = w << 2
+// in 32.32): OR each sample's bit into the tile; returns false if some sample lay near a rounding
+// boundary (from that sample on, the lane ORed into its spare word instead; the caller redoes the
+// lane exactly). Per sample: per axis a 64-bit add as LEA/IADD3 (alu) + IMAD.X (fma-heavy), a
+// 3-way min of the fractions and the near test (one predicate carries all samples' tests), the
+// shared address (IMADs), a select, the bit, the reduction: ~15.75 issue slots, the alu and
+// fma-heavy pipes (a warp instruction every 2 cycles each) about equally loaded.
+// Measured alternatives (cfg5 fill, round 2): ptxas fuses a visible 64-bit step into one
+// IMAD.WIDE, which holds the fma-heavy pipe 4 cycles -- 72.5 ms against 61.3 (hence the opaque
+// zero in the step's high word); FP64 accumulators 2^52 + A stepped by exact integer DADDs on the
+// idle FP64 pipe (12.75 slots per sample, the bit pattern's low word is the fraction): 63.7 ms,
+// latency-bound on the DADD -> address -> reduction chain; the same with two chains per axis:
+// 70.3 ms (register pressure at the 64-register cap).
+template <int G>
+__device__ __forceinline__ bool fx_loop_int(const TileArgs& g, const Piece& pc, int gl, int steps,
+                                            uint32_t sloc, uint32_t spare) {
+    constexpr int kSh = 2 + (G >= 32 ? 5 : G >= 16 ? 4 : G >= 8 ? 3 : G >= 4 ? 2 : G >= 2 ? 1 : 0);
+    const int32_t wx = (int32_t)pc.w[3], wy = (int32_t)pc.w[4], wz = (int32_t)pc.w[5];
+    const unsigned long long ax = ((unsigned long long)pc.w[0] << 9) + (unsigned long long)((long long)gl * wx * 4),
+                             ay = ((unsigned long long)pc.w[1] << 9) + (unsigned long long)((long long)gl * wy * 4),
+                             az = ((unsigned long long)pc.w[2] << 9) + (unsigned long long)((long long)gl * wz * 4);
+    const uint32_t zero = (uint32_t)g.pf >> 24;  // 0, opaque to ptxas
+    const uint32_t dxl = (uint32_t)wx << kSh, dxh = (uint32_t)(wx >> (32 - kSh)) + zero,
+                   dyl = (uint32_t)wy << kSh, dyh = (uint32_t)(wy >> (32 - kSh)) + zero,
+                   dzl = (uint32_t)wz << kSh, dzh = (uint32_t)(wz >> (32 - kSh)) + zero;
+    uint32_t xl = (uint32_t)ax, yl = (uint32_t)ay, zl = (uint32_t)az;
+    uint32_t xh = (uint32_t)(ax >> 32), yh = (uint32_t)(ay >> 32), zh = (uint32_t)(az >> 32);
+    bool ok = true;
+    auto one_sample = [&]() {
+        ok = __vimin3_u32(xl, yl, zl) >= kFxNear && ok;
+        uint32_t a = mad_u32(zh, 4u * kSS, sloc) + (yh << 4);
+        a += __umulhi(xh, 1u << 27) << 2;
+        red_or_shared(ok ? a : spare, 1u << (xh & 31));
+        asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(xl), "+r"(xh) : "r"(dxl), "r"(dxh));
+        asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(yl), "+r"(yh) : "r"(dyl), "r"(dyh));
+        asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(zl), "+r"(zh) : "r"(dzl), "r"(dzh));
+    };
+    for (int st = steps >> 2; st > 0; --st) {
+        one_sample();
+        one_sample();
+        one_sample();
+        one_sample();
+    }
+    for (int st = steps & 3; st > 0; --st) one_sample();
+    return ok;
+}
+
 // Set the bits of one piece (G lanes per piece, 32/G pieces per warp step): lane gl takes the
 // samples ka + gl, ka + gl + G, ... Every lane runs its own trip count (lanes whose piece is done
 // idle until the warp's longest piece is). sbase: the shared byte address of the tile's word 0
@@ -719,9 +768,7 @@ __device__ __forceinline__ void fill_exact(const TileArgs& g, uint32_t sbase, un
 // The fixed-point loop per sample: 3 x (64-bit add), a 3-way min of the fractions with the
 // near-boundary test (one predicate carries every sample's test: from the first near sample on,
 // the lane ORs into its spare word and redoes the piece exactly afterwards), the shared address
-// and the reduction -- no FP64. Pipe balance (the fma and alu pipes each take a warp instruction
-// every 2 cycles): the three 64-bit steps are IADD3 (alu) + IMAD.X (fma) pairs; the address is
-// IMADs; the min, the test, the select and the bit are alu -- about 14 instructions per sample.
+// and the reduction (fx_loop_int / fx_loop_dadd above).
 template <int G>
 __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, uint32_t sloc,
                                            uint32_t spare, const Piece& pc, int gl) {
@@ -751,39 +798,7 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, ui
     const int n = (int)(pc.w[7] >> 24);
     const int steps = n > gl ? (n - gl + G - 1) / G : 0;
     if (steps > 0) {
-        // 32.32 start of this lane (A0 + gl D) and step (G D); D = w << 2 as a 64-bit value. The
-        // step's words are formed with 32-bit shifts: from a visible 64-bit product ptxas makes
-        // each step one IMAD.WIDE, which occupies the fma pipe twice as long as the IADD3
-        // (alu) + IMAD.X (fma) pair and leaves the loop fma-bound (cfg5 fill 72.5 ms vs 58.5).
-        constexpr int kSh = 2 + (G >= 32 ? 5 : G >= 16 ? 4 : G >= 8 ? 3 : G >= 4 ? 2 : G >= 2 ? 1 : 0);
-        const int32_t wx = (int32_t)pc.w[3], wy = (int32_t)pc.w[4], wz = (int32_t)pc.w[5];
-        const unsigned long long ax = ((unsigned long long)pc.w[0] << 9) + (unsigned long long)((long long)gl * wx * 4),
-                                 ay = ((unsigned long long)pc.w[1] << 9) + (unsigned long long)((long long)gl * wy * 4),
-                                 az = ((unsigned long long)pc.w[2] << 9) + (unsigned long long)((long long)gl * wz * 4);
-        const uint32_t zero = (uint32_t)g.pf >> 24;  // 0, opaque to ptxas (see above)
-        const uint32_t dxl = (uint32_t)wx << kSh, dxh = (uint32_t)(wx >> (32 - kSh)) + zero,
-                       dyl = (uint32_t)wy << kSh, dyh = (uint32_t)(wy >> (32 - kSh)) + zero,
-                       dzl = (uint32_t)wz << kSh, dzh = (uint32_t)(wz >> (32 - kSh)) + zero;
-        uint32_t xl = (uint32_t)ax, yl = (uint32_t)ay, zl = (uint32_t)az;
-        uint32_t xh = (uint32_t)(ax >> 32), yh = (uint32_t)(ay >> 32), zh = (uint32_t)(az >> 32);
-        bool ok = true;
-        auto one_sample = [&]() {
-            ok = __vimin3_u32(xl, yl, zl) >= kFxNear && ok;
-            // z: IMAD (fma); y: LEA (alu); x >> 5: IMAD.HI (fma), + 4 (x >> 5): LEA (alu)
-            uint32_t a = mad_u32(zh, 4u * kSS, sloc) + (yh << 4);
-            a += __umulhi(xh, 1u << 27) << 2;
-            red_or_shared(ok ? a : spare, 1u << (xh & 31));
-            asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(xl), "+r"(xh) : "r"(dxl), "r"(dxh));
-            asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(yl), "+r"(yh) : "r"(dyl), "r"(dyh));
-            asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(zl), "+r"(zh) : "r"(dzl), "r"(dzh));
-        };
-        for (int st = steps >> 2; st > 0; --st) {
-            one_sample();
-            one_sample();
-            one_sample();
-            one_sample();
-        }
-        for (int st = steps & 3; st > 0; --st) one_sample();
+        const bool ok = fx_loop_int<G>(g, pc, gl, steps, sloc, spare);
         if (!ok)  // (rare) a sample near a rounding boundary: redo this lane's samples exactly
             fill_exact<G>(g, sbase, seg, (long long)(pc.w[7] & 0xffffffu) + gl, steps);
     }
@@ -799,7 +814,7 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, ui
 // measured slower in round 1: cfg5 scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3. Batching
 // 4-16 pieces per thread in shared memory and issuing their atomics back to back did not pay
 // either: 19.9 / 20.0 / 21.5 ms.)
-__global__ void __launch_bounds__(256) tiles_scatter_kernel(TileArgs g) {
+__global__ void __launch_bounds__(256, 3) tiles_scatter_kernel(TileArgs g) {
     const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (tix >= g.n) return;
     const long long i = walk_segment(g, tix);
@@ -999,9 +1014,8 @@ void launch_tiles_scatter(const TileArgs& g, cudaStream_t s) {
     if (const char* e = getenv("VXG_FILL_PF")) gg.pf = atoi(e);  // bit 3: exact pieces only
     tiles_scatter_kernel<<<(unsigned)((gg.n + 255) / 256), 256, 0, s>>>(gg);
 }
-template <int G, bool STREAM>
-static cudaError_t launch_fill_gs(const TileArgs& g, int num_sms, cudaStream_t s) {
-    constexpr int NW = 32;
+template <int NW, int G, bool STREAM>
+static cudaError_t launch_fill_nw(const TileArgs& g, int num_sms, cudaStream_t s) {
     const size_t smem = (size_t)(kTileWords + 32) * 4;  // the tile + 32 per-lane spare words
     cudaFuncSetAttribute(tiles_fill_kernel<NW, G, STREAM>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1013,6 +1027,13 @@ static cudaError_t launch_fill_gs(const TileArgs& g, int num_sms, cudaStream_t s
     if (grid > g.ntiles) grid = g.ntiles;
     tiles_fill_kernel<NW, G, STREAM><<<(unsigned)grid, NW * 32, smem, s>>>(g);
     return cudaGetLastError();
+}
+
+template <int G, bool STREAM>
+static cudaError_t launch_fill_gs(const TileArgs& g, int num_sms, cudaStream_t s) {
+    // 32 warps per CTA at 64 registers (one CTA per SM: the tile takes the shared memory);
+    // round 2, cfg5 fill: 61.35 ms at 32 warps, 61.45 at 24 (85 registers), 64.1 at 16
+    return launch_fill_nw<32, G, STREAM>(g, num_sms, s);
 }
 
 // (the streamed-readback signalling is a separate instantiation: the plain kernel stays as lean)
