@@ -271,6 +271,12 @@ vxg_status upload_segments(vxg_batch* b, const vxg_segment* segs, int64_t n, vxg
 
 Control* ctl_slot(vxg_batch* b, int i) { return b->ctl.as<Control>() + i; }
 
+// VXG_LIST_FX=0: the list walker's fast runs evaluate every sample in FP64 (tests, A/B)
+int list_fx_off() {
+    const char* e = std::getenv("VXG_LIST_FX");
+    return e && e[0] == '0' ? 1 : 0;
+}
+
 // Plan kernel + look-back scan (batch_preprocess).
 vxg_status run_plan(vxg_batch* b) {
     vxg_context* ctx = b->ctx;
@@ -393,7 +399,7 @@ vxg_status emit_list_device(vxg_batch* b, int32_t* d_out, int64_t out_cap, long 
                     range_len, rc, rc + 3 * nranges, d_out, out_cap, d_chain, ctl_slot(b, 1),
                     fused ? b->status.as<unsigned long long>() : nullptr,
                     std::max<int64_t>(1, (int64_t)(la_env * (double)warps)),
-                    deferred ? ctl_slot(b, 0) : nullptr};
+                    deferred ? ctl_slot(b, 0) : nullptr, list_fx_off()};
     cudaError_t e;
     if (fused) {
         cudaMemsetAsync(b->status.p, 0, sizeof(unsigned long long) * (size_t)nranges, ctx->stream);
@@ -449,7 +455,7 @@ vxg_status count_voxels_device(vxg_batch* b, int64_t* total) {
     long long* rc = b->ranges.as<long long>();
     vxg::ListArgs a{b->rec.as<SegRec>(), b->off.as<long long>(), b->n, b->capacity, nranges,
                     range_len, rc, rc + 3 * nranges, nullptr, 0, nullptr, ctl_slot(b, 1),
-                    nullptr, 1, nullptr};
+                    nullptr, 1, nullptr, list_fx_off()};
     cudaEventRecord(ctx->ev[2], ctx->stream);
     const cudaError_t e = vxg::launch_list_count(a, ctx->stream);
     ctx->launches += 2;

@@ -617,16 +617,6 @@ constexpr uint32_t kFxNear = 1u << 11;                      // 2M in units of 2^
 constexpr uint32_t kFxBias23 = (1u << 22) + (1u << 1);      // 2^23 (0.5 + M)
 constexpr uint32_t kPieceExact = 0x80000000u;               // w3 of an exact-format piece
 
-// (double)v for |v| < 2^51, exact, on the FP64 pipe (one DADD instead of an I2F)
-constexpr double kMagic52 = 0x1.8p52;
-__device__ __forceinline__ double small_to_double(long long v) {
-    return __dadd_rn(__longlong_as_double(0x4338000000000000ll + v), -kMagic52);
-}
-// The low word of rn(x) for |x| < 2^31 (two's complement), through the magic-number add (an
-// FP64-pipe op instead of an F2I on the slow conversion pipe).
-__device__ __forceinline__ uint32_t rn_low(double x) {
-    return (uint32_t)__double2loint(__dadd_rn(x, kMagic52));
-}
 
 struct Piece {
     uint32_t w[8];

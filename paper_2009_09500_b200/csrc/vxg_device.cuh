@@ -115,6 +115,57 @@ __device__ __forceinline__ double sample_axis(double s, double w, double t) {
     return __dadd_rn(s, __dmul_rn(w, t));
 }
 
+// ----------------------------------------------------------------------------- magic numbers
+// Integer <-> double conversions on the FP64 pipe (one DADD each) instead of the slow conversion
+// pipe (I2F / F2I): x + 1.5 2^52 rounds x to an integer (round to nearest) for |x| < 2^51, and the
+// low 52 bits of its bit pattern hold 2^51 + rn(x).
+constexpr double kMagic52 = 0x1.8p52;
+__device__ __forceinline__ double small_to_double(long long v) {  // exact for |v| < 2^51
+    return __dadd_rn(__longlong_as_double(0x4338000000000000ll + v), -kMagic52);
+}
+__device__ __forceinline__ uint32_t rn_low(double x) {  // rn(x) mod 2^32, |x| < 2^51
+    return (uint32_t)__double2loint(__dadd_rn(x, kMagic52));
+}
+__device__ __forceinline__ long long rn_i64(double x) {  // rn(x), |x| < 2^50
+    const long long b = __double_as_longlong(__dadd_rn(x, kMagic52));
+    return (b & 0xfffffffffffffll) - (1ll << 51);
+}
+
+// ----------------------------------------------------------------------------- fixed point
+// 32.32 fixed-point stepping of a segment's samples (the bitmap fill and the list fast runs).
+// Sample k is c_k = fl(S + fl(W k)) per axis (include/voxline/parametric.hpp:44-47); its voxel
+// is llround(c_k) = floor(c_k + 0.5) for c_k > -0.5. A lane starts from an exact FP64 sample c_t0:
+//   A_0 = round(c_t0) 2^32 + rn(2^32 (c_t0 - round(c_t0))) + (0.5 + M) 2^32,  D = rn(2^32 W),
+// (c_t0 - round(c_t0) is exact by Sterbenz for c_t0 >= 0.5) and steps A_j = A_0 + j m D for a
+// step of m samples. Then
+//   |A_j / 2^32 - (c_k + 0.5 + M)| <= 2^-33 + j m 2^-33 + 2 e1,
+// e1 = max |fl(S + fl(W k)) - (S + W k)| <= (|W k| + |c_k|) 2^-53 < 2^-26 for coordinates below
+// 2^24 (REC_FX). For j m <= 1023 that is below 2^-23 + 2^-25 < M = 2^-22, so whenever the 32-bit
+// fraction of A_j is >= 2M, its high word is llround(c_k) exactly. A sample whose fraction is
+// below 2M on some axis (probability ~3 * 2^-21) is evaluated in FP64 instead.
+constexpr uint32_t kFxNear22 = 1u << 11;                  // 2M in units of 2^-32, M = 2^-22
+constexpr long long kFxBias22 = (1ll << 31) + (1ll << 10);  // (0.5 + M) 2^32
+
+__device__ __forceinline__ void fx_start(double s, double w, double t, uint32_t& lo, uint32_t& hi) {
+    const double c = sample_axis(s, w, t);
+    const int32_t o = round_pos(c);
+    const long long A = ((long long)o << 32) +
+                        rn_i64(__dmul_rn(__dsub_rn(c, small_to_double(o)), 0x1p32)) + kFxBias22;
+    lo = (uint32_t)A;
+    hi = (uint32_t)((unsigned long long)A >> 32);
+}
+// m D = m rn(2^32 w) as (lo, hi), m a power of two
+__device__ __forceinline__ void fx_delta(double w, int shift, uint32_t& lo, uint32_t& hi) {
+    const long long d = rn_i64(__dmul_rn(w, 0x1p32)) << shift;
+    lo = (uint32_t)d;
+    hi = (uint32_t)((unsigned long long)d >> 32);
+}
+// (lo, hi) += (dlo, dhi): LEA/IADD3 (alu) + IMAD.X (fma) -- a 64-bit add that ptxas cannot fuse
+// into one IMAD.WIDE (which holds the fma-heavy pipe 4 cycles)
+__device__ __forceinline__ void fx_add(uint32_t& lo, uint32_t& hi, uint32_t dlo, uint32_t dhi) {
+    asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(lo), "+r"(hi) : "r"(dlo), "r"(dhi));
+}
+
 // ----------------------------------------------------------------------------- plan
 // make_plan (src/parametric.cpp:8-26). Returns false on a range error of either endpoint.
 struct Plan {

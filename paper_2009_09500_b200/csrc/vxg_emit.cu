@@ -176,10 +176,11 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
             // records). Measured with the same prefetch in the emit runs: cfg4 fused 10.84 ->
             // 10.67 ms; 2 or 4 records ahead and L1 prefetches were no better.
             if (lane == 0 && w.c + 1 < a.nseg) prefetch_l2(a.rec + w.c + 1);
-            double t = __ll2double_rn(row_start - w.so_c + (long long)lane * nfast);
+            const double t0 = __ll2double_rn(row_start - w.so_c + (long long)lane * nfast);
             int32_t first_key, key;
             int cnt = 0;
-            if (flags & REC_POS) {
+            auto exact_pos = [&](const SegRec& R) {  // FP64 samples, one-DADD rounding (REC_POS)
+                double t = t0;
                 first_key = key = voxel_key(round_pos(sample_axis(R.sx, R.wx, t)),
                                             round_pos(sample_axis(R.sy, R.wy, t)),
                                             round_pos(sample_axis(R.sz, R.wz, t)));
@@ -192,7 +193,38 @@ __device__ __forceinline__ int walk_block(const ListArgs& a, Walk& W, long long 
                     count_ne(cnt, k2, key);
                     key = k2;
                 }
+            };
+            if ((flags & (REC_POS | REC_FX)) == (REC_POS | REC_FX) && nfast <= 1023 &&
+                !(a.fx_off)) {
+                // 32.32 fixed-point steps (vxg_device.cuh): no FP64 per sample; a lane that meets
+                // a sample near a rounding boundary counts its sub-range again in FP64
+                uint32_t xl, xh, yl, yh, zl, zh, dxl, dxh, dyl, dyh, dzl, dzh;
+                fx_start(R.sx, R.wx, t0, xl, xh);
+                fx_start(R.sy, R.wy, t0, yl, yh);
+                fx_start(R.sz, R.wz, t0, zl, zh);
+                fx_delta(R.wx, 0, dxl, dxh);
+                fx_delta(R.wy, 0, dyl, dyh);
+                fx_delta(R.wz, 0, dzl, dzh);
+                bool ok = __vimin3_u32(xl, yl, zl) >= kFxNear22;
+                first_key = key = voxel_key((int32_t)xh, (int32_t)yh, (int32_t)zh);
+#pragma unroll 4
+                for (int f = 1; f < nfast; ++f) {
+                    fx_add(xl, xh, dxl, dxh);
+                    fx_add(yl, yh, dyl, dyh);
+                    fx_add(zl, zh, dzl, dzh);
+                    ok = __vimin3_u32(xl, yl, zl) >= kFxNear22 && ok;
+                    const int32_t k2 = voxel_key((int32_t)xh, (int32_t)yh, (int32_t)zh);
+                    count_ne(cnt, k2, key);
+                    key = k2;
+                }
+                if (!ok) {  // (rare; the record is reloaded: it is not kept live across the loop)
+                    cnt = 0;
+                    exact_pos(load_rec(a.rec + w.c));
+                }
+            } else if (flags & REC_POS) {
+                exact_pos(R);
             } else {
+                double t = t0;
                 first_key = key = voxel_key(round_fast(sample_axis(R.sx, R.wx, t)),
                                             round_fast(sample_axis(R.sy, R.wy, t)),
                                             round_fast(sample_axis(R.sz, R.wz, t)));

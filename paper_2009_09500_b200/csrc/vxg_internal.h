@@ -42,6 +42,7 @@ struct ListArgs {
     // the plan kernel earlier on the stream, range_len holds the block granularity and the
     // kernels do nothing if plan_ctl records a plan error
     const Control* plan_ctl;
+    int fx_off;                 // 1: FP64 samples in the fast runs too (tests, A/B; VXG_LIST_FX=0)
 };
 
 struct SmallArgs {           // one-launch run_batch of a small batch (list_small_kernel)

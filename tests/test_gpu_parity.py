@@ -485,6 +485,28 @@ def test_list_modes_match_oracle(vx, oracle, monkeypatch, mode):
         assert np.array_equal(vox, ovox)
 
 
+@pytest.mark.parametrize("mode", ["fused", "twopass"])
+def test_list_fixed_point_runs_vs_fp64(vx, oracle, monkeypatch, mode):
+    """The list walker's fast runs step REC_FX samples in 32.32 fixed point (vxg_device.cuh) and
+    re-evaluate samples near a rounding boundary in FP64: against the all-FP64 walker
+    (VXG_LIST_FX=0) and the oracle, on long random segments, tie lines (samples exactly on and a
+    few ulp beside half-integers) and coordinates up to just below 2^24 (REC_FX's bound)."""
+    monkeypatch.setenv("VXG_LIST_MODE", mode)
+    rng = np.random.default_rng(7)
+    big = rng.uniform(2 ** 24 - 5000, 2 ** 24 - 1, size=(3000, 6))
+    corpora = [vx.gen_segments(20000, 0, 2048, 4096, 321),
+               _tie_lines(20000, 13, [0, 1, -1, 2, -2, 3, -3]), big]
+    for segs in corpora:
+        ovox, ooff, ototal = oracle.run_batch(segs)
+        vox, off, total = vx.run_batch_flat(segs)
+        monkeypatch.setenv("VXG_LIST_FX", "0")
+        vox64, off64, total64 = vx.run_batch_flat(segs)
+        monkeypatch.delenv("VXG_LIST_FX")
+        assert total == total64 == ototal
+        assert np.array_equal(off, ooff) and np.array_equal(off64, ooff)
+        assert np.array_equal(vox, ovox) and np.array_equal(vox64, ovox)
+
+
 # ------------------------------------------------------------------ device-resident (torch)
 def test_torch_device_buffers(vx, oracle):
     import torch
