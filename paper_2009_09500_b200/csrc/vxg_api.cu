@@ -1396,7 +1396,9 @@ VXG_API vxg_status vxg_run_batch_device(vxg_context* ctx, const vxg_segment* seg
         st->h_ctl = nullptr;
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "run_batch_device: pinned memory");
     }
-    const long long ntiles = vxg::small_tile_count(n);
+    int spw = vxg::small_spw(n, ctx->num_sms);
+    if (const char* e = std::getenv("VXG_SMALL_SPW")) spw = std::atoi(e);  // (experiments)
+    const long long ntiles = vxg::small_tile_count(n, spw);
     if (!st->status.ensure(ctx, sizeof(unsigned long long) * (size_t)ntiles) ||
         !st->ctl.ensure(ctx, sizeof(Control)))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "run_batch_device: out of device memory");
@@ -1412,7 +1414,7 @@ VXG_API vxg_status vxg_run_batch_device(vxg_context* ctx, const vxg_segment* seg
     vxg::SmallArgs a{reinterpret_cast<const double*>(segs), n, ntiles,
                      reinterpret_cast<int32_t*>(out), out_cap,
                      reinterpret_cast<long long*>(chain_off),
-                     st->status.as<unsigned long long>(), st->ctl.as<Control>()};
+                     st->status.as<unsigned long long>(), st->ctl.as<Control>(), spw};
     const cudaError_t e = vxg::launch_list_small(a, ctx->num_sms, ctx->stream);
     ctx->launches++;
     if (e != cudaSuccess) return ctx->cuda_fail(e, "list_small_kernel");

@@ -53,6 +53,7 @@ struct SmallArgs {           // one-launch run_batch of a small batch (list_smal
     long long* chain_off;       // n + 1
     unsigned long long* status; // ntiles look-back words (zeroed)
     Control* ctl;               // total, max_steps, pad0 = capacity, n_entries = long segment
+    int spw;                    // segments per warp tile (small_spw)
 };
 
 struct SingleArgs {          // one segment, one CTA (single_chain_kernel)
@@ -133,7 +134,8 @@ cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s);  // count pass
 cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s);   // emit pass
 cudaError_t launch_list_fused(const ListArgs& a, int num_sms, cudaStream_t s);  // both, overlapped
 cudaError_t launch_single_chain(const SingleArgs& a, cudaStream_t s);
-long long small_tile_count(long long n);
+long long small_tile_count(long long n, int spw);
+int small_spw(long long n, int num_sms);
 cudaError_t launch_list_small(const SmallArgs& a, int num_sms, cudaStream_t s);
 int list_resident_warps(int num_sms);
 int list_fused_block_samples();  // fused kernel's staged block

@@ -19,10 +19,13 @@
 //               voxel at its position and every chain's start offset.
 //
 // Every sample is evaluated twice (count, emit) inside one launch. Measured on cfg1 (65,536 x
-// N = 128): 0.078 ms per call. Variants that did not pay: one tile in flight per warp (a third of
-// the instructions were look-back spins: 0.084 ms), a cooperative kernel with two grid barriers
-// around a one-CTA scan (0.131 ms), emit rows over the tile's flat sample space (0.081 ms), 64
-// registers for 4 CTAs per SM (spills: 0.080 ms).
+// N = 128): 0.078 ms per call (round 1); round 2: records copied from shared memory into
+// registers (the count loop re-read them per sample) 0.076 -> 0.074 ms, tiles sized so every
+// resident warp takes one pair (small_spw: 10 segments for cfg1) 0.078 -> 0.076, 32.32 fixed-point
+// count pieces (vxg_device.cuh) 0.074 -> 0.0696 ms. Variants that did not pay: one tile in flight
+// per warp (a third of the instructions were look-back spins: 0.084 ms), a cooperative kernel
+// with two grid barriers around a one-CTA scan (0.131 ms), emit rows over the tile's flat sample
+// space (0.081 ms), 64 registers for 4 CTAs per SM (spills: 0.080 ms).
 // Segments whose N exceeds kSmallMaxSteps make the call ask for the multi-pass path instead
 // (Control::n_entries).
 #include <algorithm>
@@ -34,7 +37,6 @@
 namespace vxg {
 
 constexpr int kSmallNW = 8;    // warps per tile
-constexpr int kSmallSPW = 8;   // segments per warp
 constexpr long long kSmallMaxSteps = 1 << 14;
 
 // Voxel of sample k (0 <= k <= N) of a planned segment (include/voxline/parametric.hpp:41-48).
@@ -133,6 +135,39 @@ __device__ __forceinline__ int lane_piece(const SegRec& R, int N, int k0, int k1
     double t = __int2double_rn(k0);
     int32_t x, y, z;
     int cnt = 0;
+    if (FAST && POS && (R.flags & REC_FX) && k0 < N) {
+        // 32.32 fixed-point steps (vxg_device.cuh); a lane that meets a sample near a rounding
+        // boundary counts its piece again in FP64 below
+        const int kf = min(k1, N);
+        uint32_t xl, xh, yl, yh, zl, zh, dxl, dxh, dyl, dyh, dzl, dzh;
+        fx_start(R.sx, R.wx, t, xl, xh);
+        fx_start(R.sy, R.wy, t, yl, yh);
+        fx_start(R.sz, R.wz, t, zl, zh);
+        fx_delta(R.wx, 0, dxl, dxh);
+        fx_delta(R.wy, 0, dyl, dyh);
+        fx_delta(R.wz, 0, dzl, dzh);
+        bool ok = kf - k0 <= 1024 && __vimin3_u32(xl, yl, zl) >= kFxNear22;
+        first = last = voxel_key((int32_t)xh, (int32_t)yh, (int32_t)zh);
+#pragma unroll 4
+        for (int k = k0 + 1; k < kf; ++k) {
+            fx_add(xl, xh, dxl, dxh);
+            fx_add(yl, yh, dyl, dyh);
+            fx_add(zl, zh, dzl, dzh);
+            ok = __vimin3_u32(xl, yl, zl) >= kFxNear22 && ok;
+            const int32_t key = voxel_key((int32_t)xh, (int32_t)yh, (int32_t)zh);
+            count_ne(cnt, key, last);
+            last = key;
+        }
+        if (ok) {
+            if (k1 == N + 1) {  // the piece ends with k = N: E itself
+                const int32_t key = voxel_key(R.ex, R.ey, R.ez);
+                cnt += key != last;
+                last = key;
+            }
+            return cnt;
+        }
+        cnt = 0;  // (rare) FP64 below
+    }
     if (FAST) {
         const int kf = min(k1, N);  // samples below k = N
         first = last = k0 < N ? fast_key<POS>(R, t, x, y, z) : voxel_key(R.ex, R.ey, R.ez);
@@ -167,6 +202,7 @@ __device__ __forceinline__ int lane_piece(const SegRec& R, int N, int k0, int k1
 // each piece's kept voxels to the segment's counter in shared memory. A segment's first sample is
 // always kept; any other first sample of a lane is compared with the last one of the lane before.
 // myN: lane j < kSmallSPW holds segment j's N (-1: none); cnt[j] must be zero on entry.
+template <int kSmallSPW>
 __device__ __forceinline__ void small_count_flat(const SegRec* rec, int myN, int* cnt, bool& bad,
                                                  int& bad_j) {
     const int lane = threadIdx.x & 31;
@@ -202,7 +238,7 @@ __device__ __forceinline__ void small_count_flat(const SegRec* rec, int myN, int
     for (int f = f0; f < f1;) {
         const int Pj = off[j], Nj = off[j + 1] - Pj - 1;
         const int k0 = f - Pj, k1 = min(f1 - Pj, Nj + 1);
-        const SegRec& R = rec[j];
+        const SegRec R = rec[j];  // (into registers: a shared-memory reference is re-read per sample)
         int32_t pf, pl;
         bool b = false;
         int c;
@@ -230,8 +266,9 @@ __device__ __forceinline__ void small_count_flat(const SegRec* rec, int myN, int
 }
 
 // Dispatch on the record's rounding class (warp-uniform).
-__device__ __forceinline__ void small_emit_seg(const SegRec& R, int N, int32_t* out, long long pos,
+__device__ __forceinline__ void small_emit_seg(const SegRec& Rs, int N, int32_t* out, long long pos,
                                                bool& bad) {
+    const SegRec R = Rs;  // (into registers: a shared-memory reference is re-read per row)
     if (R.flags & REC_CHECK) small_emit<false, false>(R, N, out, pos, bad);
     else if (R.flags & REC_POS) small_emit<true, true>(R, N, out, pos, bad);
     else small_emit<true, false>(R, N, out, pos, bad);
@@ -239,6 +276,7 @@ __device__ __forceinline__ void small_emit_seg(const SegRec& R, int N, int32_t* 
 
 // Plan one tile of segments (lane j < kSmallSPW: segment seg0 + j) into `rec` (shared memory).
 // Returns the lane's N (-1: no segment); pools N_max / capacity into the CTA's counters.
+template <int kSmallSPW>
 __device__ __forceinline__ int small_plan_tile(const SmallArgs& a, long long seg0, SegRec* rec,
                                                unsigned long long* s_max,
                                                unsigned long long* s_cap, bool& is_long) {
@@ -282,6 +320,7 @@ struct SmallTile {
 };
 
 // Claim the next tile, plan it into `rec`, count it and publish its total (look-back flag A).
+template <int kSmallSPW>
 __device__ __forceinline__ SmallTile small_count_tile(const SmallArgs& a, SegRec* rec, int* cnt,
                                                       unsigned long long* s_max,
                                                       unsigned long long* s_cap, int* s_long,
@@ -297,7 +336,7 @@ __device__ __forceinline__ SmallTile small_count_tile(const SmallArgs& a, SegRec
     if (T.tile >= a.ntiles) return T;
     const long long seg0 = T.tile * kSmallSPW;
     bool il;
-    T.myN = small_plan_tile(a, seg0, rec, s_max, s_cap, il);
+    T.myN = small_plan_tile<kSmallSPW>(a, seg0, rec, s_max, s_cap, il);
     T.is_long = __any_sync(0xffffffffu, il);
     if (T.is_long && lane == 0) *s_long = 1;
     __syncwarp();
@@ -306,7 +345,7 @@ __device__ __forceinline__ SmallTile small_count_tile(const SmallArgs& a, SegRec
         __syncwarp();
         bool b = false;
         int bj = 0;
-        small_count_flat(rec, T.myN, cnt, b, bj);
+        small_count_flat<kSmallSPW>(rec, T.myN, cnt, b, bj);
         if (b) {
             bad = true;
             bad_seg = seg0 + bj;
@@ -320,6 +359,7 @@ __device__ __forceinline__ SmallTile small_count_tile(const SmallArgs& a, SegRec
 }
 
 // Resolve a counted tile's output position by look-back, then emit it.
+template <int kSmallSPW>
 __device__ __forceinline__ void small_emit_tile(const SmallArgs& a, const SmallTile& T,
                                                 const SegRec* rec) {
     const int lane = threadIdx.x & 31;
@@ -357,6 +397,7 @@ __device__ __forceinline__ void small_emit_tile(const SmallArgs& a, const SmallT
 // publish tile B, then resolve and emit A, then B. Every tile's count is published one tile of
 // work before anyone waits for it, so the look-backs rarely spin; no block-wide barrier on the
 // way (the CTA only pools the N_max / capacity partials in shared memory).
+template <int kSmallSPW>
 __global__ void __launch_bounds__(kSmallNW * 32) list_small_kernel(SmallArgs a) {
     __shared__ SegRec s_rec[kSmallNW][2][kSmallSPW];
     __shared__ int s_cnt[kSmallNW][kSmallSPW];
@@ -371,14 +412,14 @@ __global__ void __launch_bounds__(kSmallNW * 32) list_small_kernel(SmallArgs a) 
     bool bad = false;
     long long bad_seg = 0;
     for (;;) {
-        const SmallTile A = small_count_tile(a, s_rec[warp][0], s_cnt[warp], &s_max, &s_cap,
+        const SmallTile A = small_count_tile<kSmallSPW>(a, s_rec[warp][0], s_cnt[warp], &s_max, &s_cap,
                                              &s_long, bad, bad_seg);
         if (A.tile >= a.ntiles) break;
-        const SmallTile B = small_count_tile(a, s_rec[warp][1], s_cnt[warp], &s_max, &s_cap,
+        const SmallTile B = small_count_tile<kSmallSPW>(a, s_rec[warp][1], s_cnt[warp], &s_max, &s_cap,
                                              &s_long, bad, bad_seg);
-        small_emit_tile(a, A, s_rec[warp][0]);
+        small_emit_tile<kSmallSPW>(a, A, s_rec[warp][0]);
         if (B.tile >= a.ntiles) break;
-        small_emit_tile(a, B, s_rec[warp][1]);
+        small_emit_tile<kSmallSPW>(a, B, s_rec[warp][1]);
         __syncwarp();
     }
     if (bad) record_error(a.ctl, bad_seg, 2);
@@ -390,20 +431,58 @@ __global__ void __launch_bounds__(kSmallNW * 32) list_small_kernel(SmallArgs a) 
     }
 }
 
-long long small_tile_count(long long n) { return (n + kSmallSPW - 1) / kSmallSPW; }
+long long small_tile_count(long long n, int spw) { return (n + spw - 1) / spw; }
+
+template <int SPW>
+static int small_per_sm() {
+    static int per_sm[64] = {0};  // per device (attributes are per device / context)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& p = per_sm[dev & 63];
+    if (!p) {
+        int q = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&q, list_small_kernel<SPW>, kSmallNW * 32, 0);
+        p = q < 1 ? 1 : q;
+    }
+    return p;
+}
+
+// Segments per warp tile: every resident warp takes two tiles at a time, so a batch whose tiles
+// all fit the resident warps in one round finishes in one tile-pair time -- the smallest tile
+// that does so (the critical path is one pair of tiles); bigger batches use 8-segment tiles.
+// (cfg1, 65,536 segments, 3 CTAs of 8 warps per SM: 8-segment tiles left 544 warps with a second
+// pair, 10-segment tiles give every warp one.)
+int small_spw(long long n, int num_sms) {
+    static const int opts[] = {4, 6, 8, 10, 12, 16};
+    for (int spw : opts) {
+        int per_sm = spw == 4 ? small_per_sm<4>() : spw == 6 ? small_per_sm<6>()
+                   : spw == 8 ? small_per_sm<8>() : spw == 10 ? small_per_sm<10>()
+                   : spw == 12 ? small_per_sm<12>() : small_per_sm<16>();
+        const long long warps = (long long)per_sm * num_sms * kSmallNW;
+        if ((small_tile_count(n, spw) + 1) / 2 <= warps) return spw;
+    }
+    return 8;
+}
 
 // Persistent CTAs: as many as are resident at once (tiles are claimed dynamically).
-cudaError_t launch_list_small(const SmallArgs& a, int num_sms, cudaStream_t s) {
-    static int per_sm = 0;  // (no dynamic shared memory: the same on every device)
-    if (!per_sm) {
-        int p = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, list_small_kernel, kSmallNW * 32, 0);
-        per_sm = p < 1 ? 1 : p;
-    }
+template <int SPW>
+static cudaError_t launch_small_spw(const SmallArgs& a, int num_sms, cudaStream_t s) {
     const long long need = (a.ntiles + 2 * kSmallNW - 1) / (2 * kSmallNW);
-    const long long grid = std::max<long long>(1, std::min<long long>(need, (long long)per_sm * num_sms));
-    list_small_kernel<<<(unsigned)grid, kSmallNW * 32, 0, s>>>(a);
+    const long long grid =
+        std::max<long long>(1, std::min<long long>(need, (long long)small_per_sm<SPW>() * num_sms));
+    list_small_kernel<SPW><<<(unsigned)grid, kSmallNW * 32, 0, s>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_list_small(const SmallArgs& a, int num_sms, cudaStream_t s) {
+    switch (a.spw) {
+        case 4: return launch_small_spw<4>(a, num_sms, s);
+        case 6: return launch_small_spw<6>(a, num_sms, s);
+        case 10: return launch_small_spw<10>(a, num_sms, s);
+        case 12: return launch_small_spw<12>(a, num_sms, s);
+        case 16: return launch_small_spw<16>(a, num_sms, s);
+        default: return launch_small_spw<8>(a, num_sms, s);
+    }
 }
 
 }  // namespace vxg
