@@ -668,9 +668,6 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     vxg_status s = read_ctl(ctx, g.ctl, c, "bitmap");
     if (s) return s;
     const long long npieces = c.n_entries;
-    if (npieces >= (1ll << 32))
-        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: %lld pieces exceed the 32-bit bin cursors; "
-                         "split the batch", npieces);
     const long long in_box = (long long)c.outside;  // samples inside the slab box
     if (outside) *outside = b->capacity - c.total;
     if (npieces == 0) {
@@ -678,10 +675,25 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
         // nothing to fill: the device words (zeroed or uploaded) go back as they are
         return host_words ? plain_readback() : VXG_OK;
     }
-    // 32-B piece records (vxg_bitmap.cu, make_piece)
-    if (!b->entries.ensure(ctx, 2 * sizeof(uint4) * (size_t)npieces))
-        return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory (%lld pieces)",
-                         npieces);
+    // More pieces than the 32-bit bin cursors count, or than the device holds as 32-B records:
+    // the slab is done as two thinner slabs (each a contiguous run of the words), recursively.
+    // The outside count is a property of the whole volume: the first half reports it.
+    long long max_pieces = 1ll << 32;
+    if (const char* e = std::getenv("VXG_BITMAP_MAX_PIECES")) max_pieces = std::atoll(e);  // tests
+    const bool fits = npieces < max_pieces &&
+                      b->entries.ensure(ctx, 2 * sizeof(uint4) * (size_t)npieces);
+    if (!fits) {
+        if (g.ntz < 2)
+            return ctx->fail(VXG_OUT_OF_MEMORY, -1,
+                             "bitmap: %lld pieces in one layer of tiles exceed the device", npieces);
+        const int64_t zm = z_lo + (g.ntz / 2) * g.tz;
+        const int64_t plane_words = V * V / 64;  // (V is a multiple of the tile width)
+        ls = LayerStream{};
+        s = emit_bitmap_tiles(b, d_words, V, z_lo, zm, nullptr, host_words);
+        if (s) return s;
+        return emit_bitmap_tiles(b, d_words + (zm - z_lo) * plane_words, V, zm, z_hi, nullptr,
+                                 host_words ? host_words + (zm - z_lo) * plane_words : nullptr);
+    }
     g.pieces = b->entries.as<uint4>();
     vxg::launch_tiles_scatter(g, ctx->stream);
     cudaEventRecord(ctx->ev[3], ctx->stream);

@@ -396,6 +396,27 @@ def test_bitmap_fill_fixed_point_vs_exact(vx, oracle, monkeypatch):
     assert out == out_e == oo
 
 
+@pytest.mark.parametrize("stream", [False, True])
+def test_bitmap_splits_slab_when_pieces_overflow(vx, oracle, monkeypatch, stream):
+    """More pieces than the bin cursors count (2^32; here a test bound of 2000) or than the device
+    holds: the tile path does the slab as two thinner slabs, recursively, instead of failing --
+    same words and outside count as the oracle, for the device readback and the streamed one."""
+    if stream:
+        monkeypatch.setenv("VXG_BITMAP_STREAM_MIN", "0")
+    segs = np.concatenate([vx.gen_segments(2000, 0, 300, 512, 33),
+                           oracle.gen_batch(200, 0, 100, 0, 34) * 4.0 - 30.0])
+    b = vx.Batch(segs)
+    for z0, z1 in [(0, 512), (37, 401)]:
+        monkeypatch.delenv("VXG_BITMAP_MAX_PIECES", raising=False)
+        _, out_whole = b.emit_bitmap(512, z0, z1)
+        monkeypatch.setenv("VXG_BITMAP_MAX_PIECES", "2000")
+        got, out = b.emit_bitmap(512, z0, z1)
+        want, _ = oracle.bitmap(segs, 512, z0, z1)
+        assert np.array_equal(got, want), (z0, z1)
+        assert out == out_whole
+    b.close()
+
+
 def test_select_slab_segments(vx, oracle):
     """The z-slab partitioner's device filter (vxg_select_slab_segments): a rank's slab of the
     bitmap from its filtered segments equals that slab of the full batch's bitmap (and the slab's
