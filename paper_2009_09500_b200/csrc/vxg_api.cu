@@ -629,7 +629,8 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     // (not for slabs thinner than a quarter of the volume: there the sort costs more than it
     // saves -- one rank of 8 on cfg5, measured)
     const bool perm = b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256 &&
-                      4 * (z_hi - z_lo) >= V && !std::getenv("VXG_BITMAP_NO_PERM");
+                      (4 * (z_hi - z_lo) >= V || std::getenv("VXG_BITMAP_PERM")) &&
+                      !std::getenv("VXG_BITMAP_NO_PERM");
     if (select || perm) {
         const size_t keys = (size_t)vxg::tile_perm_keys();
         if (!b->ent_off.ensure(ctx, keys * sizeof(long long) + sizeof(unsigned long long) +

@@ -26,6 +26,25 @@
 
 namespace vxg {
 
+// Tile shape: 128 x 120 x 120 voxels (225.5 KB with the padding): near-cubic, so a segment crosses ~14
+// tile faces instead of the ~17 of a 256 x 80 x 80 tile -- fewer pieces to bin and to fill
+// (cfg5: binning 38.4 -> 32.6 ms, fill 86.7 -> 83.1 ms; 128 x 112 x 112 and 256 x 88 x 80 were
+// in between). A row is 16 B of the bitmap, each tile's own (x0 is a multiple of 128).
+constexpr int kTX = 128, kTY = 120, kTZ = 120;
+constexpr int kRW = kTX / 32;          // 32-bit words per row
+constexpr int kSS = kRW * kTY + 1;     // words per z-slice (padded by one: bank skew per z step)
+constexpr int kTileWords = kSS * kTZ;
+
+// 1/w (0 for w == 0) for the crossing guesses only -- every guess is verified by exact samples,
+// so an approximate reciprocal will do: MUFU.RCP64H's ~20 bits and one Newton step (~40 bits),
+// instead of the IEEE division sequence.
+__device__ __forceinline__ double guess_rcp(double w) {
+    if (w == 0.0) return 0.0;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(w));
+    return __dmul_rn(r, __fma_rn(-w, r, 2.0));
+}
+
 // Exact rounded coordinate of sample k < N on one axis (any sign).
 __device__ __forceinline__ long long axis_round(double s, double w, long long k) {
     return (long long)round_fast(sample_axis(s, w, __ll2double_rn(k)));
@@ -122,9 +141,9 @@ __device__ __forceinline__ long long walk_cross(double s, double w, double inv_w
 template <typename Sink>
 __device__ __forceinline__ long long walk_pieces(const SegRec& r, long long N, const TileArgs& g,
                                                  Sink&& sink) {
-    const double invx = r.wx != 0.0 ? 1.0 / r.wx : 0.0;
-    const double invy = r.wy != 0.0 ? 1.0 / r.wy : 0.0;
-    const double invz = r.wz != 0.0 ? 1.0 / r.wz : 0.0;
+    const double invx = guess_rcp(r.wx);
+    const double invy = guess_rcp(r.wy);
+    const double invz = guess_rcp(r.wz);
     const bool e_vol = r.ex >= 0 && r.ex < g.V && r.ey >= 0 && r.ey < g.V && r.ez >= 0 &&
                        r.ez < g.V;
     // S itself is sample 0 (S + W*0 == S); sample N-1 (not E, which may sit a rounding away)
@@ -171,7 +190,7 @@ __device__ __forceinline__ long long walk_pieces(const SegRec& r, long long N, c
         // 32-bit walk (the tile path requires every N < 2^31): per axis the direction, the next
         // tile boundary B and the first k past it (khi: none); the tile id moves by strides.
         const int k0 = (int)klo, k1 = (int)khi;
-        const int tsz[3] = {g.tx, g.ty, g.tz};
+        constexpr int tsz[3] = {kTX, kTY, kTZ};  // (compile-time: divisions by constants)
         const int org[3] = {0, 0, (int)g.z_lo};
         const int stride[3] = {1, (int)g.ntx, (int)(g.ntx * g.nty)};
         const double sa[3] = {r.sx, r.sy, r.sz}, wa[3] = {r.wx, r.wy, r.wz},
@@ -215,7 +234,8 @@ __device__ __forceinline__ long long walk_pieces(const SegRec& r, long long N, c
         }
     }
     if (e_in) {
-        const long long tE = ((r.ez - g.z_lo) / g.tz * g.nty + r.ey / g.ty) * g.ntx + r.ex / g.tx;
+        const long long tE = ((long long)((int)(r.ez - g.z_lo) / kTZ) * g.nty + r.ey / kTY) * g.ntx +
+                             r.ex / kTX;
         if (last_tile == tE && last_end == N) {
             sink(last_tile, last_ka, last_end - last_ka + 1, true);
             last_tile = -1;
@@ -391,9 +411,9 @@ __global__ void __launch_bounds__(256) slab_select_kernel(TileArgs g, int* sel,
                 if (s_vol && l_vol && e_vol) {
                     inside = N + 1;
                 } else {
-                    const double invx = r.wx != 0.0 ? 1.0 / r.wx : 0.0;
-                    const double invy = r.wy != 0.0 ? 1.0 / r.wy : 0.0;
-                    const double invz = r.wz != 0.0 ? 1.0 / r.wz : 0.0;
+                    const double invx = guess_rcp(r.wx);
+                    const double invy = guess_rcp(r.wy);
+                    const double invz = guess_rcp(r.wz);
                     long long ax0, ax1, ay0, ay1, v0, v1;
                     axis_range(r.sx, r.wx, invx, N, 0, g.V, ax0, ax1);
                     axis_range(r.sy, r.wy, invy, N, 0, g.V, ay0, ay1);
@@ -563,14 +583,6 @@ __global__ void __launch_bounds__(kScanBlock) tiles_scan_lb_kernel(TileArgs g) {
 // memory and issuing their atomics back to back did not pay either: 19.9 / 20.0 / 21.5 ms.)
 __global__ void __launch_bounds__(256, 3) tiles_scatter_kernel(TileArgs g);
 
-// Tile shape: 128 x 120 x 120 voxels (225.5 KB with the padding): near-cubic, so a segment crosses ~14
-// tile faces instead of the ~17 of a 256 x 80 x 80 tile -- fewer pieces to bin and to fill
-// (cfg5: binning 38.4 -> 32.6 ms, fill 86.7 -> 83.1 ms; 128 x 112 x 112 and 256 x 88 x 80 were
-// in between). A row is 16 B of the bitmap, each tile's own (x0 is a multiple of 128).
-constexpr int kTX = 128, kTY = 120, kTZ = 120;
-constexpr int kRW = kTX / 32;          // 32-bit words per row
-constexpr int kSS = kRW * kTY + 1;     // words per z-slice (padded by one: bank skew per z step)
-constexpr int kTileWords = kSS * kTZ;
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);

@@ -1,12 +1,13 @@
-"""One rank's share of config 5 (rank R of N, sample-balanced slab), emitted twice -- for ncu
-launch lists. Usage: python tools/slab_one.py N R"""
+"""One rank's share of config 5 (rank R of N, sample-balanced slab) through bench.py's N > 1
+pipeline (device slab filter -> Batch -> clipped emit_bitmap), run twice -- for ncu launch lists.
+Usage: python tools/slab_one.py N R"""
 import sys
 
 import torch
 
 sys.path.insert(0, ".")
 import paper_2009_09500_b200 as vx  # noqa: E402
-from paper_2009_09500_b200.shard import sample_balanced_slabs  # noqa: E402
+from paper_2009_09500_b200.shard import sample_balanced_slabs, select_slab_segments  # noqa: E402
 
 N, R = int(sys.argv[1]), int(sys.argv[2])
 V, n = 4096, 64 * 1024 * 1024
@@ -18,8 +19,10 @@ bb = vx.Batch(None, ctx=ctx, device_ptr=d.data_ptr(), n=n)
 z0, z1 = sample_balanced_slabs(bb.slab_samples, V, N)[R]
 bb.close()
 words = torch.zeros(V * V * (z1 - z0) // 64, dtype=torch.int64, device="cuda")
+local = torch.empty_like(d)
 for _ in range(2):
-    b = vx.Batch(None, ctx=ctx, device_ptr=d.data_ptr(), n=n)
+    cnt = select_slab_segments(ctx, d.data_ptr(), n, z0, z1, local.data_ptr()) if N > 1 else n
+    b = vx.Batch(None, ctx=ctx, device_ptr=(local if N > 1 else d).data_ptr(), n=cnt)
     b.emit_bitmap_device(words.data_ptr(), V, z0, z1, True)
     b.close()
 torch.cuda.synchronize()
