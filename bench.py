@@ -58,9 +58,10 @@ WORKLOADS = {
 }
 DEFAULT_WORKLOAD = "cfg5"
 L2_BYTES = 126 * 1024 * 1024
-# the bitmap fill's inner loop: warp instructions per 32 in-tile samples (63 per 4-sample unrolled
-# iteration of fx_loop_int, read from cuobjdump -sass of tiles_fill_kernel<32, 2, false>)
-FILL_SLOTS_PER_ROW = 15.75
+# the bitmap fill's inner loop: warp instructions per 32 in-tile samples (62 per 4-sample unrolled
+# iteration of fx_loop_int, read from cuobjdump -sass of tiles_fill_kernel<32, 1, false>, the
+# instantiation cfg3 and cfg5 run)
+FILL_SLOTS_PER_ROW = 15.5
 SM_MAX_MHZ_FALLBACK = 1965.0  # B200 max SM clock (MEASURED_PEAKS.json sm_max_mhz)
 
 

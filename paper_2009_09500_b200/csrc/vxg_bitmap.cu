@@ -1048,10 +1048,10 @@ static cudaError_t launch_tiles_fill_g(const TileArgs& g, int num_sms, int G, cu
 
 // mean_len: mean samples per piece -> lanes per piece (VXG_FILL_G overrides: 4, 8, 16 or 32)
 cudaError_t launch_tiles_fill(const TileArgs& g, int num_sms, double mean_len, cudaStream_t s) {
-    // (measured with length-class bins and 128x120x120 tiles: G = 2 is best for the config-3
-    // and config-5 piece lengths -- cfg5 fill 79.7 ms against 83.4 (G = 4), 83.6 (G = 1), 93.5
-    // (G = 8); profiles/r1_fill_G for the earlier 256x80x80 sweep)
-    int G = mean_len < 160.0 ? 2 : (mean_len < 320.0 ? 16 : 32);
+    // (round 2, fixed-point fill: G = 1 is best for the config-3 and config-5 piece lengths --
+    // cfg5 fill 58.3 ms against 61.3 (G = 2) and 67.1 (G = 4); cfg3 1.18 / 1.29 / 1.67 ms. The
+    // exact FP64 fill of round 1 preferred G = 2: profiles/r1_fill_G)
+    int G = mean_len < 160.0 ? 1 : (mean_len < 320.0 ? 16 : 32);
     if (const char* e = getenv("VXG_FILL_G")) G = atoi(e);
     TileArgs gg = g;
     gg.pf = 1;
