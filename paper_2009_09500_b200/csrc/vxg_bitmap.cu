@@ -109,11 +109,11 @@ __device__ __forceinline__ long long axis_round_pos(double s, double w, long lon
 // 32-bit form of walk_cross for the tile walk (every N < 2^31 on the tile path).
 __device__ __forceinline__ int walk_cross32(double s, double w, double inv_w, int lo, int hi, int B,
                                             int dir) {
-    double gd = ceil(((double)B - 0.5 - s) * inv_w);
-    gd = fmin(fmax(gd, (double)lo), (double)hi);
-    const int g = (int)gd;
-    const int rg = g < hi ? round_pos(sample_axis(s, w, __int2double_rn(g))) : 0;
-    const int rp = g > lo ? round_pos(sample_axis(s, w, __int2double_rn(g - 1))) : 0;
+    // ceil + a saturating conversion in one (NaN -> 0), clamped as integers; the samples' k as
+    // doubles through the magic-number add (no I2F: the conversion pipe is the walk's slowest)
+    const int g = min(max(__double2int_ru(__dmul_rn(small_to_double(B) - 0.5 - s, inv_w)), lo), hi);
+    const int rg = g < hi ? round_pos(sample_axis(s, w, small_to_double(g))) : 0;
+    const int rp = g > lo ? round_pos(sample_axis(s, w, small_to_double(g - 1))) : 0;
     const bool at = g == hi || (dir > 0 ? rg >= B : rg < B);
     const bool before = g == lo || !(dir > 0 ? rp >= B : rp < B);
     if (at && before) return g;
