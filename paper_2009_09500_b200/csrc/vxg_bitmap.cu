@@ -282,15 +282,16 @@ __device__ __forceinline__ int len_bucket(long long N) {
 // near each other, so their pieces land in neighbouring bins (the scatter's writes and atomics
 // stay L2-local).
 __device__ __forceinline__ int perm_key(const TileArgs& g, long long i) {
-    const SegRec r = load_rec(g.rec + i);
-    const long long V = g.V, D = g.z_hi - g.z_lo;
-    auto cell = [](long long v, long long ext) {
-        const long long c = v < 0 ? 0 : (v >= ext ? ext - 1 : v);
-        return (int)(c * kCellsPerAxis / ext);
+    // (the order only steers performance: S's coarse cell from the record's first sector)
+    const double2 sxy = __ldg(reinterpret_cast<const double2*>(g.rec + i));
+    const double sz = __ldg(&g.rec[i].sz);
+    auto cell = [](double v, double lo, double ext) {
+        const int c = __double2int_rz(__dmul_rn(v - lo, (double)kCellsPerAxis / ext));
+        return min(max(c, 0), kCellsPerAxis - 1);
     };
-    const long long sx = axis_round(r.sx, r.wx, 0), sy = axis_round(r.sy, r.wy, 0),
-                    sz = axis_round(r.sz, r.wz, 0) - g.z_lo;
-    const int c = (cell(sz, D) * kCellsPerAxis + cell(sy, V)) * kCellsPerAxis + cell(sx, V);
+    const double V = (double)g.V;
+    const int c = (cell(sz, (double)g.z_lo, (double)(g.z_hi - g.z_lo)) * kCellsPerAxis +
+                   cell(sxy.y, 0.0, V)) * kCellsPerAxis + cell(sxy.x, 0.0, V);
     return len_bucket(seg_steps(g, i)) * (kCellsPerAxis * kCellsPerAxis * kCellsPerAxis) + c;
 }
 
