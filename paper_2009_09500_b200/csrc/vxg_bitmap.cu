@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(kScanBlock) tiles_scan_lb_kernel(TileArgs g) {
 // measured slower: 93 registers instead of 77 cost more warps than the overlap gained; cfg5
 // scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3. Batching 4-16 pieces per thread in shared
 // memory and issuing their atomics back to back did not pay either: 19.9 / 20.0 / 21.5 ms.)
-__global__ void __launch_bounds__(256, 3) tiles_scatter_kernel(TileArgs g);
+__global__ void __launch_bounds__(256, 4) tiles_scatter_kernel(TileArgs g);
 
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
@@ -828,7 +828,7 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, ui
 // measured slower in round 1: cfg5 scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3. Batching
 // 4-16 pieces per thread in shared memory and issuing their atomics back to back did not pay
 // either: 19.9 / 20.0 / 21.5 ms.)
-__global__ void __launch_bounds__(256, 3) tiles_scatter_kernel(TileArgs g) {
+__global__ void __launch_bounds__(256, 4) tiles_scatter_kernel(TileArgs g) {
     const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (tix >= g.n) return;
     const long long i = walk_segment(g, tix);
