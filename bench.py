@@ -443,6 +443,8 @@ def main():
             if cnt == 0:  # (no segment reaches this slab: nothing to do)
                 return 0, 0, 0, 0
         b = vx.Batch(None, ctx=ctx, device_ptr=src, n=cnt)
+        if slab_segs is not None:
+            b.set_slab(z_lo, z_hi)  # (filtered above: the tile path skips its own filter)
         if kind in ("list", "single"):
             units = b.emit_list_device(out.data_ptr(), capacity, chain.data_ptr())
         else:
@@ -638,6 +640,8 @@ def run_e2e(vx, shard, ctx, torch, d_segs, cfg, kind, n, s0, s1, units, capacity
                                                  sel.data_ptr())
                 src = sel.data_ptr()
             b = vx.Batch(None, ctx=ctx, device_ptr=src, n=cnt)
+            if sel is not None:
+                b.set_slab(z_lo, z_hi)
             b.emit_bitmap(V, z_lo, z_hi, clip=True, words=words_h, overwrite=True)
         b.close()
         dt = time.perf_counter() - t0

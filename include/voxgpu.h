@@ -184,6 +184,11 @@ VXG_API vxg_status vxg_select_slab_segments(vxg_context* ctx, const vxg_segment*
                                             int64_t* n_out);
 VXG_API vxg_status vxg_batch_slab_samples(vxg_batch* b, int64_t z_lo, int64_t z_hi,
                                           int64_t* samples);
+/* The caller states that every segment of the batch may reach planes [z_lo, z_hi) -- e.g. they
+ * came out of vxg_select_slab_segments for that slab: bitmaps of slabs inside it then skip the
+ * tile path's own slab filter (which would keep every segment). Purely a shortcut: the output is
+ * the same either way. */
+VXG_API vxg_status vxg_batch_set_slab(vxg_batch* b, int64_t z_lo, int64_t z_hi);
 /* GPU time (ns, CUDA events) on this batch of the last plan kernel + offset scan (preprocess_ns),
  * the dominant output kernel (kernel_ns: list emit pass or bitmap tile fill) and the auxiliary
  * passes before it (assemble_ns: list count pass + range scan, or the bitmap binning passes). */

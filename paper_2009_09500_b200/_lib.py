@@ -111,6 +111,7 @@ SIGNATURES = {
     "vxg_voxelize_parametric": (C.c_int, [_vp, _vp, _vp, _i64, _i64p]),
     "vxg_chain_length_bounds": (C.c_int, [_vp, _vp, _i64p, _i64p]),
     "vxg_batch_create": (C.c_int, [_vp, _vp, _i64, C.c_int, C.POINTER(_vp)]),
+    "vxg_batch_set_slab": (C.c_int, [_vp, _i64, _i64]),
     "vxg_batch_from_plan": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, C.POINTER(_vp)]),
     "vxg_batch_destroy": (None, [_vp]),
     "vxg_batch_info": (C.c_int, [_vp, _i64p, _i64p, _i64p]),

@@ -183,6 +183,13 @@ class Batch:
         self._info = None  # (max_steps, capacity): read back on first use (vxg_batch_info)
         self._plans = None
 
+    def set_slab(self, z_lo: int, z_hi: int) -> "Batch":
+        """State that every segment may reach planes [z_lo, z_hi) (e.g. the output of
+        shard.select_slab_segments): bitmaps of slabs inside it skip the tile path's own slab
+        filter (vxg_batch_set_slab). Returns self."""
+        self.ctx.check(self.ctx.lib.vxg_batch_set_slab(self.h, z_lo, z_hi))
+        return self
+
     def resolve(self):
         """Read the plan's N_max / capacity back (raises the plan's error, if any). A device-
         resident batch defers this; emit_list_device resolves it in its own readback."""

@@ -178,6 +178,7 @@ struct vxg_batch {
     const double* d_segs = nullptr;  // owned (segs) or borrowed device pointer
     DBuf segs, rec, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl, ranges;
     int64_t max_steps = 0, capacity = 0;
+    int64_t slab_lo = 0, slab_hi = -1;  // vxg_batch_set_slab: every segment may reach this slab
     // The plan's scalars (N_max, capacity) and errors are read back lazily: batch_create only
     // enqueues the plan kernel; the first call that needs them (or the emit's own readback for a
     // small list batch) resolves the plan, so a small batch costs one host round trip, not two.
@@ -624,6 +625,7 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     }
     // A thin slab (one rank's share): the passes walk only the segments that reach it.
     const bool select = b->n >= (1 << 16) && b->n < (1ll << 31) && z_hi - z_lo < V &&
+                        !(b->slab_lo <= z_lo && z_hi <= b->slab_hi) &&  // (filtered already)
                         !std::getenv("VXG_BITMAP_NO_SELECT");
     // Walk order grouped by segment length and start cell (pays off when lengths vary).
     // (not for slabs thinner than a quarter of the volume: there the sort costs more than it
@@ -1042,6 +1044,15 @@ VXG_API vxg_status vxg_batch_create(vxg_context* ctx, const vxg_segment* segs, i
         return s;
     }
     *out = b;
+    return VXG_OK;
+}
+
+VXG_API vxg_status vxg_batch_set_slab(vxg_batch* b, int64_t z_lo, int64_t z_hi) {
+    if (!b) return VXG_INVALID_ARGUMENT;
+    b->ctx->ok();
+    if (z_hi <= z_lo) return b->ctx->fail(VXG_INVALID_ARGUMENT, -1, "batch_set_slab: empty slab");
+    b->slab_lo = z_lo;
+    b->slab_hi = z_hi;
     return VXG_OK;
 }
 

@@ -66,6 +66,8 @@ __device__ __forceinline__ long long axis_cross(double s, double w, double inv_w
     gd = ceil(gd);
     gd = fmin(fmax(gd, (double)lo), (double)hi);
     long long g = (long long)gd;
+    // the guess is almost always exact: two evaluations confirm it
+    if ((g == hi || pred(g)) && (g == lo || !pred(g - 1))) return g;
     int steps = 0;
     while (g > lo && pred(g - 1) && steps < 3) {
         --g;

@@ -440,6 +440,9 @@ def test_select_slab_segments(vx, oracle):
         part = vx.Batch(None, device_ptr=local.data_ptr(), n=k)
         part.emit_bitmap_device(w_sel.data_ptr(), V, z0, z1, True)
         assert torch.equal(w_full, w_sel), (z0, z1)
+        w_sel.zero_()  # stated as filtered (vxg_batch_set_slab): the tile path's filter skipped
+        part.set_slab(z0, z1).emit_bitmap_device(w_sel.data_ptr(), V, z0, z1, True)
+        assert torch.equal(w_full, w_sel), (z0, z1)
         assert part.slab_samples(z0, z1) == full.slab_samples(z0, z1)
         part.close()
     full.close()

@@ -23,6 +23,8 @@ local = torch.empty_like(d)
 for _ in range(2):
     cnt = select_slab_segments(ctx, d.data_ptr(), n, z0, z1, local.data_ptr()) if N > 1 else n
     b = vx.Batch(None, ctx=ctx, device_ptr=(local if N > 1 else d).data_ptr(), n=cnt)
+    if N > 1:
+        b.set_slab(z0, z1)  # (as bench.py: filtered above)
     b.emit_bitmap_device(words.data_ptr(), V, z0, z1, True)
     b.close()
 torch.cuda.synchronize()

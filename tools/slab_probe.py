@@ -36,6 +36,8 @@ for r, (z0, z1) in enumerate(slabs):
             cnt = select_slab_segments(ctx, d.data_ptr(), n, z0, z1, local.data_ptr())
             src = local
         b = vx.Batch(None, ctx=ctx, device_ptr=src.data_ptr(), n=cnt)
+        if N > 1:
+            b.set_slab(z0, z1)  # (as bench.py: filtered above)
         b.emit_bitmap_device(words.data_ptr(), V, z0, z1, True)
         e1.record()
         torch.cuda.synchronize()
