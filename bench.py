@@ -175,6 +175,28 @@ class ClockSampler:
                 "samples": len(self.samples), "source": self.source}
 
 
+def time_slab_step(vx, shard, ctx, torch, d_segs, n, V, z_lo, z_hi) -> float:
+    """One rank's bitmap step on slab [z_lo, z_hi) (filter, plan, bin, fill), device ms of the
+    second of two runs -- the partition's calibration, before the timed region."""
+    local = torch.empty_like(d_segs)
+    words = torch.zeros(max(V * V * (z_hi - z_lo) // 64, 1), dtype=torch.int64, device="cuda")
+    ms = 0.0
+    for _ in range(2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        k = shard.select_slab_segments(ctx, d_segs.data_ptr(), n, z_lo, z_hi, local.data_ptr())
+        if k > 0:
+            b = vx.Batch(None, ctx=ctx, device_ptr=local.data_ptr(), n=k).set_slab(z_lo, z_hi)
+            b.emit_bitmap_device(words.data_ptr(), V, z_lo, z_hi, True)
+            b.close()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    del local, words
+    torch.cuda.empty_cache()
+    return ms
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -326,6 +348,8 @@ def main():
     ap.add_argument("--verify", action="store_true",
                     help="N > 1: compare every rank's output digest with the one-rank result")
     ap.add_argument("--segments", type=int, default=0, help="override the segment count")
+    ap.add_argument("--no-rebalance", action="store_true",
+                    help="bitmaps, N > 1: keep the sample-balanced slabs (no timed refinement)")
     ap.add_argument("--equal-slabs", action="store_true",
                     help="bitmap slabs of equal depth instead of equal sample counts")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -382,6 +406,12 @@ def main():
         if world > 1 and not args.equal_slabs:
             slabs = shard.sample_balanced_slabs(bb.slab_samples, V, world)
             part["cuts"] = "sample-balanced z-slabs (64 coarse bins)"
+            if not args.no_rebalance:  # one refinement from every rank's measured step
+                t = time_slab_step(vx, shard, ctx, torch, d_segs, n, V, *slabs[rank])
+                slabs = shard.time_balanced_slabs(bb.slab_samples, V, slabs,
+                                                  shard.gather_floats(t))
+                part["cuts"] = ("sample-balanced z-slabs (64 coarse bins), rebalanced once from "
+                                "every rank's measured step before timing")
         else:
             slabs = [shard.slab_bounds(V, world, r) for r in range(world)]
             part["cuts"] = "equal-depth z-slabs"

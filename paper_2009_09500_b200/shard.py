@@ -7,8 +7,9 @@ The path shards without a data-path collective:
   contiguous segment range; `sample_balanced_cuts` cuts the offsets scan at k * total / world so
   ranks get equal sample counts (the work), not equal segment counts;
 * bitmaps (configs 3, 5): each rank owns one z-slab -- `sample_balanced_slabs` (equal sample
-  counts; bench.py's default) or `slab_bounds(V, world, rank)` (equal depths); the device walk
-  clips every segment to its slab (vxg_bitmap.cu), slabs are disjoint, no reduction.
+  counts), refined once by `time_balanced_slabs` from every rank's measured step (bench.py's
+  default), or `slab_bounds(V, world, rank)` (equal depths); the device walk clips every segment
+  to its slab (vxg_bitmap.cu), slabs are disjoint, no reduction.
 
 The collectives here are input distribution, verification and reporting, never a reduction of
 results: `distribute_segments` gives every rank the whole batch from one host->device slice per
@@ -45,6 +46,35 @@ def sample_balanced_slabs(samples_in, V: int, world: int, bins: int = 64) -> lis
     cuts = [0]
     for r in range(1, world):
         target = total * r / world
+        b = int(np.searchsorted(cum, target, side="right")) - 1
+        b = min(max(b, 0), bins - 1)
+        frac = (target - cum[b]) / counts[b] if counts[b] > 0 else 0.0
+        z = int(round(edges[b] + frac * (edges[b + 1] - edges[b])))
+        cuts.append(min(max(z, cuts[-1] + 1), V - (world - r)))
+    cuts.append(V)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def time_balanced_slabs(samples_in, V: int, slabs, times, bins: int = 64) -> list[tuple[int, int]]:
+    """One rebalancing step of z-slabs from measured per-rank step times (decided before the
+    timed region): rank r's speed is its samples over its time, every rank is given the samples
+    it would finish in the same time at its own speed, and the cuts are placed at those sample
+    targets (interpolated in `bins` equal-depth bins, as sample_balanced_slabs). Samples alone
+    miss per-rank fixed costs -- e.g. a slab that ends in a thin partial layer of tiles, or
+    segments walked by two ranks -- that the times see."""
+    world = len(slabs)
+    if world < 2:
+        return list(slabs)
+    edges = [i * V // bins for i in range(bins + 1)]
+    counts = np.array([samples_in(edges[i], edges[i + 1]) for i in range(bins)], dtype=np.float64)
+    cum = np.concatenate([[0.0], np.cumsum(counts)])
+    total = cum[-1]
+    work = np.array([max(samples_in(a, b), 1) for a, b in slabs], dtype=np.float64)
+    speed = work / np.maximum(np.asarray(times, dtype=np.float64), 1e-9)
+    share = speed / speed.sum() * total
+    cuts = [0]
+    for r in range(1, world):
+        target = share[:r].sum()
         b = int(np.searchsorted(cum, target, side="right")) - 1
         b = min(max(b, 0), bins - 1)
         frac = (target - cum[b]) / counts[b] if counts[b] > 0 else 0.0
@@ -193,6 +223,18 @@ def max_over_ranks(value: float, group=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=_device(group))
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def gather_floats(value: float, group=None) -> list[float]:
+    """Every rank's `value`, in rank order, on every rank."""
+    import torch
+    dist = _dist()
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return [float(value)]
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_device(group))
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, t, group=group)
+    return [float(x.item()) for x in out]
 
 
 def sum_over_ranks(value: float, group=None) -> float:

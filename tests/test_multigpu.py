@@ -51,6 +51,31 @@ def test_sample_balanced_slabs():
     assert ew.max() / ew.mean() > 1.5  # what equal depths would have given
 
 
+def test_time_balanced_slabs():
+    """Rebalancing from measured times: a rank that was slow for its samples (a per-rank fixed
+    cost) gets fewer samples, the cuts stay contiguous and cover [0, V), equal speeds leave the
+    sample-balanced cuts as they were."""
+    from paper_2009_09500_b200.shard import sample_balanced_slabs, time_balanced_slabs
+    V = 4096
+    z = np.arange(V)
+    dens = np.exp(-((z - V / 2) / (V / 5)) ** 2) + 0.05
+    cum = np.concatenate([[0.0], np.cumsum(dens)])
+    samples_in = lambda a, b: cum[b] - cum[a]  # noqa: E731
+    slabs = sample_balanced_slabs(samples_in, V, 8)
+    work = np.array([samples_in(a, b) for a, b in slabs])
+    same = time_balanced_slabs(samples_in, V, slabs, work / 1e6)  # equal speeds
+    assert all(abs(a[0] - b[0]) <= 2 for a, b in zip(same, slabs))
+    times = work / 1e6
+    times[0] *= 1.05  # rank 0 is 5% slower than its samples say
+    new = time_balanced_slabs(samples_in, V, slabs, times)
+    assert new[0][0] == 0 and new[-1][1] == V
+    assert all(new[i][1] == new[i + 1][0] for i in range(7))
+    nw = np.array([samples_in(a, b) for a, b in new])
+    assert nw[0] < work[0] and nw[1:].sum() > work[1:].sum()
+    pred = nw / (work / times)  # each rank at its measured speed
+    assert pred.max() / pred.min() < 1.02
+
+
 def test_sample_balanced_cuts(oracle):
     segs = oracle.gen_batch(5000, 0, 2048, 4096, 0x5EED0004)
     steps, _, off, nmax, cap = _plan(oracle, segs)

@@ -1,8 +1,9 @@
 """Time every rank's step of config 5 on one GPU -- what bench.py --gpus N runs on rank r: filter
 the 64M broadcast segments to the rank's z-slab (sample-balanced; --equal for equal depths),
 plan them, bin and fill the slab -- device-resident, CUDA events. The max over ranks estimates
-the N-GPU step time (the slabs are independent: no collective on the data path).
-Usage: python tools/slab_probe.py N [--equal]"""
+the N-GPU step time (the slabs are independent: no collective on the data path). Then, as
+bench.py does before timing, the slabs are rebalanced once from those times and timed again.
+Usage: python tools/slab_probe.py N [--equal] [--no-rebalance]"""
 import sys
 
 import torch
@@ -10,7 +11,7 @@ import torch
 sys.path.insert(0, ".")
 import paper_2009_09500_b200 as vx  # noqa: E402
 from paper_2009_09500_b200.shard import (sample_balanced_slabs, select_slab_segments,  # noqa: E402
-                                         slab_bounds)
+                                         slab_bounds, time_balanced_slabs)
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 equal = "--equal" in sys.argv
@@ -21,13 +22,15 @@ d = torch.empty((n, 6), dtype=torch.float64, device="cuda")
 ctx.check(ctx.lib.vxg_gen_segments(ctx.h, n, None, None, 0, 2048, V, 0x5EED0105, d.data_ptr(), 1))
 bb = vx.Batch(None, ctx=ctx, device_ptr=d.data_ptr(), n=n)
 slabs = [slab_bounds(V, N, r) for r in range(N)] if equal else sample_balanced_slabs(bb.slab_samples, V, N)
-bb.close()
 local = torch.empty_like(d)
-worst = 0.0
-for r, (z0, z1) in enumerate(slabs):
+
+
+def rank_step(z0, z1, reps=3):
+    """bench.py's per-rank step on slab [z0, z1): best device ms of reps - 1 (after one warm-up)."""
     words = torch.zeros(max(V * V * (z1 - z0) // 64, 1), dtype=torch.int64, device="cuda")
     times = []
-    for _ in range(3):
+    cnt = n
+    for _ in range(reps):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -43,8 +46,23 @@ for r, (z0, z1) in enumerate(slabs):
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
         b.close()
-    t = min(times[1:])
-    worst = max(worst, t)
-    print(f"N={N} rank {r}: slab [{z0}, {z1}) {t:.2f} ms (segments {cnt})")
     del words
-print(f"N={N} {'equal' if equal else 'balanced'}: max over ranks {worst:.2f} ms")
+    return min(times[1:]), cnt
+
+
+def run(slabs, label):
+    ts = []
+    for r, (z0, z1) in enumerate(slabs):
+        t, cnt = rank_step(z0, z1)
+        ts.append(t)
+        print(f"N={N} {label} rank {r}: slab [{z0}, {z1}) {t:.2f} ms (segments {cnt})")
+    print(f"N={N} {label}: max over ranks {max(ts):.2f} ms")
+    return ts
+
+
+ts = run(slabs, "equal" if equal else "balanced")
+if N > 1 and not equal and "--no-rebalance" not in sys.argv:
+    # bench.py's partition: the sample-balanced slabs refined once from the ranks' measured steps
+    slabs2 = time_balanced_slabs(bb.slab_samples, V, slabs, ts)
+    run(slabs2, "rebalanced")
+bb.close()
