@@ -262,12 +262,13 @@ __device__ __forceinline__ long long walk_pieces(const SegRec& r, long long N, c
     return inside;
 }
 
-// Bins are (tile, length class): a tile's pieces are stored grouped by length (classes of 8
+// Bins are (tile, length class): a tile's pieces are stored grouped by length (classes of 4
 // samples), so the fill's warp steps, which run as long as their longest piece, get pieces of
 // nearly equal length. A tile's bins are consecutive: its pieces are still one CSR range.
-// (cfg5: 8-sample classes fill in 77.3 ms against 79.5 with 16-sample ones, for 1.7 ms more
-// binning.)
-constexpr int kLenShift = 3;                   // class width 2^kLenShift samples
+// (Round 1, exact fill: 8-sample classes 77.3 ms against 79.5 with 16-sample ones, for 1.7 ms
+// more binning; round 2, fixed-point fill with one lane per piece: 4-sample classes 57.4 ms
+// against 58.4 with 8, for 0.5 ms more binning.)
+constexpr int kLenShift = 2;                   // class width 2^kLenShift samples
 constexpr int kLenClasses = 256 >> kLenShift;  // (longer pieces share the last class)
 __device__ __forceinline__ long long bin_of(long long tile, long long len) {
     return tile * kLenClasses + min((len - 1) >> kLenShift, (long long)(kLenClasses - 1));

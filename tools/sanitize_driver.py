@@ -1,7 +1,9 @@
 """Mid-size run of the look-back / shared-memory kernels for compute-sanitizer (tools/
 gpu_sanitize.sh): plan_kernel (look-back offset scan), list_fused_kernel (count/emit task queues +
 look-back), list_small_kernel (per-warp tiles + look-back), tiles_scan_lb_kernel, tiles_fill_kernel
-(shared-memory tile, streamed readback), each output checked against the oracle."""
+(shared-memory tile, fixed-point samples with the FP64 redo of near-boundary lanes, streamed
+readback), tiles_count / tiles_scatter (shared-memory walk state), each output checked against
+the oracle."""
 import os
 import sys
 
@@ -19,7 +21,11 @@ vox, off, total = vx.run_batch_flat(segs)                      # plan_kernel + l
 ovox, ooff, ototal = orc.run_batch(segs)
 assert total == ototal and np.array_equal(off, ooff) and np.array_equal(vox, ovox), "list"
 
-bsegs = vx.gen_segments(70000, 0, 300, 512, 0x5A12)
+rng = np.random.default_rng(0x5A15)  # tie lines: samples on half-integers (the fills' FP64 redo)
+base = rng.integers(2, 200, size=(3000, 3)).astype(np.float64) + 0.5
+ties = np.concatenate([base, base + rng.integers(1, 250, size=(3000, 1)) * np.array([1.0, 0.5, 0.25])],
+                      axis=1)
+bsegs = np.concatenate([vx.gen_segments(70000, 0, 300, 512, 0x5A12), ties])
 b = vx.Batch(bsegs)
 w, out = b.emit_bitmap(512, 0, 512)                             # count/scan_lb/scatter/fill
 ow, oo = orc.bitmap(bsegs, 512)
