@@ -750,7 +750,7 @@ __device__ __forceinline__ bool fx_loop_int(const TileArgs& g, const Piece& pc, 
     const unsigned long long ax = ((unsigned long long)pc.w[0] << 9) + (unsigned long long)((long long)gl * wx * 4),
                              ay = ((unsigned long long)pc.w[1] << 9) + (unsigned long long)((long long)gl * wy * 4),
                              az = ((unsigned long long)pc.w[2] << 9) + (unsigned long long)((long long)gl * wz * 4);
-    const uint32_t zero = (uint32_t)g.pf >> 24;  // 0, opaque to ptxas
+    const uint32_t zero = (uint32_t)g.zero;  // 0, opaque to ptxas
     const uint32_t dxl = (uint32_t)wx << kSh, dxh = (uint32_t)(wx >> (32 - kSh)) + zero,
                    dyl = (uint32_t)wy << kSh, dyh = (uint32_t)(wy >> (32 - kSh)) + zero,
                    dzl = (uint32_t)wz << kSh, dzh = (uint32_t)(wz >> (32 - kSh)) + zero;
