@@ -101,6 +101,18 @@ __device__ __forceinline__ void small_emit(const SegRec& R, int N, int32_t* __re
         }
     }
     if (FAST) {  // the row holding k = N: samples below it as above, then E itself
+        if (r0 == N && N > 0) {  // (N a multiple of 32: the row holds E alone -- lane 0 does it)
+            if (lane == 0) {
+                const int32_t key = voxel_key(R.ex, R.ey, R.ez);
+                if (key != carry) {
+                    int32_t* d = out + 3 * (pos + running);
+                    d[0] = R.ex;
+                    d[1] = R.ey;
+                    d[2] = R.ez;
+                }
+            }
+            return;
+        }
         if (r0 <= N) {
             const int k = r0 + lane;
             int32_t x, y, z;
