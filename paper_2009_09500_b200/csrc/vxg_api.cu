@@ -177,6 +177,7 @@ struct vxg_batch {
     int64_t n = 0;
     const double* d_segs = nullptr;  // owned (segs) or borrowed device pointer
     DBuf segs, rec, off, status, status2, tile_seg, out, chain, entries, ent_off, ctl, ranges;
+    DBuf prec;  // bitmap tile path: the records in walk order (+ their N)
     int64_t max_steps = 0, capacity = 0;
     int64_t slab_lo = 0, slab_hi = -1;  // vxg_batch_set_slab: every segment may reach this slab
     // The plan's scalars (N_max, capacity) and errors are read back lazily: batch_create only
@@ -659,9 +660,24 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
         if (perm && g.n > 0) {
             g.perm_cur = perm_cur;
             g.perm = order;
+            // Copy the records into walk order when the memory is there: the count and scatter
+            // passes then read them sequentially instead of gathering 64 B per segment (whole
+            // 128-B lines come from DRAM for each gather).
+            // (N rides in the copy's flag word: N < 2^28)
+            const bool copy = !std::getenv("VXG_BITMAP_PERM_INDEX") &&
+                              b->max_steps < (1ll << (32 - vxg::kRecNShift)) &&
+                              b->prec.ensure(ctx, sizeof(SegRec) * (size_t)g.n);
+            if (copy) g.prec = b->prec.as<SegRec>();
             cudaMemsetAsync(perm_cur, 0, keys * sizeof(long long), ctx->stream);
             vxg::launch_tiles_perm(g, ctx->stream);
             ctx->launches += 3;
+            if (copy) {  // from here on segment ids are positions in the copy
+                g.rec = g.prec;
+                g.rec_n = 1;
+                g.perm = nullptr;
+                g.sel = nullptr;
+                g.prec = nullptr;
+            }
         }
     }
     vxg::launch_tiles_count(g, ctx->stream);

@@ -277,6 +277,10 @@ __device__ __forceinline__ long long bin_of(long long tile, long long len) {
 __device__ __forceinline__ long long seg_steps(const TileArgs& g, long long i) {
     return __ldg(g.off + i + 1) - __ldg(g.off + i) - 1;
 }
+// N of a loaded record: records copied into walk order carry it above their flag bits.
+__device__ __forceinline__ long long rec_steps(const TileArgs& g, const SegRec& r, long long i) {
+    return g.rec_n ? (long long)(r.flags >> kRecNShift) : seg_steps(g, i);
+}
 
 // Walk order: segments grouped by length (8 buckets of N / 256), so the 32 segments a warp walks
 // in lock step have similar piece counts (the warp runs as long as its longest walk), and by
@@ -335,7 +339,22 @@ __global__ void __launch_bounds__(256) perm_scatter_kernel(TileArgs g) {
                          (unsigned long long)__popc(peers));
     base = __shfl_sync(peers, base, leader);
     const unsigned below = peers & ((1u << (threadIdx.x & 31)) - 1u);
-    g.perm[base + __popc(below)] = (int)i;
+    const unsigned long long pos = base + __popc(below);
+    if (g.prec) {  // the record itself moves: the passes after read it sequentially
+        const uint4* q = reinterpret_cast<const uint4*>(g.rec + i);
+        uint4* d = reinterpret_cast<uint4*>(g.prec + pos);
+        const uint4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+        uint4 e = __ldg(q + 3);
+        e.w = (e.w & ((1u << kRecNShift) - 1u)) | ((uint32_t)seg_steps(g, i) << kRecNShift);
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(d),
+                     "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                     : "memory");
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(d + 2),
+                     "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w), "r"(e.x), "r"(e.y), "r"(e.z), "r"(e.w)
+                     : "memory");
+    } else {
+        g.perm[pos] = (int)i;
+    }
 }
 
 // Exclusive prefix of the kPermKeys bucket counts, in place (one CTA).
@@ -478,7 +497,7 @@ __global__ void __launch_bounds__(256, 3) tiles_count_kernel(TileArgs g) {
     if (tix < g.n) {
         const long long i = walk_segment(g, tix);
         const SegRec r = load_rec(g.rec + i);
-        inside = walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long, long long len, bool) {
+        inside = walk_pieces(r, rec_steps(g, r, i), g, [&](long long t, long long, long long len, bool) {
             atomicAdd(reinterpret_cast<unsigned long long*>(g.tile_cnt) + bin_of(t, len), 1ull);
             inbox += len;
         });
@@ -850,7 +869,7 @@ __global__ void __launch_bounds__(256, 4) tiles_scatter_kernel(TileArgs g) {
         st_piece(g.pieces + 2 * (size_t)pslot,
                  make_piece(r, D, fx, g.z_lo, i, pka, plen & 0x7fffffffu, (plen >> 31) != 0u));
     };
-    walk_pieces(r, seg_steps(g, i), g, [&](long long t, long long ka, long long len, bool hasE) {
+    walk_pieces(r, rec_steps(g, r, i), g, [&](long long t, long long ka, long long len, bool hasE) {
         // store the previous piece first: its slot arrived while this piece was being walked;
         // the new atomic's result lands directly in pslot and is not read until the next piece
         if (pending) store();

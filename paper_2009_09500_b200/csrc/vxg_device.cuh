@@ -28,6 +28,8 @@ enum : uint32_t {
     REC_FX = 8u,     // plan-kernel W and every |coordinate| of S and E < 2^24: the bitmap fill may
                      // step samples in 32.32 fixed point (vxg_bitmap.cu, fill_piece)
 };
+// The bitmap passes' walk-order copy of the records keeps N in the flag word's upper bits.
+constexpr int kRecNShift = 4;
 
 // Voxel key for consecutive-duplicate tests: x + 8y + 64z (mod 2^32). Consecutive samples of one
 // segment differ by |W| <= 1 per axis plus a few ulp, so their voxels differ by at most 2 per

@@ -89,6 +89,8 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     unsigned long long* words;        // the slab's bitmap (OR-ed into)
     Control* ctl;                     // total: in-volume samples, n_entries: pieces
     int* perm;                        // walk order (segments grouped by length) or null
+    SegRec* prec;                     // perm pass: records copied in walk order, or null
+    int rec_n;                        // rec holds such copies: N = flags >> kRecNShift
     const int* sel;                   // thin slab: the segments reaching it (g.n of them) or null
     long long* perm_cur;              // tile_perm_keys(): bucket counts, then cursors (zeroed)
     unsigned long long* scan_status;  // bin scan: look-back words, one per 4096 bins (zeroed)

@@ -325,6 +325,26 @@ def test_bitmap_tiles_adversarial(vx, oracle):
             assert np.array_equal(words, ow), (V, z0, z1)
 
 
+@pytest.mark.parametrize("order", ["copy", "index", "none"])
+def test_bitmap_walk_orders(vx, oracle, monkeypatch, order):
+    """The count/scatter walk orders of large batches with long segments (n >= 2^16, N >= 256):
+    records copied into walk order (N carried in the copy's flag word), the index permutation,
+    and no sort; on the whole volume, a thin selected slab (sorted on request) and a slab cut
+    mid-tile -- bit-exact against the oracle every time."""
+    if order == "index":
+        monkeypatch.setenv("VXG_BITMAP_PERM_INDEX", "1")
+    elif order == "none":
+        monkeypatch.setenv("VXG_BITMAP_NO_PERM", "1")
+    monkeypatch.setenv("VXG_BITMAP_PERM", "1")  # (thin slabs sorted too)
+    segs = vx.gen_segments(70000, 0, 600, 1024, 23)
+    for z0, z1 in [(0, 1024), (400, 460), (7, 131)]:
+        words, outside = vx.voxelize_bitmap(segs, 1024, z0, z1, clip=True)
+        ow, oo = oracle.bitmap(segs, 1024, z0, z1)
+        assert np.array_equal(words, ow), (order, z0, z1)
+        if (z0, z1) == (0, 1024):
+            assert outside == oo, order
+
+
 def test_bitmap_tiles_accumulate_and_match_atomic_path(vx, oracle, monkeypatch):
     """Words are OR-ed into (the caller's bits survive), and the tile path equals the generic
     global-atomic path on the same batch."""
