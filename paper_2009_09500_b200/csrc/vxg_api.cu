@@ -1359,12 +1359,17 @@ namespace {
 
 // The multi-pass path for a batch the one-launch kernel handed back (a segment with N > 2^14).
 vxg_status small_reroute(vxg_context* ctx, const vxg_segment* segs, int64_t n, vxg_voxel* out,
-                         int64_t out_cap, int64_t* chain, int64_t* total) {
+                         int64_t out_cap, int64_t* chain, int64_t* total, int64_t* max_steps,
+                         int64_t* capacity) {
     vxg_batch* b = nullptr;
     vxg_status s = vxg_batch_create(ctx, segs, n, VXG_MEM_DEVICE, &b);
     if (s) return s;
     s = emit_list_device(b, reinterpret_cast<int32_t*>(out), out_cap,
                          reinterpret_cast<long long*>(chain), total);
+    if (!s) {  // (the one-launch kernel's partials clamp N at 2^14 + 1: the plan's own values)
+        if (max_steps) *max_steps = b->max_steps;
+        if (capacity) *capacity = b->capacity;
+    }
     vxg_batch_destroy(b);
     return s;
 }
@@ -1385,11 +1390,10 @@ vxg_status small_result(vxg_context* ctx, int64_t* total, int64_t* max_steps, in
                          "than 2^14 steps (only the synchronous form re-routes it)");
     if (c.n_entries) {  // long segment: the multi-pass path
         int64_t t = 0;
-        vxg_status s = small_reroute(ctx, st->segs, st->n, st->out, st->out_cap, st->chain, &t);
+        vxg_status s = small_reroute(ctx, st->segs, st->n, st->out, st->out_cap, st->chain, &t,
+                                     max_steps, capacity);
         if (s) return s;
         if (total) *total = t;
-        if (max_steps) *max_steps = (int64_t)c.max_steps;
-        if (capacity) *capacity = (int64_t)c.pad0;
         return VXG_OK;
     }
     // (plan errors first: they are batch_preprocess's; ctl_status reports the lowest segment)

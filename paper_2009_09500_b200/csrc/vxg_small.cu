@@ -22,7 +22,10 @@
 // N = 128): 0.078 ms per call (round 1); round 2: records copied from shared memory into
 // registers (the count loop re-read them per sample) 0.076 -> 0.074 ms, tiles sized so every
 // resident warp takes one pair (small_spw: 10 segments for cfg1) 0.078 -> 0.076, 32.32 fixed-point
-// count pieces (vxg_device.cuh) 0.074 -> 0.0696 ms. Variants that did not pay: one tile in flight
+// count pieces (vxg_device.cuh) 0.074 -> 0.0696 ms, the E-only last row by lane 0 -> 0.0675,
+// N_max / capacity pooled per warp in shared slots instead of 64-bit shared atomics (CAS loops)
+// per segment, one rotate shuffle per emit row and 32-bit store indices -> 0.0633 ms. Variants
+// that did not pay: one tile in flight
 // per warp (a third of the instructions were look-back spins: 0.084 ms), a cooperative kernel
 // with two grid barriers around a one-CTA scan (0.131 ms), emit rows over the tile's flat sample
 // space (0.081 ms), 64 registers for 4 CTAs per SM (spills: 0.080 ms).
@@ -76,6 +79,7 @@ __device__ __forceinline__ void small_emit(const SegRec& R, int N, int32_t* __re
                                            long long pos, bool& bad) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
+    int32_t* const ob = out + 3 * pos;  // (this chain's output: 32-bit indices below)
     int running = 0;
     int32_t carry = 0;
     double t = __int2double_rn(lane);
@@ -83,7 +87,7 @@ __device__ __forceinline__ void small_emit(const SegRec& R, int N, int32_t* __re
     auto commit = [&](bool keep, int32_t key, int32_t x, int32_t y, int32_t z) {
         const unsigned m = __ballot_sync(0xffffffffu, keep);
         if (keep) {
-            int32_t* d = out + 3 * (pos + running + __popc(m & lt));
+            int32_t* d = ob + 3 * (running + __popc(m & lt));
             d[0] = x;
             d[1] = y;
             d[2] = z;
@@ -92,20 +96,32 @@ __device__ __forceinline__ void small_emit(const SegRec& R, int N, int32_t* __re
         carry = __shfl_sync(0xffffffffu, key, 31);
     };
     if (FAST) {
+        // One rotate per row: lane l gets lane l-1's key, lane 0 this row's lane-31 key -- the
+        // previous row's (the carry lane 0 compares with) is what lane 0 got one row earlier.
         for (; r0 + 32 <= N; r0 += 32) {  // every sample of the row has k < N
             int32_t x, y, z;
             const int32_t key = fast_key<POS>(R, t, x, y, z);
             t = __dadd_rn(t, 32.0);
-            const int32_t up = __shfl_up_sync(0xffffffffu, key, 1);
-            commit((r0 | lane) == 0 || key != (lane == 0 ? carry : up), key, x, y, z);
+            const int32_t rot = __shfl_sync(0xffffffffu, key, (lane + 31) & 31);
+            const bool keep = (r0 | lane) == 0 || key != (lane == 0 ? carry : rot);
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                int32_t* d = ob + 3 * (running + __popc(m & lt));
+                d[0] = x;
+                d[1] = y;
+                d[2] = z;
+            }
+            running += __popc(m);
+            carry = rot;  // (lane 0: this row's last key)
         }
+        carry = __shfl_sync(0xffffffffu, carry, 0);
     }
     if (FAST) {  // the row holding k = N: samples below it as above, then E itself
         if (r0 == N && N > 0) {  // (N a multiple of 32: the row holds E alone -- lane 0 does it)
             if (lane == 0) {
                 const int32_t key = voxel_key(R.ex, R.ey, R.ez);
                 if (key != carry) {
-                    int32_t* d = out + 3 * (pos + running);
+                    int32_t* d = ob + 3 * running;
                     d[0] = R.ex;
                     d[1] = R.ey;
                     d[2] = R.ez;
@@ -287,14 +303,15 @@ __device__ __forceinline__ void small_emit_seg(const SegRec& Rs, int N, int32_t*
 }
 
 // Plan one tile of segments (lane j < kSmallSPW: segment seg0 + j) into `rec` (shared memory).
-// Returns the lane's N (-1: no segment); pools N_max / capacity into the CTA's counters.
+// Returns the lane's N (-1: no segment); pools N_max / capacity into the lane's partials.
 template <int kSmallSPW>
 __device__ __forceinline__ int small_plan_tile(const SmallArgs& a, long long seg0, SegRec* rec,
-                                               unsigned long long* s_max,
-                                               unsigned long long* s_cap, bool& is_long) {
+                                               unsigned& w_max, unsigned long long& w_cap,
+                                               bool& is_long) {
     const int lane = threadIdx.x & 31;
     int myN = -1;
     is_long = false;
+    unsigned n32 = 0, c32 = 0;
     if (lane < kSmallSPW) {
         const long long i = seg0 + lane;
         if (i < a.n) {
@@ -315,11 +332,20 @@ __device__ __forceinline__ int small_plan_tile(const SmallArgs& a, long long seg
             r.ez = pl.ez;
             r.flags = rec_flags(sx, sy, sz, ex, ey, ez);
             rec[lane] = r;
-            atomicMax(s_max, (unsigned long long)pl.n);
-            atomicAdd(s_cap, (unsigned long long)(pl.n + 1));
+            // (32-bit partials: a batch holding N > 2^14 is redone by the multi-pass path,
+            // which reports its own N_max and capacity)
+            n32 = (unsigned)min(pl.n, (long long)kSmallMaxSteps + 1);
+            c32 = n32 + 1u;
             is_long = pl.n > kSmallMaxSteps;
             myN = is_long ? 0 : (int)pl.n;
         }
+    }
+    // the warp's partials (a shared slot per warp: no atomics, nothing held in registers)
+    n32 = __reduce_max_sync(0xffffffffu, n32);
+    c32 = __reduce_add_sync(0xffffffffu, c32);
+    if (lane == 0) {
+        w_max = max(w_max, n32);
+        w_cap += c32;
     }
     return myN;
 }
@@ -334,8 +360,8 @@ struct SmallTile {
 // Claim the next tile, plan it into `rec`, count it and publish its total (look-back flag A).
 template <int kSmallSPW>
 __device__ __forceinline__ SmallTile small_count_tile(const SmallArgs& a, SegRec* rec, int* cnt,
-                                                      unsigned long long* s_max,
-                                                      unsigned long long* s_cap, int* s_long,
+                                                      unsigned& w_max,
+                                                      unsigned long long& w_cap, int* s_long,
                                                       bool& bad, long long& bad_seg) {
     const int lane = threadIdx.x & 31;
     SmallTile T;
@@ -348,7 +374,7 @@ __device__ __forceinline__ SmallTile small_count_tile(const SmallArgs& a, SegRec
     if (T.tile >= a.ntiles) return T;
     const long long seg0 = T.tile * kSmallSPW;
     bool il;
-    T.myN = small_plan_tile<kSmallSPW>(a, seg0, rec, s_max, s_cap, il);
+    T.myN = small_plan_tile<kSmallSPW>(a, seg0, rec, w_max, w_cap, il);
     T.is_long = __any_sync(0xffffffffu, il);
     if (T.is_long && lane == 0) *s_long = 1;
     __syncwarp();
@@ -423,11 +449,18 @@ __global__ void __launch_bounds__(kSmallNW * 32) list_small_kernel(SmallArgs a) 
     __syncthreads();
     bool bad = false;
     long long bad_seg = 0;
+    __shared__ unsigned s_wmax[kSmallNW];
+    __shared__ unsigned long long s_wcap[kSmallNW];
+    if ((tid & 31) == 0) {
+        s_wmax[warp] = 0;
+        s_wcap[warp] = 0;
+    }
+    __syncwarp();
     for (;;) {
-        const SmallTile A = small_count_tile<kSmallSPW>(a, s_rec[warp][0], s_cnt[warp], &s_max, &s_cap,
+        const SmallTile A = small_count_tile<kSmallSPW>(a, s_rec[warp][0], s_cnt[warp], s_wmax[warp], s_wcap[warp],
                                              &s_long, bad, bad_seg);
         if (A.tile >= a.ntiles) break;
-        const SmallTile B = small_count_tile<kSmallSPW>(a, s_rec[warp][1], s_cnt[warp], &s_max, &s_cap,
+        const SmallTile B = small_count_tile<kSmallSPW>(a, s_rec[warp][1], s_cnt[warp], s_wmax[warp], s_wcap[warp],
                                              &s_long, bad, bad_seg);
         small_emit_tile<kSmallSPW>(a, A, s_rec[warp][0]);
         if (B.tile >= a.ntiles) break;
@@ -435,6 +468,10 @@ __global__ void __launch_bounds__(kSmallNW * 32) list_small_kernel(SmallArgs a) 
         __syncwarp();
     }
     if (bad) record_error(a.ctl, bad_seg, 2);
+    if ((tid & 31) == 0) {
+        if (s_wmax[warp]) atomicMax(&s_max, (unsigned long long)s_wmax[warp]);
+        if (s_wcap[warp]) atomicAdd(&s_cap, s_wcap[warp]);
+    }
     __syncthreads();
     if (tid == 0) {
         if (s_max) atomicMax(&a.ctl->max_steps, s_max);

@@ -710,7 +710,9 @@ def test_run_batch_device_one_launch(vx, oracle, case):
     out.zero_()
     if case == "long":  # asynchronous: one call is re-routed by its result, a chain is refused
         vx.run_batch_device(d.data_ptr(), n, out.data_ptr(), cap, chain.data_ptr(), sync=False)
-        assert vx.run_batch_device_result()[0] == ototal
+        t, mx, capa = vx.run_batch_device_result()
+        o = oracle.batch_preprocess(segs)  # (N_max and capacity of the re-routed plan)
+        assert t == ototal and capa == o["capacity"] and mx == o["max_steps"]
         assert np.array_equal(out.cpu().numpy()[:total], ovox)
         for _ in range(2):
             vx.run_batch_device(d.data_ptr(), n, out.data_ptr(), cap, chain.data_ptr(), sync=False)
