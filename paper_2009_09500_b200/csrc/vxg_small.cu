@@ -9,8 +9,8 @@
 //   1. plan   : lane j runs make_plan (src/parametric.cpp:8-26) for segment j into shared memory;
 //               N_max and the capacity are pooled per CTA and added to the control block once;
 //   2. count  : the warp evaluates the tile's samples k = 0..N of every segment (sample k < N is
-//               S + W*k, k = N is E; include/voxline/parametric.hpp:41-48), each lane an equal
-//               contiguous range of the tile, and counts the kept voxels per segment (consecutive
+//               S + W*k, k = N is E; include/voxline/parametric.hpp:41-48), each lane a contiguous
+//               share of one segment, and counts the kept voxels per segment (consecutive
 //               duplicates dropped, src/batch.cpp:139-142); the tile's total is published
 //               (decoupled look-back, flag A);
 //   3. prefix : after counting its NEXT tile too, the warp finds this tile's output position by
@@ -24,8 +24,9 @@
 // resident warp takes one pair (small_spw: 10 segments for cfg1) 0.078 -> 0.076, 32.32 fixed-point
 // count pieces (vxg_device.cuh) 0.074 -> 0.0696 ms, the E-only last row by lane 0 -> 0.0675,
 // N_max / capacity pooled per warp in shared slots instead of 64-bit shared atomics (CAS loops)
-// per segment, one rotate shuffle per emit row and 32-bit store indices -> 0.0633 ms. Variants
-// that did not pay: one tile in flight
+// per segment, one rotate shuffle per emit row and 32-bit store indices -> 0.0633 ms, count
+// lanes apportioned to segments (one piece per lane instead of two divergent ones) -> 0.0581 ms.
+// Variants that did not pay: one tile in flight
 // per warp (a third of the instructions were look-back spins: 0.084 ms), a cooperative kernel
 // with two grid barriers around a one-CTA scan (0.131 ms), emit rows over the tile's flat sample
 // space (0.081 ms), 64 registers for 4 CTAs per SM (spills: 0.080 ms).
@@ -224,73 +225,61 @@ __device__ __forceinline__ int lane_piece(const SegRec& R, int N, int k0, int k1
     return cnt;
 }
 
-// Count pass of a whole tile, one warp: the tile's samples (segment j's N_j + 1 samples after
-// segment j - 1's) split into 32 equal contiguous lane ranges, so lanes stay busy across segment
-// boundaries; a lane walks the pieces of the (one or two) segments its range touches and adds
-// each piece's kept voxels to the segment's counter in shared memory. A segment's first sample is
-// always kept; any other first sample of a lane is compared with the last one of the lane before.
-// myN: lane j < kSmallSPW holds segment j's N (-1: none); cnt[j] must be zero on entry.
+// Count pass of a whole tile, one warp: every non-empty segment j gets L_j = 1 +
+// floor((32 - segments) * (N_j + 1) / T) consecutive lanes (T: the tile's samples), and each of
+// them an equal contiguous share of the segment's samples -- one piece per lane, so the warp's
+// fixed-point loop runs as long as the longest share (lanes split across two segments ran two
+// divergent loops: twice the iterations on config 1). A lane's first sample is kept when it is
+// the segment's k = 0, else compared with the last sample of the lane before (the same segment's
+// previous share). myN: lane j < kSmallSPW holds segment j's N (-1: none); cnt[j] must be zero on
+// entry.
 template <int kSmallSPW>
 __device__ __forceinline__ void small_count_flat(const SegRec* rec, int myN, int* cnt, bool& bad,
                                                  int& bad_j) {
     const int lane = threadIdx.x & 31;
     const int M = myN >= 0 ? myN + 1 : 0;
-    int P = M;  // inclusive prefix of the segments' sample counts
+    const int T = (int)__reduce_add_sync(0xffffffffu, (unsigned)M);
+    const int nseg = __popc(__ballot_sync(0xffffffffu, M > 0));
+    const int L = M > 0 ? 1 + (int)((long long)(32 - nseg) * M / max(T, 1)) : 0;
+    int Lx = L;  // inclusive prefix of the lane counts, then exclusive
 #pragma unroll
     for (int o = 1; o < kSmallSPW; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, P, o);
-        if (lane >= o) P += u;
+        const int u = __shfl_up_sync(0xffffffffu, Lx, o);
+        if (lane >= o) Lx += u;
     }
-    const int T = __shfl_sync(0xffffffffu, P, kSmallSPW - 1);
-    P -= M;  // exclusive: segment j's first sample in the tile
-    const int q = (T + 31) >> 5;
-    const int f0 = min(lane * q, T), f1 = min(f0 + q, T);
-    // the segment holding f0: the last j with P_j <= f0 (and a non-empty segment)
-    int j = 0;
+    Lx -= L;
+    int j = 0;  // this lane's segment: the last non-empty one whose lanes start at or below it
 #pragma unroll
     for (int i = 1; i < kSmallSPW; ++i) {
-        const int Pi = __shfl_sync(0xffffffffu, P, i);
-        const int Mi = __shfl_sync(0xffffffffu, M, i);
-        if (Mi > 0 && Pi <= f0) j = i;
+        const int Li = __shfl_sync(0xffffffffu, L, i);
+        const int Lxi = __shfl_sync(0xffffffffu, Lx, i);
+        if (Li > 0 && Lxi <= lane) j = i;
     }
+    const int Lj = __shfl_sync(0xffffffffu, L, j), Lxj = __shfl_sync(0xffffffffu, Lx, j);
+    const int Mj = __shfl_sync(0xffffffffu, M, j);
+    const int r = lane - Lxj;
+    const int q = Lj > 0 ? (Mj + Lj - 1) / Lj : 0;
+    const int k0 = r * q, k1 = min(k0 + q, Mj);
+    const bool active = r < Lj && k0 < k1;
     int32_t first = 0, last = 0;
-    const int first_j = j;
-    int first_k = -1;
-    // (the lanes' walks diverge: segment offsets from shared memory, not shuffles)
-    __shared__ int s_off[kSmallNW][kSmallSPW + 1];
-    const int warp = threadIdx.x >> 5;
-    if (lane < kSmallSPW) s_off[warp][lane] = P;
-    if (lane == kSmallSPW - 1) s_off[warp][kSmallSPW] = P + M;
-    __syncwarp();
-    const int* off = s_off[warp];
-    for (int f = f0; f < f1;) {
-        const int Pj = off[j], Nj = off[j + 1] - Pj - 1;
-        const int k0 = f - Pj, k1 = min(f1 - Pj, Nj + 1);
+    int c = 0;
+    if (active) {
         const SegRec R = rec[j];  // (into registers: a shared-memory reference is re-read per sample)
-        int32_t pf, pl;
+        const int Nj = Mj - 1;
         bool b = false;
-        int c;
-        if (R.flags & REC_CHECK) c = lane_piece<false, false>(R, Nj, k0, k1, pf, pl, b);
-        else if (R.flags & REC_POS) c = lane_piece<true, true>(R, Nj, k0, k1, pf, pl, b);
-        else c = lane_piece<true, false>(R, Nj, k0, k1, pf, pl, b);
+        if (R.flags & REC_CHECK) c = lane_piece<false, false>(R, Nj, k0, k1, first, last, b);
+        else if (R.flags & REC_POS) c = lane_piece<true, true>(R, Nj, k0, k1, first, last, b);
+        else c = lane_piece<true, false>(R, Nj, k0, k1, first, last, b);
         if (b) {
             bad = true;
             bad_j = j;
         }
-        if (f == f0) {
-            first = pf;
-            first_k = k0;
-        } else {
-            ++c;  // a later piece starts its segment: k = 0 is kept
-        }
-        last = pl;
-        if (c) atomicAdd(&cnt[j], c);
-        f = Pj + k1;
-        ++j;
-        while (j < kSmallSPW && off[j + 1] == off[j]) ++j;  // (skip empty slots)
     }
     const int32_t up = __shfl_up_sync(0xffffffffu, last, 1);
-    if (f0 < f1 && (first_k == 0 || first != up)) atomicAdd(&cnt[first_j], 1);
+    if (active) {
+        c += (k0 == 0 || first != up) ? 1 : 0;
+        atomicAdd(&cnt[j], c);
+    }
 }
 
 // Dispatch on the record's rounding class (warp-uniform).
