@@ -461,9 +461,14 @@ def main():
         small_ev.append((e0, e1))
         return None, 0, 0, 0
 
+    seg_host = d_segs[s0].cpu().numpy() if kind == "single" else None  # (48 B: the input)
+
     def step():
         if small:
             return step_small()
+        if kind == "single":  # voxelize_parametric: one launch + one readback of the count
+            u = vx.voxelize_parametric_device(seg_host, out.data_ptr(), capacity, ctx=ctx)
+            return u, 0, 0, 0  # (its kernel time is read once, after the timed loop)
         src, cnt = my_ptr, my_n
         if slab_segs is not None:
             cnt = shard.select_slab_segments(ctx, d_segs.data_ptr(), n, z_lo, z_hi,
@@ -514,6 +519,8 @@ def main():
         assert vx.run_batch_device_result(ctx)[0] == units
         emit_ms = [a.elapsed_time(b) for a, b in small_ev]
         plan_ms = aux_ms = [0.0]
+    if kind == "single":  # the last call's long_chain_kernel (CUDA events inside the library)
+        emit_ms = [vx.voxelize_parametric_kernel_ns(ctx) / 1e6]
     ms = barrier_max(local_ms, world) / args.steps
     if kind == "slab":
         total_units = float(batch_voxels)
@@ -528,9 +535,11 @@ def main():
     emit_avg = statistics.mean(emit_ms) if emit_ms else 0.0
     traffic, traffic_src = load_traffic(args.workload)
     if kind in ("list", "single"):
-        alg_bytes = 12 * units + 8 * (my_n + 1) + 48 * my_n
+        alg_bytes = 12 * units + (8 * (my_n + 1) + 48 * my_n if kind == "list" else 0)
         achieved = alg_bytes / (emit_avg / 1e3) / 1e9
-        dominant = ("list_small_kernel (plan + count + prefix + emit in one launch)" if small
+        dominant = ("long_chain_kernel (plan + samples + dedup + look-back + emit in one launch)"
+                    if kind == "single"
+                    else "list_small_kernel (plan + count + prefix + emit in one launch)" if small
                     else "list_fused_kernel (count + emit tasks overlapped)"
                     if capacity >= 43_000_000 else "list_emit_kernel")
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -643,6 +652,8 @@ def run_e2e(vx, shard, ctx, torch, d_segs, cfg, kind, n, s0, s1, units, capacity
         out_h = vx.pinned_empty((max(units, 1), 3), np.int32)
         chain_h = vx.pinned_empty((my_n + 1,), np.int64)
         h2d = 48 * my_n
+        if kind == "single":
+            need = 12 * units
     else:
         nwords = (V * V * (z_hi - z_lo) + 63) // 64
         words_h = vx.pinned_empty((nwords,), np.uint64)
@@ -655,7 +666,9 @@ def run_e2e(vx, shard, ctx, torch, d_segs, cfg, kind, n, s0, s1, units, capacity
     for it in range(steps + 1):
         barrier(world)
         t0 = time.perf_counter()
-        if kind in ("list", "single"):
+        if kind == "single":  # voxelize_parametric into a pinned host buffer
+            assert vx.voxelize_parametric_host(segs_h[s0], out_h, ctx=ctx) == units
+        elif kind == "list":
             b = vx.Batch(segs_h[s0:s1], ctx=ctx)
             _, _, total = b.emit_list(out=out_h, chain_off=chain_h)
             assert total == units
@@ -673,7 +686,8 @@ def run_e2e(vx, shard, ctx, torch, d_segs, cfg, kind, n, s0, s1, units, capacity
             if sel is not None:
                 b.set_slab(z_lo, z_hi)
             b.emit_bitmap(V, z_lo, z_hi, clip=True, words=words_h, overwrite=True)
-        b.close()
+        if kind != "single":
+            b.close()
         dt = time.perf_counter() - t0
         if it > 0:
             times.append(dt)
@@ -682,7 +696,9 @@ def run_e2e(vx, shard, ctx, torch, d_segs, cfg, kind, n, s0, s1, units, capacity
     return {"value": total_units / sec / 1e9, "unit": "Gvoxels/s",
             "h2d_bytes_per_step": int(barrier_sum(float(h2d), world)),
             "d2h_bytes_per_step": int(barrier_sum(float(need), world)), "ms_per_step": sec * 1e3,
-            "api": "paper_2009_09500_b200.Batch(host) + Batch.emit_list/emit_bitmap(host)"
+            "api": ("paper_2009_09500_b200.voxelize_parametric_host (pinned output)"
+                    if kind == "single" else
+                    "paper_2009_09500_b200.Batch(host) + Batch.emit_list/emit_bitmap(host)")
             + ("; N > 1 bitmaps: shard.distribute_segments (1/N H2D + NCCL all-gather)"
                if kind == "slab" and world > 1 else "")}
 

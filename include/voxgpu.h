@@ -109,9 +109,20 @@ VXG_API vxg_status vxg_make_plans(vxg_context* ctx, const vxg_segment* segs, int
  * `out` (capacity `cap` voxels; N+1 always suffices), its length to *count. A chain longer than
  * `cap` -> LOGIC_ERROR with the true length in *count and the first `cap` voxels written.
  * Chains up to 2^14 samples take one launch and one synchronisation (single_chain_kernel, the
- * latency regime); longer ones the batch passes. */
+ * latency regime); longer ones up to 2^30 one multi-CTA launch into device memory and a copy
+ * back (long_chain_kernel); longer still the batch passes. */
 VXG_API vxg_status vxg_voxelize_parametric(vxg_context* ctx, const vxg_segment* seg,
                                            vxg_voxel* out, int64_t cap, int64_t* count);
+/* voxelize_parametric (src/parametric.cpp:28-40) into DEVICE memory: the segment (host memory,
+ * passed as launch arguments) is planned and voxelized by one launch over as many CTAs as its
+ * length asks for (long_chain_kernel; chains beyond 2^30 samples take the batch passes), then
+ * one readback of the count. At most `cap` voxels are written; a longer chain -> LOGIC_ERROR
+ * with *count set to its length. */
+VXG_API vxg_status vxg_voxelize_parametric_device(vxg_context* ctx, const vxg_segment* seg,
+                                                  vxg_voxel* d_out, int64_t cap, int64_t* count);
+/* GPU time (CUDA events) of the last long_chain_kernel launch on this context (kernel_ns; the
+ * other fields 0; all 0 before the first). */
+VXG_API vxg_status vxg_voxelize_parametric_timing(vxg_context* ctx, vxg_timing* t);
 /* chain_length_bounds (src/parametric.cpp:42-50). */
 VXG_API vxg_status vxg_chain_length_bounds(vxg_context* ctx, const vxg_segment* seg,
                                            int64_t* lo, int64_t* hi);

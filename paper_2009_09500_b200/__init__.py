@@ -11,7 +11,8 @@ from .api import (Batch, BatchPlan, batch_preprocess, batch_voxelize, chain_leng
                   compute_mvps, effective_item_count, gen_arbitrary_batch, gen_segment_of_length,
                   gen_segments, kernel_work_item, make_plan, pinned_empty, round_point, run_batch,
                   run_batch_flat, run_batch_device, run_batch_device_result, segment_length,
-                  voxelize_bitmap, voxelize_parametric,
+                  voxelize_bitmap, voxelize_parametric, voxelize_parametric_device,
+                  voxelize_parametric_host, voxelize_parametric_kernel_ns,
                   read_segments_csv, write_chains, batch_to_file)
 from ._lib import IoError
 
@@ -22,7 +23,8 @@ __all__ = [
     "Batch", "run_batch_flat", "voxelize_bitmap", "gen_segments", "pinned_empty", "Context",
     "default_context", "VoxGpuError", "InvalidArgument", "RangeError", "OutOfRange", "LogicError",
     "CudaError", "IoError", "read_segments_csv", "write_chains", "batch_to_file",
-    "run_batch_device", "run_batch_device_result",
+    "run_batch_device", "run_batch_device_result", "voxelize_parametric_device",
+    "voxelize_parametric_host", "voxelize_parametric_kernel_ns",
 ]
 
 

@@ -109,6 +109,8 @@ SIGNATURES = {
     "vxg_segment_lengths": (C.c_int, [_vp, _vp, _i64, _vp]),
     "vxg_make_plans": (C.c_int, [_vp, _vp, _i64, _vp, _vp]),
     "vxg_voxelize_parametric": (C.c_int, [_vp, _vp, _vp, _i64, _i64p]),
+    "vxg_voxelize_parametric_device": (C.c_int, [_vp, _vp, _vp, _i64, _i64p]),
+    "vxg_voxelize_parametric_timing": (C.c_int, [_vp, C.POINTER(vxg_timing)]),
     "vxg_chain_length_bounds": (C.c_int, [_vp, _vp, _i64p, _i64p]),
     "vxg_batch_create": (C.c_int, [_vp, _vp, _i64, C.c_int, C.POINTER(_vp)]),
     "vxg_batch_set_slab": (C.c_int, [_vp, _i64, _i64]),

@@ -129,7 +129,11 @@ def make_plan(start, end):
 
 def _voxelize_one(seg: np.ndarray) -> np.ndarray:
     ctx = default_context()
-    cap = 4096
+    d = np.asarray(seg[3:6], dtype=np.float64) - np.asarray(seg[0:3], dtype=np.float64)
+    with np.errstate(all="ignore"):
+        bound = max(float(np.sqrt(np.dot(d, d))), float(np.max(np.abs(d)))) + 5.0
+    # (N + 1 <= bound: one call; otherwise the count of the first call sizes the second)
+    cap = int(bound) if np.isfinite(bound) and bound < 2 ** 31 else 4096
     while True:
         out = np.zeros((cap, 3), np.int32)
         cnt = C.c_int64()
@@ -144,6 +148,40 @@ def _voxelize_one(seg: np.ndarray) -> np.ndarray:
 def voxelize_parametric(start, end) -> list:
     """Sample-and-round chain of one segment (src/parametric.cpp:28-40) as a list of tuples."""
     return [tuple(v) for v in _voxelize_one(_one_segment(start, end)).tolist()]
+
+
+def voxelize_parametric_device(seg, out_ptr: int, cap: int, ctx=None) -> int:
+    """voxelize_parametric (src/parametric.cpp:28-40) into device memory: `seg` is one segment
+    (sx, sy, sz, ex, ey, ez) in host memory, at most `cap` voxels (3 x int32 each) go to the
+    device address `out_ptr`; returns the chain's length (vxg_voxelize_parametric_device: one
+    launch and one readback). A chain longer than `cap` raises LogicError."""
+    ctx = ctx or default_context()
+    s = np.ascontiguousarray(np.asarray(seg, dtype=np.float64).reshape(6))
+    cnt = C.c_int64()
+    ctx.check(ctx.lib.vxg_voxelize_parametric_device(ctx.h, _ptr(s), C.c_void_p(out_ptr), cap,
+                                                     C.byref(cnt)))
+    return cnt.value
+
+
+def voxelize_parametric_host(seg, out: np.ndarray, ctx=None) -> int:
+    """voxelize_parametric (src/parametric.cpp:28-40) into a caller's host buffer: `out` is a
+    C-contiguous (cap, 3) int32 array (pinned memory makes the copy back direct); returns the
+    chain's length. A chain longer than cap raises LogicError."""
+    ctx = ctx or default_context()
+    _check_host_buffer(out, np.int32, "out", 0, (3,))
+    s = np.ascontiguousarray(np.asarray(seg, dtype=np.float64).reshape(6))
+    cnt = C.c_int64()
+    ctx.check(ctx.lib.vxg_voxelize_parametric(ctx.h, _ptr(s), _ptr(out), out.shape[0],
+                                              C.byref(cnt)))
+    return cnt.value
+
+
+def voxelize_parametric_kernel_ns(ctx=None) -> int:
+    """GPU time (ns) of the last voxelize_parametric_device launch on the context."""
+    ctx = ctx or default_context()
+    t = _lib.vxg_timing()
+    ctx.check(ctx.lib.vxg_voxelize_parametric_timing(ctx.h, C.byref(t)))
+    return t.kernel_ns
 
 
 def chain_length_bounds(start, end):

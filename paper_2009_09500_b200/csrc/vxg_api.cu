@@ -110,6 +110,8 @@ struct vxg_context {
     int32_t* h_single = nullptr;
     Control* h_single_ctl = nullptr;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t lev[2] = {nullptr, nullptr};  // the last long_chain_kernel launch (created on use)
+    bool lev_set = false;
     // one-launch small-batch path (vxg_run_batch_device): look-back words, control block, the
     // last asynchronous call's arguments (re-routed to the multi-pass path if needed)
     struct SmallState;
@@ -830,6 +832,8 @@ VXG_API void vxg_destroy(vxg_context* ctx) {
     if (ctx->h_single) cudaFreeHost(ctx->h_single);
     for (cudaEvent_t e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->lev)
+        if (e) cudaEventDestroy(e);
     delete ctx;
 }
 
@@ -978,6 +982,53 @@ bool single_chain(vxg_context* ctx, const vxg_segment* seg, vxg_voxel* out, int6
     return true;
 }
 
+// Longer chains (up to kLongMaxSamples): one launch of long_chain_kernel over as many CTAs as the
+// host-side bound on N + 1 asks for, writing at most `cap` voxels to device memory, then one
+// readback of the control block. Returns false when the segment is too long or non-finite (or the
+// look-back words cannot be allocated): the caller takes the batch path.
+constexpr double kLongMaxSamples = (double)(1ll << 30);
+
+bool long_chain(vxg_context* ctx, const vxg_segment* seg, int32_t* d_out, int64_t cap,
+                int64_t* count, vxg_status* st) {
+    const double dx = seg->ex - seg->sx, dy = seg->ey - seg->sy, dz = seg->ez - seg->sz;
+    const double ext = std::max(std::fabs(dx), std::max(std::fabs(dy), std::fabs(dz)));
+    const double bound = std::max(std::sqrt(dx * dx + dy * dy + dz * dz), ext) + 4.0;  // (as above)
+    if (!(bound < kLongMaxSamples)) return false;
+    const long long per = vxg::long_chain_samples_per_cta();
+    const long long ctas = (long long)bound / per + 1;
+    DBuf buf;
+    const size_t bytes = sizeof(Control) + sizeof(unsigned long long) * (size_t)ctas;
+    if (!buf.ensure(ctx, bytes)) return false;
+    Control* d_ctl = buf.as<Control>();
+    cudaMemsetAsync(buf.p, 0, bytes, ctx->stream);
+    vxg::LongArgs a{{seg->sx, seg->sy, seg->sz, seg->ex, seg->ey, seg->ez}, cap, ctas * per, d_out,
+                    reinterpret_cast<unsigned long long*>(d_ctl + 1), d_ctl};
+    if (!ctx->lev[0] && (cudaEventCreate(&ctx->lev[0]) != cudaSuccess ||
+                         cudaEventCreate(&ctx->lev[1]) != cudaSuccess))
+        return false;
+    cudaEventRecord(ctx->lev[0], ctx->stream);
+    cudaError_t e = vxg::launch_long_chain(a, ctas, ctx->stream);
+    cudaEventRecord(ctx->lev[1], ctx->stream);
+    ctx->lev_set = true;
+    ctx->launches++;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->h_ctl, d_ctl, sizeof(Control), cudaMemcpyDeviceToHost,
+                                              ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+        *st = ctx->cuda_fail(e, "voxelize_parametric");
+        return true;
+    }
+    const Control c = *ctx->h_ctl;
+    if (c.n_entries != 0) return false;  // longer than the bound: batch path
+    *st = ctl_status(ctx, c, "voxelize_parametric");
+    if (*st) return true;
+    *count = c.total;
+    if (c.total > cap)
+        *st = ctx->fail(VXG_LOGIC_ERROR, 0, "voxelize_parametric: chain of %lld voxels exceeds cap %lld",
+                        (long long)c.total, (long long)cap);
+    return true;
+}
+
 VXG_API vxg_status vxg_voxelize_parametric(vxg_context* ctx, const vxg_segment* seg,
                                            vxg_voxel* out, int64_t cap, int64_t* count) {
     if (!ctx || !seg || !count || cap < 0 || (cap > 0 && !out)) return VXG_INVALID_ARGUMENT;
@@ -986,6 +1037,30 @@ VXG_API vxg_status vxg_voxelize_parametric(vxg_context* ctx, const vxg_segment* 
     if (!std::getenv("VXG_NO_SINGLE")) {
         vxg_status st = VXG_OK;
         if (single_chain(ctx, seg, out, cap, count, &st)) return st;
+        // a long chain: one launch into device memory, then its voxels come back
+        const double dx = seg->ex - seg->sx, dy = seg->ey - seg->sy, dz = seg->ez - seg->sz;
+        const double bound = std::max(std::sqrt(dx * dx + dy * dy + dz * dz),
+                                      std::max(std::fabs(dx), std::max(std::fabs(dy), std::fabs(dz)))) + 4.0;
+        DBuf dout;
+        const int64_t dcap = bound < kLongMaxSamples ? std::min<int64_t>(cap, (int64_t)bound + 1) : 0;
+        int64_t total = 0;
+        if (dcap >= 0 && bound < kLongMaxSamples && dout.ensure(ctx, 12 * (size_t)std::max<int64_t>(dcap, 1)) &&
+            long_chain(ctx, seg, dout.as<int32_t>(), dcap, &total, &st)) {
+            if (st && st != VXG_LOGIC_ERROR) return st;  // (a plan / range error: nothing to copy)
+            if (st) st = VXG_OK, ctx->ok();             // (total > dcap: decided against cap below)
+            *count = total;
+            const int64_t ncopy = std::min(total, cap);
+            if (ncopy > 0) {
+                cudaError_t e = cudaMemcpyAsync(out, dout.p, 12 * (size_t)ncopy, cudaMemcpyDeviceToHost,
+                                                ctx->stream);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+                if (e != cudaSuccess) return ctx->cuda_fail(e, "voxelize_parametric readback");
+            }
+            if (total > cap)
+                return ctx->fail(VXG_LOGIC_ERROR, 0, "voxelize_parametric: chain of %lld voxels exceeds cap %lld",
+                                 (long long)total, (long long)cap);
+            return VXG_OK;
+        }
     }
     vxg_batch* b = nullptr;
     vxg_status s = vxg_batch_create(ctx, seg, 1, VXG_MEM_HOST, &b);
@@ -1015,6 +1090,39 @@ VXG_API vxg_status vxg_voxelize_parametric(vxg_context* ctx, const vxg_segment* 
     }
     vxg_batch_destroy(b);
     return s;
+}
+
+VXG_API vxg_status vxg_voxelize_parametric_device(vxg_context* ctx, const vxg_segment* seg,
+                                                  vxg_voxel* d_out, int64_t cap, int64_t* count) {
+    if (!ctx || !seg || !count || cap < 0 || (cap > 0 && !d_out)) return VXG_INVALID_ARGUMENT;
+    if ((reinterpret_cast<uintptr_t>(d_out) & 3u) != 0)
+        return ctx->fail(VXG_INVALID_ARGUMENT, -1, "voxelize_parametric: output must be 4-byte aligned");
+    ctx->ok();
+    cudaSetDevice(ctx->device);
+    vxg_status st = VXG_OK;
+    if (long_chain(ctx, seg, reinterpret_cast<int32_t*>(d_out), cap, count, &st)) return st;
+    // (too long for one launch: the batch passes, straight into the caller's buffer)
+    vxg_batch* b = nullptr;
+    vxg_status s = vxg_batch_create(ctx, seg, 1, VXG_MEM_HOST, &b);
+    if (!s) s = plan_ready(b);
+    DBuf chain;
+    if (!s && !chain.ensure(ctx, 16)) s = ctx->fail(VXG_OUT_OF_MEMORY, -1, "voxelize_parametric: out of device memory");
+    int64_t total = 0;
+    if (!s) s = emit_list_device(b, reinterpret_cast<int32_t*>(d_out), cap, chain.as<long long>(), &total);
+    if (!s) *count = total;
+    vxg_batch_destroy(b);
+    return s;
+}
+
+VXG_API vxg_status vxg_voxelize_parametric_timing(vxg_context* ctx, vxg_timing* t) {
+    if (!ctx || !t) return VXG_INVALID_ARGUMENT;
+    *t = vxg_timing{0, 0, 0};
+    if (!ctx->lev_set) return VXG_OK;
+    float ms = 0.f;
+    const cudaError_t e = cudaEventElapsedTime(&ms, ctx->lev[0], ctx->lev[1]);
+    if (e != cudaSuccess) return ctx->cuda_fail(e, "voxelize_parametric_timing");
+    t->kernel_ns = (int64_t)((double)ms * 1e6);
+    return VXG_OK;
 }
 
 VXG_API vxg_status vxg_chain_length_bounds(vxg_context* ctx, const vxg_segment* seg, int64_t* lo,

@@ -940,6 +940,186 @@ cudaError_t launch_single_chain(const SingleArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// voxelize_parametric of one long chain in one launch (the batch path's plan readback + count /
+// scan / emit launches dominate a single segment's ~10 us of work). CTA t (claimed in order)
+// takes samples [t * 8192, (t + 1) * 8192): thread 0 plans the segment (make_plan,
+// src/parametric.cpp:8-26) into shared memory, each thread evaluates its kLongP samples (1024
+// apart) once and holds the voxels in registers; a sample is kept when it is k = 0 or its voxel
+// differs from its predecessor's (src/batch.cpp:139-142) -- the lane before (shuffle), the last
+// lane of the warp before / the row before (shared memory), or, for the CTA's first sample, the
+// voxel thread 0 evaluates for it. The CTA's count goes through the decoupled look-back (one
+// window: 123 CTAs for 10^6 samples), then the kept voxels are written in order.
+constexpr int kLongThreads = 1024, kLongP = 8, kLongWarps = kLongThreads / 32;
+constexpr int kLongGroups = kLongP * kLongWarps;  // (row, warp) groups, scanned 8 per lane
+static_assert(kLongGroups == 256, "the offsets scan below takes 8 groups per lane");
+
+__global__ void __launch_bounds__(kLongThreads) long_chain_kernel(LongArgs a) {
+    __shared__ int s_off[kLongGroups];    // kept voxels per (row p, warp), then offsets
+    __shared__ int s_last[kLongGroups][3];  // voxel of each group's last lane
+    __shared__ int s_prev[3];               // voxel of the sample before the CTA's first
+    __shared__ SegRec s_rec;
+    __shared__ long long s_tile, s_pre, s_n;
+    __shared__ int s_ok, s_agg;
+    extern __shared__ __align__(16) uint32_t s_stage[];  // the CTA's output: 3 * 8192 + 4 words
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        s_tile = (long long)atomicAdd(&a.ctl->tile_counter, 1ull);
+        Plan pl;
+        s_ok = make_plan(a.seg[0], a.seg[1], a.seg[2], a.seg[3], a.seg[4], a.seg[5], pl);
+        SegRec r;
+        r.sx = a.seg[0];
+        r.sy = a.seg[1];
+        r.sz = a.seg[2];
+        r.wx = pl.wx;
+        r.wy = pl.wy;
+        r.wz = pl.wz;
+        r.ex = pl.ex;
+        r.ey = pl.ey;
+        r.ez = pl.ez;
+        r.flags = rec_flags(a.seg[0], a.seg[1], a.seg[2], a.seg[3], a.seg[4], a.seg[5]);
+        s_rec = r;
+        s_n = pl.n;
+    }
+    __syncthreads();
+    const long long tile = s_tile;
+    if (!s_ok) {
+        if (tid == 0 && tile == 0) record_error(a.ctl, 0, 2);
+        return;
+    }
+    const long long N = s_n, samples = N + 1;
+    if (samples > a.max_samples) {  // the host's bound was wrong: nothing written, host reroutes
+        if (tid == 0 && tile == 0) a.ctl->n_entries = samples;
+        return;
+    }
+    const SegRec r = s_rec;
+    const long long base = tile * (kLongThreads * kLongP);
+    bool bad = false;
+    if (tid == 0 && base > 0 && base < samples)
+        eval_sample(r, base - 1, N, s_prev[0], s_prev[1], s_prev[2], bad);
+    int32_t vx[kLongP], vy[kLongP], vz[kLongP];
+#pragma unroll
+    for (int p = 0; p < kLongP; ++p) {
+        const long long k = base + p * kLongThreads + tid;
+        vx[p] = vy[p] = vz[p] = 0;
+        if (k < samples) eval_sample(r, k, N, vx[p], vy[p], vz[p], bad);
+        if (lane == 31) {
+            s_last[p * kLongWarps + warp][0] = vx[p];
+            s_last[p * kLongWarps + warp][1] = vy[p];
+            s_last[p * kLongWarps + warp][2] = vz[p];
+        }
+    }
+    if (bad) record_error(a.ctl, 0, 2);
+    __syncthreads();
+    unsigned keep = 0;
+#pragma unroll
+    for (int p = 0; p < kLongP; ++p) {
+        const long long k = base + p * kLongThreads + tid;
+        int32_t px = __shfl_up_sync(0xffffffffu, vx[p], 1);
+        int32_t py = __shfl_up_sync(0xffffffffu, vy[p], 1);
+        int32_t pz = __shfl_up_sync(0xffffffffu, vz[p], 1);
+        if (lane == 0) {  // the group before in sample order, or the CTA's predecessor sample
+            const int g = p * kLongWarps + warp - 1;
+            const int* q = g >= 0 ? s_last[g] : s_prev;
+            px = q[0];
+            py = q[1];
+            pz = q[2];
+        }
+        const bool kp = k < samples && (k == 0 || vx[p] != px || vy[p] != py || vz[p] != pz);
+        keep |= (unsigned)kp << p;
+        const unsigned m = __ballot_sync(0xffffffffu, kp);
+        if (lane == 0) s_off[p * kLongWarps + warp] = __popc(m);
+    }
+    __syncthreads();
+    if (warp == 0) {  // offsets of the groups in sample order; the CTA's look-back
+        int v[8];
+        int sum = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            v[i] = s_off[8 * lane + i];
+            sum += v[i];
+        }
+        int incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        int run = incl - sum;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            s_off[8 * lane + i] = run;
+            run += v[i];
+        }
+        const long long agg = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 0) lookback_publish(a.status, tile, agg);
+        const long long pre = lookback_resolve(a.status, tile, agg, a.ctl);
+        if (lane == 0) {
+            s_pre = pre;
+            s_agg = (int)agg;
+            if (tile == (long long)gridDim.x - 1) {  // the last CTA: the chain's length
+                a.ctl->total = pre + agg;
+                a.ctl->max_steps = (unsigned long long)N;
+            }
+        }
+    }
+    __syncthreads();
+    // The CTA's voxels are one contiguous run of the output: staged in shared memory at the
+    // global address's offset mod 16, the aligned middle leaves in ONE bulk copy (TMA), the head
+    // and tail words through registers (as list_emit_kernel does per warp).
+    const long long pre = s_pre;
+    const long long cnt = max(0ll, min((long long)s_agg, a.cap - pre));  // (ranks past cap: dropped)
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(a.out) + 12ull * (unsigned long long)pre;
+    uint32_t* stage = s_stage + (int)((g0 & 15u) >> 2);  // stage word i <-> global word g0/4 + i
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int p = 0; p < kLongP; ++p) {
+        const bool kp = (keep >> p) & 1u;
+        const unsigned m = __ballot_sync(0xffffffffu, kp);
+        const int rank = s_off[p * kLongWarps + warp] + __popc(m & lt);
+        if (kp && rank < cnt) {
+            uint32_t* d = stage + 3 * rank;
+            d[0] = (uint32_t)vx[p];
+            d[1] = (uint32_t)vy[p];
+            d[2] = (uint32_t)vz[p];
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // STS -> async proxy
+    __syncthreads();
+    const uintptr_t g1 = g0 + 12ull * (unsigned long long)cnt;
+    const uintptr_t a0 = (g0 + 15) & ~(uintptr_t)15, a1 = g1 & ~(uintptr_t)15;
+    if (a1 > a0) {
+        const int hw = (int)((a0 - g0) >> 2), tw = (int)((g1 - a1) >> 2);
+        if (tid == 0) {
+            bulk_store(reinterpret_cast<void*>(a0), stage + hw, (unsigned)(a1 - a0));
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        } else if (tid >= 32 && tid - 32 < hw) {
+            reinterpret_cast<uint32_t*>(g0)[tid - 32] = stage[tid - 32];
+        } else if (tid >= 64 && tid - 64 < tw) {
+            reinterpret_cast<uint32_t*>(a1)[tid - 64] = stage[hw + (int)((a1 - a0) >> 2) + (tid - 64)];
+        }
+    } else if (tid < (int)((g1 - g0) >> 2)) {  // (fewer than 8 words)
+        reinterpret_cast<uint32_t*>(g0)[tid] = stage[tid];
+    }
+}
+
+long long long_chain_samples_per_cta() { return kLongThreads * kLongP; }
+
+cudaError_t launch_long_chain(const LongArgs& a, long long ctas, cudaStream_t s) {
+    constexpr size_t smem = (3 * (size_t)kLongThreads * kLongP + 4) * 4;
+    static bool set_dev[kMaxDevices] = {};
+    const int dev = current_device();
+    {
+        std::lock_guard<std::mutex> g(g_attr_mu);
+        if (!set_dev[dev]) {
+            cudaFuncSetAttribute(long_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            set_dev[dev] = true;
+        }
+    }
+    long_chain_kernel<<<(unsigned)ctas, kLongThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 int bitmap_tile_log2() { return 12; }
 
 cudaError_t launch_emit_bitmap(const BitmapArgs& a, bool clip, cudaStream_t s) {

@@ -64,6 +64,16 @@ struct SingleArgs {          // one segment, one CTA (single_chain_kernel)
     Control* ctl;               // mapped: total, max_steps (= N), err_seg, n_entries (reroute)
 };
 
+struct LongArgs {            // one segment over many CTAs (long_chain_kernel)
+    double seg[6];
+    long long cap;              // voxels `out` can hold (more are counted, not written)
+    long long max_samples;      // samples the grid covers (more: nothing done, host reroutes)
+    int32_t* out;               // 3 int32 per voxel (device)
+    unsigned long long* status; // one look-back word per CTA (zeroed)
+    Control* ctl;               // device: total, max_steps (= N), err_seg, n_entries (reroute),
+                                // tile_counter (zeroed)
+};
+
 struct BitmapArgs {
     const SegRec* rec;
     const ClipEntry* entries;   // CLIP mode only
@@ -137,6 +147,8 @@ cudaError_t launch_list_count(const ListArgs& a, cudaStream_t s);  // count pass
 cudaError_t launch_list_emit(const ListArgs& a, cudaStream_t s);   // emit pass
 cudaError_t launch_list_fused(const ListArgs& a, int num_sms, cudaStream_t s);  // both, overlapped
 cudaError_t launch_single_chain(const SingleArgs& a, cudaStream_t s);
+long long long_chain_samples_per_cta();
+cudaError_t launch_long_chain(const LongArgs& a, long long ctas, cudaStream_t s);
 long long small_tile_count(long long n, int spw);
 int small_spw(long long n, int num_sms);
 cudaError_t launch_list_small(const SmallArgs& a, int num_sms, cudaStream_t s);

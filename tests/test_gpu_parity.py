@@ -168,6 +168,41 @@ def test_single_long_segments(vx, oracle):
         assert np.array_equal(got, oracle.voxelize_parametric(s)), L
 
 
+def test_long_chain_kernel_device_api(vx, oracle, monkeypatch):
+    """voxelize_parametric of chains longer than the one-CTA path (long_chain_kernel: 2048-sample
+    CTAs joined by a decoupled look-back), through the device-output entry point and the host
+    one, against the oracle: lengths straddling the CTA size, ties, negative and descending
+    segments, the int32 edge (checked rounding), the cap contract and the range errors."""
+    import torch
+    cases = [oracle.gen_segment_of_length(L, 91 + L) for L in (1, 2047, 2048, 2049, 4097, 16385,
+                                                               100_000, 1_000_000, 3_000_000)]
+    cases += [np.array(c, dtype=np.float64) for c in (
+        [0.5, 0.5, 0.5, 40000.5, 20000.5, -10000.5],           # ties on every axis
+        [-70000.25, 300.5, -2.5, 10.5, -5000.5, 9000.75],        # negative, descending
+        [2147000000.0, 5.0, -3.0, 2147483647.4, 9.0, 2.0],      # checked rounding at the edge
+        [12.0, 12.0, 12.0, 12.0, 12.0, 50000.0])]               # axis-parallel
+    for s in cases:
+        want = oracle.voxelize_parametric(s)
+        out = torch.zeros((len(want) + 7, 3), dtype=torch.int32, device="cuda")
+        n = vx.voxelize_parametric_device(s, out.data_ptr(), out.shape[0])
+        assert n == len(want), s
+        assert np.array_equal(out[:n].cpu().numpy(), want), s
+        got = np.asarray(vx.voxelize_parametric(s[:3], s[3:]), dtype=np.int32).reshape(-1, 3)
+        assert np.array_equal(got, want), s
+    s = cases[7]  # 10^6 voxels: a short buffer raises, nothing past cap is written
+    out = torch.full((1000, 3), -1, dtype=torch.int32, device="cuda")
+    with pytest.raises(vx.LogicError):
+        vx.voxelize_parametric_device(s, out.data_ptr(), 999)
+    assert (out[999] == -1).all()
+    with pytest.raises(vx.RangeError):
+        vx.voxelize_parametric_device([0.0, np.nan, 0.0, 1.0, 2.0, 3.0], out.data_ptr(), 1000)
+    with pytest.raises(vx.RangeError):
+        vx.voxelize_parametric_device([0.0, 0.0, 0.0, 3e9, 2.0, 3.0], out.data_ptr(), 1000)
+    with pytest.raises(vx.RangeError):  # the samples leave the int32 lattice
+        vx.voxelize_parametric_device([2147483000.0, 0.0, 0.0, 2147483647.6, 1.0, 0.0],
+                                      out.data_ptr(), 1000)
+
+
 def test_single_chain_kernel_matches_batch_path(vx, oracle, monkeypatch):
     """voxelize_parametric's one-launch path (single_chain_kernel: plan + samples + dedup in one
     CTA, chain into mapped pinned memory) == the batch path (VXG_NO_SINGLE) == the oracle, on the
