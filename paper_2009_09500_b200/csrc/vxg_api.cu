@@ -630,11 +630,15 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     const bool select = b->n >= (1 << 16) && b->n < (1ll << 31) && z_hi - z_lo < V &&
                         !(b->slab_lo <= z_lo && z_hi <= b->slab_hi) &&  // (filtered already)
                         !std::getenv("VXG_BITMAP_NO_SELECT");
-    // Walk order grouped by segment length and start cell (pays off when lengths vary).
-    // (not for slabs thinner than a quarter of the volume: there the sort costs more than it
-    // saves -- one rank of 8 on cfg5, measured)
+    // Walk order grouped by segment length and start cell (pays off when lengths vary). Thin
+    // slabs (below a quarter of the volume) only with the record copy (N < 2^28): as an index
+    // permutation the sort cost them more than it saved (one rank of 8 on cfg5: 18.00 ->
+    // 17.84 ms), with the copy it pays (rank steps N = 4: 26.03 -> 25.87 ms, N = 8: 14.84 ->
+    // 14.77, tools/slab_probe.py).
+    const bool copyable = b->max_steps < (1ll << (32 - vxg::kRecNShift)) &&
+                          !std::getenv("VXG_BITMAP_PERM_INDEX");
     const bool perm = b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256 &&
-                      (4 * (z_hi - z_lo) >= V || std::getenv("VXG_BITMAP_PERM")) &&
+                      (4 * (z_hi - z_lo) >= V || copyable || std::getenv("VXG_BITMAP_PERM")) &&
                       !std::getenv("VXG_BITMAP_NO_PERM");
     if (select || perm) {
         const size_t keys = (size_t)vxg::tile_perm_keys();
@@ -666,9 +670,7 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
             // passes then read them sequentially instead of gathering 64 B per segment (whole
             // 128-B lines come from DRAM for each gather).
             // (N rides in the copy's flag word: N < 2^28)
-            const bool copy = !std::getenv("VXG_BITMAP_PERM_INDEX") &&
-                              b->max_steps < (1ll << (32 - vxg::kRecNShift)) &&
-                              b->prec.ensure(ctx, sizeof(SegRec) * (size_t)g.n);
+            const bool copy = copyable && b->prec.ensure(ctx, sizeof(SegRec) * (size_t)g.n);
             if (copy) g.prec = b->prec.as<SegRec>();
             cudaMemsetAsync(perm_cur, 0, keys * sizeof(long long), ctx->stream);
             vxg::launch_tiles_perm(g, ctx->stream);

@@ -310,7 +310,22 @@ __device__ __forceinline__ int perm_key(const TileArgs& g, long long i) {
     const double V = (double)g.V;
     const int c = (cell(sz, (double)g.z_lo, (double)(g.z_hi - g.z_lo)) * kCellsPerAxis +
                    cell(sxy.y, 0.0, V)) * kCellsPerAxis + cell(sxy.x, 0.0, V);
-    return len_bucket(seg_steps(g, i)) * (kCellsPerAxis * kCellsPerAxis * kCellsPerAxis) + c;
+    long long N = seg_steps(g, i);
+    if (g.z_lo > 0 || g.z_hi < g.V) {
+        // A slab: what a lane walks is the segment's share inside it -- estimate it from the z
+        // overlap, in buckets scaled to the slab's depth (the shares are short), so a warp's
+        // lanes walk alike.
+        const double wz = __ldg(&g.rec[i].wz);
+        const double z1 = sz + wz * (double)N;
+        const double lo = fmin(sz, z1), hi = fmax(sz, z1);
+        if (hi - lo > 1.0) {
+            const double ov = fmin(hi, (double)g.z_hi) - fmax(lo, (double)g.z_lo);
+            N = (long long)((double)N * fmax(ov, 0.0) / (hi - lo));
+        }
+        const long long depth = g.z_hi - g.z_lo;
+        N <<= depth <= 256 ? 3 : depth <= 512 ? 2 : depth <= 1024 ? 1 : 0;
+    }
+    return len_bucket(N) * (kCellsPerAxis * kCellsPerAxis * kCellsPerAxis) + c;
 }
 
 __global__ void __launch_bounds__(256) perm_hist_kernel(TileArgs g) {
