@@ -632,9 +632,10 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
                         !std::getenv("VXG_BITMAP_NO_SELECT");
     // Walk order grouped by segment length and start cell (pays off when lengths vary). Thin
     // slabs (below a quarter of the volume) only with the record copy (N < 2^28): as an index
-    // permutation the sort cost them more than it saved (one rank of 8 on cfg5: 18.00 ->
-    // 17.84 ms), with the copy it pays (rank steps N = 4: 26.03 -> 25.87 ms, N = 8: 14.84 ->
-    // 14.77, tools/slab_probe.py).
+    // permutation the sort cost them about what it saved (one rank of 8 on cfg5: 18.00 ->
+    // 17.84 ms); with the copy and the in-slab length key (perm_key) it pays: cfg5 rank steps
+    // N = 4 25.90 -> 24.31 ms, N = 8 14.79 -> 14.22 (tools/slab_probe.py,
+    // profiles/r2_multigpu_s6/).
     const bool copyable = b->max_steps < (1ll << (32 - vxg::kRecNShift)) &&
                           !std::getenv("VXG_BITMAP_PERM_INDEX");
     const bool perm = b->n >= (1 << 16) && b->n < (1ll << 31) && b->max_steps >= 256 &&
