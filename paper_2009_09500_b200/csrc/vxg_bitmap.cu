@@ -506,7 +506,13 @@ __global__ void __launch_bounds__(256) slab_select_kernel(TileArgs g, int* sel,
 // Pass A: pieces per tile, in-volume samples.
 // (256, 3): at most 80 registers, 3 CTAs per SM -- 84 registers round to 88 and leave 2 CTAs,
 // 64 (4 CTAs) spill: cfg5 binning 35.5 / 32.3 / 33.2 ms for 2 / 3 / 4 CTAs (round 2)
-__global__ void __launch_bounds__(256, 3) tiles_count_kernel(TileArgs g) {
+#ifndef VXG_COUNT_MINB
+#define VXG_COUNT_MINB 3
+#endif
+#ifndef VXG_SCATTER_MINB
+#define VXG_SCATTER_MINB 4
+#endif
+__global__ void __launch_bounds__(256, VXG_COUNT_MINB) tiles_count_kernel(TileArgs g) {
     const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     long long inside = 0, inbox = 0;
     if (tix < g.n) {
@@ -630,7 +636,7 @@ __global__ void __launch_bounds__(kScanBlock) tiles_scan_lb_kernel(TileArgs g) {
 // measured slower: 93 registers instead of 77 cost more warps than the overlap gained; cfg5
 // scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3. Batching 4-16 pieces per thread in shared
 // memory and issuing their atomics back to back did not pay either: 19.9 / 20.0 / 21.5 ms.)
-__global__ void __launch_bounds__(256, 4) tiles_scatter_kernel(TileArgs g);
+__global__ void __launch_bounds__(256, VXG_SCATTER_MINB) tiles_scatter_kernel(TileArgs g);
 
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
@@ -865,7 +871,7 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, ui
 // measured slower in round 1: cfg5 scatter 19.8 ms at depth 1, 21.3 at 2, 25.3 at 3. Batching
 // 4-16 pieces per thread in shared memory and issuing their atomics back to back did not pay
 // either: 19.9 / 20.0 / 21.5 ms.)
-__global__ void __launch_bounds__(256, 4) tiles_scatter_kernel(TileArgs g) {
+__global__ void __launch_bounds__(256, VXG_SCATTER_MINB) tiles_scatter_kernel(TileArgs g) {
     const long long tix = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (tix >= g.n) return;
     const long long i = walk_segment(g, tix);
