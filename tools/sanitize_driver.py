@@ -2,8 +2,9 @@
 gpu_sanitize.sh): plan_kernel (look-back offset scan), list_fused_kernel (count/emit task queues +
 look-back), list_small_kernel (per-warp tiles + look-back), tiles_scan_lb_kernel, tiles_fill_kernel
 (shared-memory tile, fixed-point samples with the FP64 redo of near-boundary lanes, streamed
-readback), tiles_count / tiles_scatter (shared-memory walk state), each output checked against
-the oracle."""
+readback), tiles_count / tiles_scatter (shared-memory walk state), perm_scatter (records copied
+into walk order), long_chain_kernel (look-back over CTAs, shared-memory staging + bulk copy),
+each output checked against the oracle."""
 import os
 import sys
 
@@ -45,4 +46,10 @@ o = torch.empty((st, 3), dtype=torch.int32, device="cuda")
 c = torch.empty(ssegs.shape[0] + 1, dtype=torch.int64, device="cuda")
 t = vx.run_batch_device(d.data_ptr(), ssegs.shape[0], o.data_ptr(), st, c.data_ptr())
 assert t == st and np.array_equal(o.cpu().numpy(), so) and np.array_equal(c.cpu().numpy(), sc)
+for seg in (orc.gen_segment_of_length(200_000, 0x5A14),
+            np.array([-7000.5, 300.5, 2.5, 60000.5, -4000.25, 900.0])):  # long chains, ties
+    want = orc.voxelize_parametric(seg)
+    lo = torch.zeros((len(want) + 3, 3), dtype=torch.int32, device="cuda")
+    n = vx.voxelize_parametric_device(seg, lo.data_ptr(), lo.shape[0])
+    assert n == len(want) and np.array_equal(lo[:n].cpu().numpy(), want), "long chain"
 print("sanitize driver ok")
