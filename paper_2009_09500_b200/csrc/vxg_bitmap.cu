@@ -826,7 +826,7 @@ __device__ __forceinline__ bool fx_loop_int(const TileArgs& g, const Piece& pc, 
 // near-boundary test (one predicate carries every sample's test: from the first near sample on,
 // the lane ORs into its spare word and redoes the piece exactly afterwards), the shared address
 // and the reduction (fx_loop_int / fx_loop_dadd above).
-template <int G>
+template <int G, bool LATE_E>
 __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, uint32_t sloc,
                                            uint32_t spare, const Piece& pc, int gl) {
     if (pc.w[3] == kPieceExact) {  // exact-format piece: gather S and W, FP64 samples
@@ -859,6 +859,11 @@ __device__ __forceinline__ void fill_piece(const TileArgs& g, uint32_t sbase, ui
         if (!ok)  // (rare) a sample near a rounding boundary: redo this lane's samples exactly
             fill_exact<G>(g, sbase, seg, (long long)(pc.w[7] & 0xffffffu) + gl, steps);
     }
+    // LATE_E: E's address is computed here, not hoisted above the loop by the compiler, so the
+    // gather's latency hides behind the samples instead of stalling the warp before them (cfg5,
+    // 76 samples per piece: fill 57.30 -> 56.95 ms; with cfg3's ~43-sample pieces the early
+    // form is faster: 1.17 against 1.30 ms)
+    if (LATE_E) asm volatile("" : "+r"(ex), "+r"(ey), "+r"(ez));
     __syncwarp();
     if (hasE && gl == 0)
         red_or_shared(sbase + 4u * (uint32_t)(ez * kSS + ey * kRW + (ex >> 5)), 1u << (ex & 31));
@@ -942,7 +947,7 @@ __device__ __forceinline__ void layer_tile_done(const TileArgs& g, long long tzi
     }
 }
 
-template <int NW, int G, bool STREAM>
+template <int NW, int G, bool STREAM, bool LATE_E>
 __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
     extern __shared__ __align__(16) uint32_t bits[];
     __shared__ long long s_tile[2];
@@ -981,7 +986,7 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
             const long long pn = pb + step + grp;
             Piece nxt{};
             if (pn < p1) nxt = ld_piece(pcs + 2 * pn);
-            fill_piece<G>(g, sbase, sloc, spare, cur, gl);
+            fill_piece<G, LATE_E>(g, sbase, sloc, spare, cur, gl);
             cur = nxt;
         }
         __syncthreads();
@@ -1071,26 +1076,30 @@ void launch_tiles_scatter(const TileArgs& g, cudaStream_t s) {
     if (const char* e = getenv("VXG_FILL_PF")) gg.pf = atoi(e);  // bit 3: exact pieces only
     tiles_scatter_kernel<<<(unsigned)((gg.n + 255) / 256), 256, 0, s>>>(gg);
 }
-template <int NW, int G, bool STREAM>
+template <int NW, int G, bool STREAM, bool LATE_E>
 static cudaError_t launch_fill_nw(const TileArgs& g, int num_sms, cudaStream_t s) {
     const size_t smem = (size_t)(kTileWords + 32) * 4;  // the tile + 32 per-lane spare words
-    cudaFuncSetAttribute(tiles_fill_kernel<NW, G, STREAM>,
+    cudaFuncSetAttribute(tiles_fill_kernel<NW, G, STREAM, LATE_E>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiles_fill_kernel<NW, G, STREAM>, NW * 32,
-                                                  smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiles_fill_kernel<NW, G, STREAM, LATE_E>,
+                                                  NW * 32, smem);
     if (per_sm < 1) per_sm = 1;
     long long grid = (long long)per_sm * num_sms;
     if (grid > g.ntiles) grid = g.ntiles;
-    tiles_fill_kernel<NW, G, STREAM><<<(unsigned)grid, NW * 32, smem, s>>>(g);
+    tiles_fill_kernel<NW, G, STREAM, LATE_E><<<(unsigned)grid, NW * 32, smem, s>>>(g);
     return cudaGetLastError();
 }
 
 template <int G, bool STREAM>
 static cudaError_t launch_fill_gs(const TileArgs& g, int num_sms, cudaStream_t s) {
     // 32 warps per CTA at 64 registers (one CTA per SM: the tile takes the shared memory);
-    // round 2, cfg5 fill: 61.35 ms at 32 warps, 61.45 at 24 (85 registers), 64.1 at 16
-    return launch_fill_nw<32, G, STREAM>(g, num_sms, s);
+    // round 2, cfg5 fill: 61.35 ms at 32 warps, 61.45 at 24 (85 registers), 64.1 at 16.
+    // Pieces of one lane (G = 1) averaging >= 60 samples: E's address after the samples.
+    if constexpr (G == 1) {
+        if (g.late_e) return launch_fill_nw<32, G, STREAM, true>(g, num_sms, s);
+    }
+    return launch_fill_nw<32, G, STREAM, false>(g, num_sms, s);
 }
 
 // (the streamed-readback signalling is a separate instantiation: the plain kernel stays as lean)
@@ -1109,6 +1118,8 @@ cudaError_t launch_tiles_fill(const TileArgs& g, int num_sms, double mean_len, c
     int G = mean_len < 160.0 ? 1 : (mean_len < 320.0 ? 16 : 32);
     if (const char* e = getenv("VXG_FILL_G")) G = atoi(e);
     TileArgs gg = g;
+    gg.late_e = mean_len >= 60.0 ? 1 : 0;
+    if (const char* e = getenv("VXG_FILL_LATE_E")) gg.late_e = atoi(e);
     gg.pf = 1;
     if (const char* e = getenv("VXG_FILL_PF")) gg.pf = atoi(e);
     if (const char* e = getenv("VXG_FILL_ORDER")) {  // "bx,by,bz" (experiments)

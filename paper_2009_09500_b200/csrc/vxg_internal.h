@@ -108,6 +108,7 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     unsigned* layer_done;             // ... and per-layer done flags in mapped host memory, or null
     int bx, by, bz;                   // fill: tiles claimed in blocks of bx x by x bz (0: linear)
     int zero;                         // always 0: a value ptxas cannot see through (fill steps)
+    int late_e;                       // fill: E's shared address computed after the samples
     int pf;                           // fill: record prefetch (bit 0: L1 at step start, bit 1: L2
                                       // at step start, bit 2: L1 before the last samples)
 };
