@@ -282,9 +282,10 @@ __device__ __forceinline__ long long rec_steps(const TileArgs& g, const SegRec& 
     return g.rec_n ? (long long)(r.flags >> kRecNShift) : seg_steps(g, i);
 }
 
-// Walk order: segments grouped by length (8 buckets of N / 256), so the 32 segments a warp walks
-// in lock step have similar piece counts (the warp runs as long as its longest walk), and by
-// coarse start cell (16^3). Swept on cfg5 (binning ms): no sort 41.5; 16^3 cells x {1, 2, 4, 8,
+// Walk order: segments grouped by length (8 buckets of N / 256; on a slab, of the estimated
+// in-slab share, scaled to the slab's depth), so the 32 segments a warp walks in lock step have
+// similar piece counts (the warp runs as long as its longest walk), and by coarse start cell
+// (16^3). The perm pass copies the records into this order (perm_scatter_kernel). Swept on cfg5 (binning ms): no sort 41.5; 16^3 cells x {1, 2, 4, 8,
 // 16, 32} length buckets 41.8, 35.4, 32.6, 32.2, 32.6, 33.5; {1, 4, 8, 12, 32}^3 cells x 32
 // buckets 57.8, 36.2, 33.4, 33.4, 35.5; {20, 24}^3 cells x 16 buckets 32.8, 33.0.
 constexpr int kLenBucketShift = 8;
