@@ -187,7 +187,8 @@ def time_slab_step(vx, shard, ctx, torch, d_segs, n, V, z_lo, z_hi) -> float:
         k = shard.select_slab_segments(ctx, d_segs.data_ptr(), n, z_lo, z_hi, local.data_ptr())
         if k > 0:
             b = vx.Batch(None, ctx=ctx, device_ptr=local.data_ptr(), n=k).set_slab(z_lo, z_hi)
-            b.emit_bitmap_device(words.data_ptr(), V, z_lo, z_hi, True)
+            b.emit_bitmap_device(words.data_ptr(), V, z_lo, z_hi, True,
+                                 overwrite=not os.environ.get("VXG_BENCH_OR"))
             b.close()
         e1.record()
         torch.cuda.synchronize()
@@ -483,7 +484,10 @@ def main():
         if kind in ("list", "single"):
             units = b.emit_list_device(out.data_ptr(), capacity, chain.data_ptr())
         else:
-            b.emit_bitmap_device(words.data_ptr(), V, z_lo, z_hi, clip=True)
+            # (overwrite: the step's bitmap replaces the buffer -- the fill stores every word,
+            # no read of the old ones; VXG_BENCH_OR=1 ORs into the buffer instead)
+            b.emit_bitmap_device(words.data_ptr(), V, z_lo, z_hi, clip=True,
+                                 overwrite=not os.environ.get("VXG_BENCH_OR"))
             units = batch_voxels
         plan_ns, emit_ns, aux_ns = b.gpu_timing()
         b.close()

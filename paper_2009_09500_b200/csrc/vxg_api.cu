@@ -577,9 +577,11 @@ bool layer_stream_setup(vxg_context* ctx, int64_t ntz, LayerStream& ls) {
 }
 
 vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t V, int64_t z_lo,
-                             int64_t z_hi, int64_t* outside, uint64_t* host_words = nullptr) {
+                             int64_t z_hi, int64_t* outside, uint64_t* host_words = nullptr,
+                             bool overwrite = false) {
     vxg_context* ctx = b->ctx;
     vxg::TileArgs g{};
+    g.overwrite = overwrite ? 1 : 0;
     g.rec = b->rec.as<SegRec>();
     g.off = b->off.as<long long>();
     g.n = b->n;
@@ -697,6 +699,7 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
     if (npieces == 0) {
         b->emit_ms = b->aux_ms = 0.f;
         // nothing to fill: the device words (zeroed or uploaded) go back as they are
+        if (overwrite) cudaMemsetAsync(d_words, 0, slab_bytes, ctx->stream);
         return host_words ? plain_readback() : VXG_OK;
     }
     // More pieces than the 32-bit bin cursors count, or than the device holds as 32-B records:
@@ -713,10 +716,11 @@ vxg_status emit_bitmap_tiles(vxg_batch* b, unsigned long long* d_words, int64_t 
         const int64_t zm = z_lo + (g.ntz / 2) * g.tz;
         const int64_t plane_words = V * V / 64;  // (V is a multiple of the tile width)
         ls = LayerStream{};
-        s = emit_bitmap_tiles(b, d_words, V, z_lo, zm, nullptr, host_words);
+        s = emit_bitmap_tiles(b, d_words, V, z_lo, zm, nullptr, host_words, overwrite);
         if (s) return s;
         return emit_bitmap_tiles(b, d_words + (zm - z_lo) * plane_words, V, zm, z_hi, nullptr,
-                                 host_words ? host_words + (zm - z_lo) * plane_words : nullptr);
+                                 host_words ? host_words + (zm - z_lo) * plane_words : nullptr,
+                                 overwrite);
     }
     g.pieces = b->entries.as<uint4>();
     vxg::launch_tiles_scatter(g, ctx->stream);
@@ -776,8 +780,15 @@ bool use_tiles(const vxg_batch* b, int64_t V, int64_t z_lo, int64_t z_hi) {
 }
 
 vxg_status emit_bitmap_device(vxg_batch* b, unsigned long long* d_words, int64_t V, int64_t z_lo,
-                              int64_t z_hi, int clip, int64_t* outside) {
-    if (use_tiles(b, V, z_lo, z_hi)) return emit_bitmap_tiles(b, d_words, V, z_lo, z_hi, outside);
+                              int64_t z_hi, int clip, int64_t* outside, bool overwrite = false) {
+    // overwrite: the tile path stores every word of the slab itself (no memset, no read of the
+    // old words); the global-atomic path ORs into a zeroed buffer
+    if (use_tiles(b, V, z_lo, z_hi))
+        return emit_bitmap_tiles(b, d_words, V, z_lo, z_hi, outside, nullptr, overwrite);
+    if (overwrite) {
+        const size_t nwords = (size_t)((V * V * (z_hi - z_lo) + 63) / 64);
+        cudaMemsetAsync(d_words, 0, 8 * nwords, b->ctx->stream);
+    }
     return emit_bitmap_atomic(b, d_words, V, z_lo, z_hi, clip, outside);
 }
 
@@ -1374,18 +1385,16 @@ VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t 
     const size_t nwords = (size_t)((V * V * (z_hi - z_lo) + 63) / 64);
     const auto t0 = Clock::now();
     if (where == VXG_MEM_DEVICE) {
-        if (overwrite) cudaMemsetAsync(words, 0, 8 * nwords, ctx->stream);
         const vxg_status s = emit_bitmap_device(b, reinterpret_cast<unsigned long long*>(words), V,
-                                                z_lo, z_hi, clip, outside);
+                                                z_lo, z_hi, clip, outside, overwrite);
         b->timing.kernel_ns = ns_since(t0);
         return s;
     }
     DBuf d;
     if (!d.ensure(ctx, 8 * std::max<size_t>(nwords, 1)))
         return ctx->fail(VXG_OUT_OF_MEMORY, -1, "bitmap: out of device memory");
-    if (overwrite)
-        cudaMemsetAsync(d.p, 0, 8 * nwords, ctx->stream);
-    else
+    // (overwrite on the tile path: the fill stores every word itself)
+    if (!overwrite)
         cudaMemcpyAsync(d.p, words, 8 * nwords, cudaMemcpyHostToDevice, ctx->stream);
     // large slabs through the tile path: streamed readback (each finished z-layer of tiles goes
     // over PCIe while the fill continues)
@@ -1393,12 +1402,13 @@ VXG_API vxg_status vxg_batch_emit_bitmap(vxg_batch* b, uint64_t* words, int64_t 
     if (use_tiles(b, V, z_lo, z_hi) && 8 * nwords >= (smin ? std::strtoull(smin, nullptr, 10) : (64ull << 20)) &&
         !std::getenv("VXG_BITMAP_NO_STREAM")) {
         const vxg_status s = emit_bitmap_tiles(b, d.as<unsigned long long>(), V, z_lo, z_hi,
-                                               outside, words);
+                                               outside, words, overwrite);
         b->timing.kernel_ns = ns_since(t0);
         b->timing.assemble_ns = 0;
         return s;
     }
-    vxg_status s = emit_bitmap_device(b, d.as<unsigned long long>(), V, z_lo, z_hi, clip, outside);
+    vxg_status s = emit_bitmap_device(b, d.as<unsigned long long>(), V, z_lo, z_hi, clip, outside,
+                                      overwrite);
     b->timing.kernel_ns = ns_since(t0);
     if (s) return s;
     const auto t1 = Clock::now();

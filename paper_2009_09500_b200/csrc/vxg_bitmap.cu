@@ -966,12 +966,27 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
         const long long tile = fill_tile_of(g, s_tile[it & 1]);
         const long long p0 = __ldg(g.tile_off + tile * kLenClasses),
                         p1 = __ldg(g.tile_off + (tile + 1) * kLenClasses);
-        if (p0 == p1) {  // no samples: the bitmap keeps its words
-            if (STREAM && tid == 0) layer_tile_done(g, tile / (g.ntx * g.nty));
-            continue;
-        }
         const long long txi = tile % g.ntx, tyi = (tile / g.ntx) % g.nty, tzi = tile / (g.ntx * g.nty);
         const int x0 = (int)(txi * kTX), y0 = (int)(tyi * kTY), z0 = (int)(g.z_lo + tzi * kTZ);
+        if (p0 == p1) {  // no samples: the bitmap keeps its words (overwrite: zeros)
+            if (g.overwrite) {
+                const int xw = (int)min((unsigned long long)kTX, V - x0) / 64;
+                for (int r = tid; r < kTY * kTZ * (kRW / 4); r += NW * 32) {
+                    const int half = r % (kRW / 4), row = r / (kRW / 4);
+                    const long long y = y0 + row % kTY, z = z0 + row / kTY;
+                    if (y >= (long long)V || z >= g.z_hi || 2 * half >= xw) continue;
+                    *reinterpret_cast<ulonglong2*>(
+                        g.words + ((((unsigned long long)(z - g.z_lo) * V + y) * V + x0) >> 6) +
+                        2 * half) = make_ulonglong2(0ull, 0ull);
+                }
+                if (STREAM) {
+                    __threadfence();
+                    __syncthreads();
+                }
+            }
+            if (STREAM && tid == 0) layer_tile_done(g, tzi);
+            continue;
+        }
         const int base = z0 * kSS + y0 * kRW + (x0 >> 5);  // (x0 is a multiple of 32)
         const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(bits) - 4u * (uint32_t)base;
         const uint32_t sloc = (uint32_t)__cvta_generic_to_shared(bits);
@@ -1013,13 +1028,14 @@ __global__ void __launch_bounds__(NW * 32) tiles_fill_kernel(TileArgs g) {
                     wb[u] = (unsigned long long)sw[2] | ((unsigned long long)sw[3] << 32);
                     sw[0] = sw[1] = sw[2] = sw[3] = 0u;
                     const long long y = y0 + ly, z = z0 + lz;
-                    if (y >= (long long)V || z >= g.z_hi || 2 * half >= xw || (wa[u] | wb[u]) == 0)
+                    if (y >= (long long)V || z >= g.z_hi || 2 * half >= xw ||
+                        ((wa[u] | wb[u]) == 0 && !g.overwrite))
                         continue;
                     // (rows are 16-B aligned: V and x0 are multiples of 128)
                     dst[u] = reinterpret_cast<ulonglong2*>(
                         g.words + ((((unsigned long long)(z - g.z_lo) * V + y) * V + x0) >> 6) +
                         2 * half);
-                    cur[u] = *dst[u];
+                    cur[u] = g.overwrite ? make_ulonglong2(0ull, 0ull) : *dst[u];
                 }
 #pragma unroll
                 for (int u = 0; u < kBatch; ++u)

@@ -109,6 +109,8 @@ struct TileArgs {  // tile-binned bitmap (vxg_bitmap.cu)
     int bx, by, bz;                   // fill: tiles claimed in blocks of bx x by x bz (0: linear)
     int zero;                         // always 0: a value ptxas cannot see through (fill steps)
     int late_e;                       // fill: E's shared address computed after the samples
+    int overwrite;                    // fill: store the tiles (zeros included), no read of the
+                                      // old words (VXG_BITMAP_OVERWRITE: no memset either)
     int pf;                           // fill: record prefetch (bit 0: L1 at step start, bit 1: L2
                                       // at step start, bit 2: L1 before the last samples)
 };

@@ -41,7 +41,7 @@ def rank_step(z0, z1, reps=3):
         b = vx.Batch(None, ctx=ctx, device_ptr=src.data_ptr(), n=cnt)
         if N > 1:
             b.set_slab(z0, z1)  # (as bench.py: filtered above)
-        b.emit_bitmap_device(words.data_ptr(), V, z0, z1, True)
+        b.emit_bitmap_device(words.data_ptr(), V, z0, z1, True, overwrite=True)  # (as bench.py)
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
