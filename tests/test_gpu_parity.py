@@ -523,8 +523,8 @@ def test_sample_balanced_slabs_on_device(vx):
 
 
 def test_bitmap_overwrite_discards_prior_words(vx, oracle):
-    """VXG_BITMAP_OVERWRITE zeroes the words on the device: garbage in the caller's buffer
-    (host or device) does not survive, on the tile path and on a slab."""
+    """VXG_BITMAP_OVERWRITE replaces the caller's words: garbage in the buffer (host or device)
+    does not survive, on the tile path and on a slab."""
     import torch
     segs = vx.gen_segments(2000, 0, 300, 512, 23)
     b = vx.Batch(segs)
@@ -540,6 +540,44 @@ def test_bitmap_overwrite_discards_prior_words(vx, oracle):
     torch.cuda.synchronize()
     ow, _ = oracle.bitmap(segs, 512)
     assert np.array_equal(d.cpu().numpy().view(np.uint64), ow)
+    b.close()
+
+
+@pytest.mark.parametrize("route", ["plain", "streamed", "split", "atomic"])
+def test_bitmap_overwrite_store_only(vx, oracle, monkeypatch, route):
+    """Overwrite mode on the tile path stores every word of the slab from the fill (empty tiles as
+    zeros; no memset, no read of the old words): junk in host and device buffers never survives --
+    partial tiles (V = 384, 640), slabs cutting tiles, the streamed host readback, the slab split
+    on piece overflow, a batch with no sample in the slab, and the global-atomic path."""
+    import torch
+    if route == "streamed":
+        monkeypatch.setenv("VXG_BITMAP_STREAM_MIN", "0")
+    elif route == "split":  # (whole-volume slabs split; no layer alone holds that many)
+        monkeypatch.setenv("VXG_BITMAP_MAX_PIECES", "4000")
+    elif route == "atomic":
+        monkeypatch.setenv("VXG_BITMAP_ATOMIC", "1")
+    for V in (384, 640):
+        segs = np.concatenate([vx.gen_segments(2000 if route == "split" else 3000, 0, 250, V,
+                                               29 + V),
+                               np.array([[5.0, 5.0, 5.0, 9.0, 7.0, 6.0]])])  # (all in one corner)
+        b = vx.Batch(segs)
+        for z0, z1 in [(0, V), (V // 3, V // 3 + 130), (V - 100, V)]:
+            n = V * V * (z1 - z0) // 64
+            junk = np.full(n, np.uint64(0xF0F0F0F0F0F0F0F0), np.uint64)
+            w, _ = b.emit_bitmap(V, z0, z1, clip=True, words=junk, overwrite=True)
+            ow, _ = oracle.bitmap(segs, V, z0, z1)
+            assert np.array_equal(w, ow), (route, V, z0, z1)
+            d = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+            b.emit_bitmap_device(d.data_ptr(), V, z0, z1, clip=True, overwrite=True)
+            torch.cuda.synchronize()
+            assert np.array_equal(d.cpu().numpy().view(np.uint64), ow), (route, V, z0, z1)
+        b.close()
+    # no sample in the slab at all: the slab comes back as zeros
+    b = vx.Batch(np.array([[1.0, 1.0, 1.0, 20.0, 9.0, 4.0]] * 70000))
+    d = torch.full((384 * 384 * 128 // 64,), -1, dtype=torch.int64, device="cuda")
+    b.emit_bitmap_device(d.data_ptr(), 384, 200, 328, clip=True, overwrite=True)
+    torch.cuda.synchronize()
+    assert int(d.count_nonzero()) == 0
     b.close()
 
 
