@@ -5,7 +5,8 @@
 
 A step is one pass of the hot path over one batch: plan kernel + look-back offset scan
 (batch_preprocess) and the emit (batch_voxelize's kernel + assemble phases), inputs resident in
-HBM. Workloads (BASELINE.json configs; the other configs are `--workload` lines):
+HBM; a bitmap step writes a fresh bitmap of its batch (VXG_BITMAP_OVERWRITE; VXG_BENCH_OR=1
+ORs into the buffer instead). Workloads (BASELINE.json configs; the other configs are `--workload` lines):
   cfg5 (default)  64M segments, N ~ U{1..2048}, 4096^3 bitmap  -> z-slab per rank (strong)
   cfg3            16M segments, N = 64, 1024^3 bitmap          -> z-slab per rank (strong)
   cfg4            4M segments, N ~ U{1..2048}, voxel list      -> one batch cut into sample-
