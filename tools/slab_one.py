@@ -25,7 +25,7 @@ for _ in range(2):
     b = vx.Batch(None, ctx=ctx, device_ptr=(local if N > 1 else d).data_ptr(), n=cnt)
     if N > 1:
         b.set_slab(z0, z1)  # (as bench.py: filtered above)
-    b.emit_bitmap_device(words.data_ptr(), V, z0, z1, True)
+    b.emit_bitmap_device(words.data_ptr(), V, z0, z1, True, overwrite=True)  # (as bench.py)
     b.close()
 torch.cuda.synchronize()
 print(f"slab [{z0}, {z1})")
