@@ -35,6 +35,9 @@ w2, _ = b.emit_bitmap(512, 100, 300, clip=True)                 # slab select + 
 ow2, _ = orc.bitmap(bsegs, 512, 100, 300)
 assert np.array_equal(w2, ow2), "slab bitmap"
 assert b.count_voxels() == orc.run_batch(bsegs)[2], "count"
+junk = np.full(512 ** 3 // 64, np.uint64(0xF0F0F0F0F0F0F0F0), np.uint64)  # overwrite: store-only fill
+w3, _ = b.emit_bitmap(512, 0, 512, words=junk, overwrite=True)
+assert np.array_equal(w3, ow), "overwrite bitmap"
 b.close()
 
 import torch  # noqa: E402  (device buffers for the one-launch path)
