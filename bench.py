@@ -617,7 +617,10 @@ def main():
                        "volume": V, "partition": part,
                        "l2": "inputs+outputs larger than L2 (no flush needed)"
                        if alg_bytes > 2 * L2_BYTES else "L2-resident working set",
-                       "parallelism": f"{cfg['scaling']}-sharded x{world}"},
+                       "parallelism": f"{cfg['scaling']}-sharded x{world}",
+                       **({"bitmap_step": "OR into the buffer" if os.environ.get("VXG_BENCH_OR")
+                           else "fresh bitmap per batch (overwrite: every word stored)"}
+                          if kind == "slab" else {})},
             "segments_per_s": n * (world if kind == "single" else 1) / (ms / 1e3),
             "samples_per_s": total_samples / (ms / 1e3),
             "units": "deduplicated voxels (BatchResult.total_voxels)",
